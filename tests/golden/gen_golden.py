@@ -1,0 +1,133 @@
+"""Generate the golden parity fixtures from the REFERENCE interpreter.
+
+This script is the only place that executes the reference implementation
+(`minigpu.interp.run_program`, /root/reference/pkg/src/minigpu/interp.py:380).
+It runs in the build container, where /root/reference exists; the GPU box never
+reads the reference, it only sees the committed outputs:
+
+    tests/golden/golden.npz      arrays (inputs + reference outputs) per case
+    tests/golden/manifest.json   case list: program, entry, shapes, result
+
+Run:  PYTHONPATH=/root/reference/pkg/src python tests/golden/gen_golden.py
+
+Inputs are handed to the interpreter as Python values (`.tolist()`), never as
+numpy scalars (SURVEY 8c "harness hazard": numpy int32 scalars would wrap).
+"""
+from __future__ import annotations
+
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+REF = os.environ.get("MINIGPU_REF", "/root/reference/pkg/src")
+sys.path.insert(0, REF)
+
+from minigpu.interp import Array, run_program  # noqa: E402  (reference)
+from minigpu.parser import parse_program  # noqa: E402  (reference)
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+PROG = os.path.join(HERE, "programs")
+
+
+def load(name):
+    with open(os.path.join(PROG, name)) as f:
+        return parse_program(f.read(), name)
+
+
+def main():
+    cases = []
+    arrays = {}
+
+    def add(case, **arrs):
+        cid = f"c{len(cases):03d}"
+        case["id"] = cid
+        for k, v in arrs.items():
+            arrays[f"{cid}_{k}"] = v
+        cases.append(case)
+        print(cid, case["kind"], case.get("shape", case.get("n")), case.get("note", ""),
+              f"{case['ref_seconds']:.3f}s", flush=True)
+
+    # ---------------- transposes ----------------
+    def transpose_case(prog_name, H, W, a, cell, note, bits=None):
+        prog = load(prog_name)
+        params = [p for p, _ in prog.fn("transpose").params]
+        pin, pout = params[0], params[1]
+        t0 = time.perf_counter()
+        _, outs = run_program(prog, "transpose", {
+            pin: Array([H, W], a.reshape(-1).tolist(), cell),
+            pout: Array.alloc([W, H], cell), "W": W, "H": H})
+        dt = time.perf_counter() - t0
+        out = np.array(outs[pout], dtype=a.dtype).reshape(W, H)
+        add({"kind": "transpose", "program": prog_name, "shape": [H, W], "cell": cell,
+             "dtype": str(a.dtype), "bits": bits, "note": note, "ref_seconds": dt},
+            inp=a, out=out)
+
+    rng = np.random.default_rng(20260517)
+    idx8 = np.arange(64, dtype=np.float32).reshape(8, 8)
+    transpose_case("transpose_naive.optc", 8, 8, idx8, "float", "SPEC.md:502 8x8 index matrix")
+    for (H, W) in [(1, 1), (1, 17), (17, 1), (33, 65), (64, 96), (7, 128), (129, 31)]:
+        a = rng.uniform(-1, 1, (H, W)).astype(np.float32)
+        transpose_case("transpose_naive.optc", H, W, a, "float", "fp32 U[-1,1)")
+    a = rng.standard_normal((40, 24)).astype(np.float32) * np.float32(1e30)
+    transpose_case("transpose_naive_yx.optc", 40, 24, a, "float", "loops swapped, wide exponents")
+    # bit-pattern transposes through int cells: fp64, bf16, int32
+    f64 = rng.standard_normal((5, 7))
+    transpose_case("transpose_naive_int.optc", 5, 7, f64.view(np.uint64).copy(), "int",
+                   "fp64 bit patterns", bits="f64")
+    bf16 = (rng.standard_normal((33, 65)).astype(np.float32).view(np.uint32) >> 16).astype(np.uint16)
+    transpose_case("transpose_naive_int.optc", 33, 65, bf16, "int", "bf16 bit patterns", bits="bf16")
+    i32 = rng.integers(-2**31, 2**31, (48, 80), dtype=np.int64).astype(np.int32)
+    transpose_case("transpose_naive_int.optc", 48, 80, i32, "int", "int32 full range")
+    for (H, W) in [(32, 32), (64, 96), (96, 64)]:
+        a = rng.uniform(-1, 1, (H, W)).astype(np.float32)
+        transpose_case("transpose_gpu.optc", H, W, a, "float", "GPU form (A.4)")
+
+    # ---------------- reductions ----------------
+    def reduce_case(prog_name, x, note):
+        prog = load(prog_name)
+        t0 = time.perf_counter()
+        ret, _ = run_program(prog, "reduce", {"arr": x.tolist(), "N": int(x.size)})
+        dt = time.perf_counter() - t0
+        if isinstance(ret, float):
+            res = {"result_f32_bits": int(np.float32(ret).view(np.uint32)), "result": ret}
+            assert float(np.float32(ret)) == ret
+        else:
+            res = {"result_int": str(ret), "result": float(ret)}
+        add({"kind": "reduce", "program": prog_name, "n": int(x.size), "dtype": str(x.dtype),
+             "note": note, "ref_seconds": dt, **res}, inp=x)
+
+    reduce_case("reduce_naive_f32.optc", np.arange(1, 13, dtype=np.float32), "SPEC.md:501 [1..12] -> 78")
+    reduce_case("reduce_naive_int.optc", np.arange(1, 13, dtype=np.int32), "SPEC.md:501 [1..12] -> 78")
+    reduce_case("reduce_naive_int.optc", np.full(4, 2**31 - 1, dtype=np.int32), "4 x INT32_MAX, no wrap")
+    reduce_case("reduce_naive_int.optc", np.full(5, -2**31, dtype=np.int32), "5 x INT32_MIN, no wrap")
+    for n in [1, 7, 1000, 4096, 1 << 14]:
+        for dist in ["u01", "um11", "wide"]:
+            if dist == "u01":
+                x = rng.uniform(0, 1, n).astype(np.float32)
+            elif dist == "um11":
+                x = rng.uniform(-1, 1, n).astype(np.float32)
+            else:
+                x = (rng.standard_normal(n) * np.exp2(rng.integers(-20, 20, n))).astype(np.float32)
+            reduce_case("reduce_naive_f32.optc", x, f"fp32 sequential {dist}")
+    for n in [1, 1000, 1 << 14]:
+        x = rng.integers(-2**31, 2**31, n, dtype=np.int64).astype(np.int32)
+        reduce_case("reduce_naive_int.optc", x, "int32 full range")
+    for n in [512, 4096, 1 << 14]:
+        for dist in ["u01", "um11"]:
+            lo = 0.0 if dist == "u01" else -1.0
+            x = rng.uniform(lo, 1, n).astype(np.float32)
+            reduce_case("reduce_tree_f32.optc", x, f"A.5 tree order {dist}")
+
+    np.savez_compressed(os.path.join(HERE, "golden.npz"), **arrays)
+    with open(os.path.join(HERE, "manifest.json"), "w") as f:
+        json.dump({"generator": "tests/golden/gen_golden.py",
+                   "reference": "minigpu.interp.run_program (interp.py:380)",
+                   "cases": cases}, f, indent=1)
+    print(len(cases), "cases written")
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,423 @@
+#!/usr/bin/env python
+"""Benchmark: effective GB/s of the OptiGPU transpose + tree reduction on B200.
+
+One step = one pass of the hot path over one batch of synthetic input:
+  * transpose  fp32 32768 x 32768 (BASELINE config C4: 4 GiB in + 4 GiB out)
+  * reduction  int32 sum over 2^30 elements (config C3: 4 GiB in, int64 result)
+    plus, at N > 1 GPUs, one NCCL reduce of the per-GPU int64 partial.
+Weak scaling (default): every rank owns one row block / shard of that size, so
+the global problem at N GPUs is an (N*32768) x 32768 transpose and an N*2^30
+reduction. `--scaling strong` keeps the global sizes fixed and splits them.
+
+metric value = algorithmic bytes of all ranks / max-over-ranks device time,
+bytes = 2*H*W*4 (transpose) + N*4 + 8 (reduction).
+Inputs (4 GiB each) are larger than the 126 MB L2, so no flush is needed.
+
+`--impl reference` times the reference's CPU path instead (the oracle port of
+minigpu.interp; the reference itself is Python and cannot run at these sizes).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+TILE_ROWS, TILE_COLS = 32768, 32768
+RED_N = 1 << 30
+L2_BYTES = 126 * 1024 * 1024
+FALLBACK_HBM = 6650.0
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--scaling", choices=["weak", "strong"], default="weak")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--paper-configs", action="store_true", default=True)
+    p.add_argument("--rows", type=int, default=TILE_ROWS)
+    p.add_argument("--cols", type=int, default=TILE_COLS)
+    p.add_argument("--n", type=int, default=RED_N)
+    return p.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    except Exception:
+        return FALLBACK_HBM, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def shard_sizes(args, world, rank):
+    """Per-rank transpose rows and reduction elements."""
+    if args.scaling == "weak":
+        return args.rows, args.cols, args.n
+    rows = args.rows // world + (1 if rank < args.rows % world else 0)
+    n = args.n // world + (1 if rank < args.n % world else 0)
+    return rows, args.cols, n
+
+
+def workload_name(args):
+    return (f"C4 fp32 {args.rows}x{args.cols} transpose + C3 int32 2^{int(np.log2(args.n))} "
+            f"sum ({args.scaling} scaling: sizes are per GPU)" if args.scaling == "weak" else
+            f"C4 fp32 {args.rows}x{args.cols} transpose + C3 int32 n={args.n} sum (global)")
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """Polls NVML (SM clock + throttle reasons) in a thread while the GPU works."""
+
+    REASONS = {
+        "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4,
+        "hw_slowdown": 0x8, "sync_boost": 0x10, "sw_thermal_slowdown": 0x20,
+        "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80,
+        "display_clock_setting": 0x100,
+    }
+
+    def __init__(self, dev):
+        self.samples = []
+        self.window = None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(dev)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # pragma: no cover
+            self.nv = None
+            self.err = str(e)
+            self.max_mhz = None
+
+    def start(self):
+        if self.nv is None:
+            return
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.samples.append((time.perf_counter(), sm, rs))
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def stop(self):
+        self._stop.set()
+        if self.nv is not None:
+            self.t.join()
+
+    def summary(self):
+        if self.nv is None:
+            return {"error": getattr(self, "err", "nvml unavailable")}
+        t0, t1 = self.window if self.window else (0, float("inf"))
+        win = [s for s in self.samples if t0 <= s[0] <= t1]
+        use = win if len(win) >= 3 else self.samples
+        mhz = [s[1] for s in use]
+        reasons = set()
+        for _, _, rs in use:
+            for k, bit in self.REASONS.items():
+                if rs & bit and k != "gpu_idle":
+                    reasons.add(k)
+        return {"sm_mhz": statistics.median(mhz) if mhz else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(reasons), "samples": len(use),
+                "window": "timed region" if use is win else "warmup+timed region"}
+
+
+# ----------------------------------------------------------------------------- CPU legs
+def cpu_leg(rows, cols, n, reps=1):
+    """Oracle (C restatement of minigpu.interp) on host cores: GB/s on a bounded sample."""
+    from oracle import oracle
+    threads = oracle.max_threads()
+    a = np.empty((rows, cols), dtype=np.float32)
+    oracle.fill_u32(a.view(np.uint32).reshape(-1), 1)
+    out = np.empty((cols, rows), dtype=np.float32)
+    x = np.empty(n, dtype=np.int32)
+    oracle.fill_u32(x.view(np.uint32), 2)
+    oracle.transpose_into(a[:64], np.empty((cols, 64), np.float32))  # warm the thread pool
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        oracle.transpose_into(a, out)
+        t1 = time.perf_counter()
+        s = oracle.reduce_i32(x)
+        t2 = time.perf_counter()
+        times.append((t1 - t0, t2 - t1))
+    tt = min(t[0] for t in times)
+    tr = min(t[1] for t in times)
+    bytes_ = 2 * rows * cols * 4 + n * 4 + 8
+    assert np.array_equal(out[:5, :7], a[:7, :5].T)
+    return {"value": bytes_ / (tt + tr) / 1e9, "unit": "GB/s", "cores": threads,
+            "transpose_s": tt, "reduce_s": tr, "checksum": s}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from oracle import oracle
+    rows, cols, n = args.rows, args.cols, args.n
+    threads = oracle.max_threads()
+    a = np.empty((rows, cols), dtype=np.float32)
+    oracle.fill_u32(a.view(np.uint32).reshape(-1), 1)
+    out = np.empty((cols, rows), dtype=np.float32)
+    x = np.empty(n, dtype=np.int32)
+    oracle.fill_u32(x.view(np.uint32), 2)
+    bytes_ = 2 * rows * cols * 4 + n * 4 + 8
+    for _ in range(args.warmup):
+        oracle.transpose_into(a, out)
+        oracle.reduce_i32(x)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.transpose_into(a, out)
+        oracle.reduce_i32(x)
+    dt = time.perf_counter() - t0
+    v = bytes_ * args.steps / dt / 1e9
+    sample = (f"full per-GPU workload each step: fp32 {rows}x{cols} transpose + int32 n={n} sum, "
+              f"oracle C port of minigpu.interp (OpenMP, {threads} threads)")
+    line = {
+        "metric": "effective_GBps_transpose_plus_reduce", "value": v, "unit": "GB/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": args.scaling,
+        "vs_baseline": None, "dtype": "f32+i32", "data": "synthetic (splitmix64 bits)",
+        "config": {"workload": workload_name(args), "rows": rows, "cols": cols, "n": n},
+        "impl": "reference",
+        "cpu_baseline": {"value": v, "unit": "GB/s", "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": ("reference = minigpu.interp (pure Python, ~1 MB/s single core; cannot run 12 GiB "
+                 "workloads), timed through its C restatement oracle/oracle.c"),
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_2605_13864_b200 as b2
+    from paper_2605_13864_b200 import ops
+
+    ops.set_host_device(local)
+    dev = torch.device("cuda", local)
+    rows, cols, n = shard_sizes(args, world, rank)
+    g = torch.Generator(device=dev).manual_seed(1234 + rank)
+    a = torch.rand((rows, cols), device=dev, generator=g) * 2 - 1
+    out = torch.empty((cols, rows), device=dev)
+    x = torch.randint(-2**31, 2**31, (n,), device=dev, dtype=torch.int64, generator=g).to(torch.int32)
+    partial = torch.zeros(1, dtype=torch.int64, device=dev)
+    torch.cuda.synchronize()
+
+    st = torch.cuda.current_stream(dev)
+
+    def step(ev=None):
+        if ev is not None:
+            ev[0].record(st)
+        b2.transpose(a, out)
+        if ev is not None:
+            ev[1].record(st)
+        b2.reduce_sum(x, out=partial)
+        if ev is not None:
+            ev[2].record(st)
+        if world > 1:
+            dist.reduce(partial, dst=0)
+
+    # correctness spot checks (cheap, outside the timed region)
+    step()
+    torch.cuda.synchronize()
+    assert torch.equal(out[:64, :64], a[:64, :64].t()) and torch.equal(out[-64:, -64:], a[-64:, -64:].t())
+    if world == 1:
+        assert int(partial.item()) == int(x.to(torch.int64).sum().item())
+
+    clk = ClockSampler(local)
+    clk.start()
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = b2.launch_count()
+    w0 = time.perf_counter()
+    t_start.record(st)
+    for i in range(args.steps):
+        step(evs[i])
+    t_end.record(st)
+    torch.cuda.synchronize()
+    w1 = time.perf_counter()
+    if world > 1:
+        dist.barrier()
+    clk.window = (w0, w1)
+    clk.stop()
+    launches = b2.launch_count() - launches0
+    ms = t_start.elapsed_time(t_end)
+    ms_t = statistics.mean(e[0].elapsed_time(e[1]) for e in evs)
+    ms_r = statistics.mean(e[1].elapsed_time(e[2]) for e in evs)
+    ms_max = ms
+    if world > 1:
+        tt = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms_max = float(tt.item())
+
+    bytes_t = 2 * rows * cols * 4
+    bytes_r = n * 4 + 8
+    tot_rows = rows * world if args.scaling == "weak" else args.rows
+    tot_n = n * world if args.scaling == "weak" else args.n
+    total_bytes = 2 * tot_rows * cols * 4 + tot_n * 4 + 8 * world
+    value = total_bytes * args.steps / (ms_max / 1e3) / 1e9
+    peak, peak_src = peaks()
+    ach_t = bytes_t / (ms_t / 1e3) / 1e9
+    ach_r = bytes_r / (ms_r / 1e3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            prof = json.load(f)
+        traffic = prof.get("transpose", {}).get("dram_bytes_per_launch")
+        traffic_r = prof.get("reduce", {}).get("dram_bytes_per_launch")
+    except Exception:
+        traffic_r = None
+
+    res = {
+        "metric": "effective_GBps_transpose_plus_reduce", "value": value, "unit": "GB/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": args.scaling,
+        "vs_baseline": None, "dtype": "f32+i32", "data": "synthetic (torch.rand / randint on device)",
+        "config": {"workload": workload_name(args), "rows": rows, "cols": cols, "n": n,
+                   "l2": "inputs (4 GiB each) larger than L2 (126 MB): no flush needed",
+                   "combine": "NCCL reduce of the int64 partial" if world > 1 else "none (1 GPU)"},
+        "roofline": {"bound": "hbm", "kernel": "transpose_vec_kernel<4,16,16,256>",
+                     "achieved": ach_t, "peak": peak, "unit": "GB/s", "frac": ach_t / peak,
+                     "traffic": traffic, "algorithmic_bytes": bytes_t, "peak_source": peak_src},
+        "kernels": {
+            "transpose": {"ms": ms_t, "GBps": ach_t, "frac": ach_t / peak, "bytes": bytes_t,
+                          "traffic": traffic},
+            "reduce": {"ms": ms_r, "GBps": ach_r, "frac": ach_r / peak, "bytes": bytes_r,
+                       "traffic": traffic_r},
+        },
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+
+    if not args.no_e2e:
+        res["e2e"] = e2e_leg(b2, a, x, rows, cols, n, args, world, dev)
+    if args.paper_configs and world == 1:
+        res["paper_configs"] = paper_configs(b2, dev)
+    if rank == 0 and world == 1 and not args.no_cpu:
+        c = cpu_leg(min(rows, 8192), cols, min(n, 1 << 28))
+        res["cpu_baseline"] = {
+            "value": c["value"], "unit": "GB/s", "cores": c["cores"], "kind": "port",
+            "sample": (f"oracle C port on fp32 {min(rows, 8192)}x{cols} transpose + int32 "
+                       f"n={min(n, 1 << 28)} sum (best of 1; same byte formula)"),
+        }
+    if world > 1:
+        dist.barrier()
+    if rank == 0:
+        print(json.dumps(res), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def e2e_leg(b2, a, x, rows, cols, n, args, world, dev):
+    """Same step through the host-buffer public API: pinned host inputs, H2D +
+    kernels + D2H inside the timed region (wall clock around the synchronous calls)."""
+    import torch
+    import torch.distributed as dist
+    hin = torch.empty((rows, cols), dtype=torch.float32, pin_memory=True)
+    hout = torch.empty((cols, rows), dtype=torch.float32, pin_memory=True)
+    hx = torch.empty(n, dtype=torch.int32, pin_memory=True)
+    hin.copy_(a)
+    hx.copy_(x)
+    hin_n, hout_n, hx_n = hin.numpy(), hout.numpy(), hx.numpy()
+    steps = max(1, min(args.steps, 5))
+    b2.transpose(hin_n[:256], np.empty((cols, 256), np.float32))  # warm the staging buffers
+    s = b2.reduce_sum(hx_n)
+    for _ in range(1):
+        b2.transpose(hin_n, hout_n)
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        b2.transpose(hin_n, hout_n)
+        s = b2.reduce_sum(hx_n)
+    dt = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([dt], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dt = float(t.item())
+    assert np.array_equal(hout_n[:8, :8], hin_n[:8, :8].T)
+    tot = (2 * rows * cols * 4 + n * 4 + 8) * world
+    return {"value": tot * steps / dt / 1e9, "unit": "GB/s", "steps": steps,
+            "h2d_bytes_per_step": rows * cols * 4 + n * 4,
+            "d2h_bytes_per_step": rows * cols * 4 + 8,
+            "api": "paper_2605_13864_b200.transpose / reduce_sum on pinned numpy host buffers "
+                   "(b2_transpose_host / b2_reduce_sum_host)",
+            "checksum": int(s)}
+
+
+def paper_configs(b2, dev):
+    """PAPER.md Table 7.4 workloads (4096^2 fp32 transpose, 2^24 fp32 sum) with an L2
+    flush between launches, for a like-for-like comparison (RTX 5060 numbers)."""
+    import torch
+    flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device=dev)
+    out = {}
+    a = torch.rand((4096, 4096), device=dev)
+    o = torch.empty_like(a)
+    x = torch.rand(1 << 24, device=dev)
+    r = torch.empty(1, device=dev)
+    for name, fn, bytes_, paper in [
+        ("transpose_4096sq_f32", lambda: b2.transpose(a, o), 2 * 4096 * 4096 * 4, 340.6),
+        ("reduce_2^24_f32", lambda: b2.reduce_sum(x, out=r), (1 << 24) * 4 + 4, 376.8),
+    ]:
+        ts = []
+        for i in range(23):
+            flush.fill_(float(i))
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            torch.cuda.synchronize()
+            if i >= 3:
+                ts.append(e0.elapsed_time(e1))
+        med = statistics.median(ts)
+        out[name] = {"ms_median": med, "GBps": bytes_ / (med / 1e3) / 1e9,
+                     "paper_best_rtx5060_GBps": paper, "l2": "flushed (252 MB write) per launch"}
+    return out
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,125 @@
+/*
+ * b2k.h — C ABI of libb200k.so, the B200 (sm_100a) implementation of the two
+ * OptiGPU hot-path programs: the tiled matrix transpose and the tree reduction.
+ *
+ * The reference (arXiv 2605.13864 artifact, /root/reference/pkg/src/minigpu) is
+ * pure Python and has no FFI of its own: its only executable form of these
+ * programs is the interpreter entry `run_program(program, entry, inputs)`
+ * (interp.py:380-387) walking the DSL loop nests (interp.py:248-309). Each entry
+ * point below replaces the part of that walk cited beside it; the Python package
+ * paper_2605_13864_b200 binds them with ctypes behind a run_program-compatible
+ * API (INTEGRATION.md shows the binding a minigpu maintainer would add).
+ *
+ * Conventions
+ *   - Plain pointers and sizes only; no C++ or torch types cross this boundary.
+ *   - "dev" functions take DEVICE pointers owned by the caller and a cudaStream_t
+ *     passed as void* (NULL = legacy default stream). They are asynchronous.
+ *   - "host" functions take HOST pointers (pinned or pageable), stage through
+ *     library-owned device buffers with overlapped H2D / kernel / D2H, and return
+ *     after the result is in host memory.
+ *   - Sizes and pitches are in ELEMENTS, 64-bit. Return 0 on success, a B2_ERR_*
+ *     code otherwise; b2_last_error() gives the calling thread's message.
+ *   - The library never frees caller memory and never falls back to the CPU.
+ */
+#ifndef B2K_H
+#define B2K_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define B2K_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define B2_API __attribute__((visibility("default")))
+#else
+#define B2_API
+#endif
+
+/* element types (interp cells are binary32 `float` or `int`, intrinsics.py:35;
+ * bf16 / fp64 / 64-bit ints are carried as bit patterns) */
+enum b2_dtype {
+    B2_BF16 = 1,
+    B2_F16 = 2,
+    B2_F32 = 3,
+    B2_F64 = 4,
+    B2_I32 = 5,
+    B2_I64 = 6,
+    B2_U8 = 7,
+    B2_U16 = 8,
+    B2_U32 = 9,
+    B2_U64 = 10
+};
+
+enum b2_status {
+    B2_OK = 0,
+    B2_ERR_INVALID = 1,     /* bad argument (InterpError-class at the Python layer) */
+    B2_ERR_UNSUPPORTED = 2, /* dtype / alignment combination not implemented      */
+    B2_ERR_CUDA = 3,        /* CUDA runtime error (message in b2_last_error)      */
+    B2_ERR_NOMEM = 4        /* device or pinned allocation failed                 */
+};
+
+/* ---- library ------------------------------------------------------------- */
+B2_API int b2_abi_version(void);
+B2_API const char *b2_last_error(void);
+B2_API int b2_device_count(int *count);
+/* Number of kernels this library has launched in this process (evidence for the
+ * bench's gpu_launches claim). */
+B2_API uint64_t b2_launch_count(void);
+B2_API size_t b2_dtype_size(int dtype);
+
+/* ---- transpose ------------------------------------------------------------
+ * out[c][r] = in[r][c] for r < rows, c < cols; in has pitch ld_in, out has pitch
+ * ld_out (elements). Bit-exact permutation for 1/2/4/8-byte elements.
+ * Replaces: interp.py:282-300 executing the DSL nest
+ *   `for x < W { for y < H { out[x][y] = in[y][x]; } }`
+ *   and its GPU form (A.4, PAPER.md:586-618 / 1041-1068), with rows = H, cols = W. */
+B2_API int b2_transpose(const void *in, void *out, int64_t rows, int64_t cols, int64_t ld_in,
+                 int64_t ld_out, int dtype, int dev, void *stream);
+
+/* Host-buffer form of b2_transpose: chunked, copy/compute-overlapped pipeline.
+ * Replaces the host half of A.4: memcpy_host_to_device / device_to_host
+ * (interp.py:353-365) around the kernel_launch scope (interp.py:334-347). */
+B2_API int b2_transpose_host(const void *in_host, void *out_host, int64_t rows, int64_t cols,
+                      int64_t ld_in, int64_t ld_out, int dtype, int dev);
+
+/* ---- reduction ------------------------------------------------------------
+ * Single-pass sum: vectorised grid-stride loads, warp shuffle tree, shared-memory
+ * block tree with __syncthreads, last-block-done grid combine (deterministic).
+ *   dtype B2_F32 -> *out is float   (order differs from the reference's
+ *                                     sequential sum: tolerance, not bits)
+ *   dtype B2_I32 -> *out is int64_t (exact == the reference's unbounded int sum)
+ *   dtype B2_F64 -> *out is double
+ * Replaces: interp.py:282-300 + :262-270 executing `for i < N { sum += arr[i]; }`
+ *   (PAPER.md:155-172).
+ * ws: device workspace of b2_reduce_ws_bytes(n, dtype) bytes, zero-filled before
+ * first use and left zero-filled on return; ws == NULL uses a library-owned
+ * per-device workspace (calls on one device must then be stream-ordered). */
+B2_API size_t b2_reduce_ws_bytes(int64_t n, int dtype);
+B2_API int b2_reduce_sum(const void *in, int64_t n, int dtype, void *out, void *ws, size_t ws_bytes,
+                  int dev, void *stream);
+
+/* Host-buffer form of b2_reduce_sum; *out_host receives float/int64/double. */
+B2_API int b2_reduce_sum_host(const void *in_host, int64_t n, int dtype, void *out_host, int dev);
+
+/* Appendix A.5 order: per 512-element block b,
+ * s[t] = a[2t] + a[2t+1], then s[t] = s[t] + s[t + 2^(7-k)] for k = 0..7;
+ * partials[b] = s[0]. Bit-identical to the reference interpreter's tree form.
+ * Requires 512 | n (exact_div, interp.py:209-214), else B2_ERR_INVALID. */
+B2_API int b2_reduce_tree512_partials(const float *in, int64_t n, float *partials, int dev,
+                               void *stream);
+/* Full A.5 program: partials on the device, memcpy_device_to_host, then the
+ * program's host loop `sum += p[i]` in binary32 (bit-exact with the reference).
+ * `in` is a device pointer; *result_host receives the float. Synchronous. */
+B2_API int b2_reduce_tree512(const float *in, int64_t n, float *result_host, int dev, void *stream);
+
+/* Block until all work this library queued on `stream` of `dev` is done. */
+B2_API int b2_sync(int dev, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* B2K_H */

@@ -1,0 +1,17 @@
+"""B200-native (sm_100a) drop-in for the OptiGPU transpose and tree-reduction
+programs (arXiv 2605.13864; reference package `minigpu`).
+
+Public surface:
+  * `run_program`, `Interp`, `Array`, `InterpError`, `f32`  — the reference's
+    interpreter entry points (minigpu/interp.py:39-387), executing recognised
+    transpose / reduce Programs on the GPU;
+  * `parse_program`, `ParseError`                           — the program
+    grammar (minigpu/parser.py:893) for building those Programs;
+  * `transpose`, `reduce_sum`, `reduce_tree512`              — typed zero-copy
+    entries on CUDA tensors or host arrays.
+"""
+from .ops import reduce_sum, reduce_tree512, reduce_tree512_partials, transpose  # noqa: F401
+from ._lib import B2Error, launch_count  # noqa: F401
+
+__all__ = ["transpose", "reduce_sum", "reduce_tree512", "reduce_tree512_partials", "B2Error",
+           "launch_count"]

@@ -1,0 +1,83 @@
+"""ctypes binding of libb200k.so (include/b2k.h).
+
+There is deliberately no CPU fallback: if the library cannot be loaded, every
+product entry point raises. The .so is built in-tree by `_build.build()`
+(`__graft_entry__.build()` on the driver) so it travels with the repo snapshot.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "libb200k.so")
+
+# enum b2_dtype (include/b2k.h)
+BF16, F16, F32, F64, I32, I64, U8, U16, U32, U64 = 1, 2, 3, 4, 5, 6, 7, 8, 9, 10
+DTYPE_NAMES = {BF16: "bf16", F16: "f16", F32: "f32", F64: "f64", I32: "i32", I64: "i64",
+               U8: "u8", U16: "u16", U32: "u32", U64: "u64"}
+B2_OK, B2_ERR_INVALID, B2_ERR_UNSUPPORTED, B2_ERR_CUDA, B2_ERR_NOMEM = 0, 1, 2, 3, 4
+
+# every symbol include/b2k.h declares: (name, restype, argtypes)
+_i64, _vp, _int, _sz = ctypes.c_int64, ctypes.c_void_p, ctypes.c_int, ctypes.c_size_t
+SIGNATURES = {
+    "b2_abi_version": (_int, []),
+    "b2_last_error": (ctypes.c_char_p, []),
+    "b2_device_count": (_int, [ctypes.POINTER(_int)]),
+    "b2_launch_count": (ctypes.c_uint64, []),
+    "b2_dtype_size": (_sz, [_int]),
+    "b2_transpose": (_int, [_vp, _vp, _i64, _i64, _i64, _i64, _int, _int, _vp]),
+    "b2_transpose_host": (_int, [_vp, _vp, _i64, _i64, _i64, _i64, _int, _int]),
+    "b2_reduce_ws_bytes": (_sz, [_i64, _int]),
+    "b2_reduce_sum": (_int, [_vp, _i64, _int, _vp, _vp, _sz, _int, _vp]),
+    "b2_reduce_sum_host": (_int, [_vp, _i64, _int, _vp, _int]),
+    "b2_reduce_tree512_partials": (_int, [_vp, _i64, _vp, _int, _vp]),
+    "b2_reduce_tree512": (_int, [_vp, _i64, _vp, _int, _vp]),
+    "b2_sync": (_int, [_int, _vp]),
+}
+
+
+class B2Error(RuntimeError):
+    """A libb200k call failed (code + the library's thread-local message)."""
+
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"libb200k error {code}: {msg}")
+        self.code = code
+        self.msg = msg
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: build it with `python __graft_entry__.py build` "
+                "(there is no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        if L.b2_abi_version() != 1:
+            raise ImportError("libb200k ABI version mismatch")
+        _lib = L
+    return _lib
+
+
+def check(rc: int) -> None:
+    if rc != B2_OK:
+        msg = lib().b2_last_error().decode(errors="replace")
+        raise B2Error(rc, msg)
+
+
+def launch_count() -> int:
+    return int(lib().b2_launch_count())
+
+
+def device_count() -> int:
+    n = ctypes.c_int(0)
+    rc = lib().b2_device_count(ctypes.byref(n))
+    return n.value if rc == B2_OK else 0

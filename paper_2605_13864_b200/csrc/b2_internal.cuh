@@ -1,0 +1,56 @@
+// Internal helpers shared by the sm_100a kernels and the C-ABI layer.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <string>
+
+#include "../../include/b2k.h"
+
+namespace b2 {
+
+// ---- error state (thread-local message, integer codes at the ABI) ----------
+void set_error(const std::string &msg);
+int fail(int code, const std::string &msg);
+int cuda_fail(cudaError_t e, const char *what);
+
+#define B2_CUDA(call)                                  \
+    do {                                               \
+        cudaError_t e_ = (call);                       \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+    } while (0)
+
+extern std::atomic<uint64_t> g_launches;
+inline void count_launch(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+int num_sms(int dev);
+
+// ---- global memory access with explicit cache policy -----------------------
+// Streaming 128-bit load that bypasses L1 (read-once data).
+__device__ __forceinline__ uint4 ldg_stream(const uint4 *p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+// Streaming 128-bit store (evict-first in L2: the output is written once).
+__device__ __forceinline__ void stg_stream(uint4 *p, const uint4 &v) {
+    asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x),
+                 "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+
+// ---- kernel launchers (defined in transpose.cu / reduce.cu) ---------------
+int launch_transpose(const void *in, void *out, int64_t rows, int64_t cols, int64_t ld_in,
+                     int64_t ld_out, int esize, int dev, cudaStream_t st);
+
+size_t reduce_ws_bytes(int64_t n, int dtype, int dev);
+int launch_reduce(const void *in, int64_t n, int dtype, void *out, void *ws, size_t ws_bytes,
+                  int dev, cudaStream_t st);
+int launch_tree512(const float *in, int64_t n, float *partials, int dev, cudaStream_t st);
+
+}  // namespace b2

@@ -1,0 +1,322 @@
+// C ABI of libb200k.so (include/b2k.h): argument validation, per-device context
+// (streams, staging buffers, default reduce workspace), and the host-buffer
+// pipelines that overlap H2D copy, kernel and D2H copy chunk by chunk.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "b2_internal.cuh"
+
+namespace b2 {
+
+static thread_local std::string t_err;
+std::atomic<uint64_t> g_launches{0};
+
+void set_error(const std::string &msg) { t_err = msg; }
+int fail(int code, const std::string &msg) {
+    t_err = msg;
+    return code;
+}
+int cuda_fail(cudaError_t e, const char *what) {
+    t_err = std::string(what) + ": " + cudaGetErrorName(e) + ": " + cudaGetErrorString(e);
+    return e == cudaErrorMemoryAllocation ? B2_ERR_NOMEM : B2_ERR_CUDA;
+}
+
+static int g_sms[64] = {0};
+int num_sms(int dev) {
+    if (dev < 0 || dev >= 64) return 148;
+    if (g_sms[dev] == 0) {
+        int n = 0;
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+            n = 148;
+        g_sms[dev] = n;
+    }
+    return g_sms[dev];
+}
+
+// ---------------------------------------------------------------- device context
+namespace {
+
+constexpr int kStages = 3;
+
+struct DevCtx {
+    std::mutex mu;
+    bool ready = false;
+    cudaStream_t s_h2d = nullptr, s_comp = nullptr, s_d2h = nullptr;
+    cudaEvent_t ev_in[kStages], ev_comp[kStages], ev_out[kStages];
+    void *d_in[kStages] = {nullptr, nullptr, nullptr};
+    void *d_out[kStages] = {nullptr, nullptr, nullptr};
+    size_t stage_bytes = 0;
+    void *ws = nullptr;  // default reduce workspace (zero-filled)
+    size_t ws_bytes = 0;
+    void *d_small = nullptr;  // per-chunk results / tree partials
+    size_t small_bytes = 0;
+    void *h_small = nullptr;  // pinned mirror of d_small
+};
+
+DevCtx g_ctx[64];
+
+int check_dev(int dev) {
+    int n = 0;
+    B2_CUDA(cudaGetDeviceCount(&n));
+    if (dev < 0 || dev >= n || dev >= 64)
+        return fail(B2_ERR_INVALID, "device " + std::to_string(dev) + " out of range (have " +
+                                        std::to_string(n) + ")");
+    B2_CUDA(cudaSetDevice(dev));
+    return B2_OK;
+}
+
+int ctx_init(DevCtx &c, int dev) {
+    if (c.ready) return B2_OK;
+    B2_CUDA(cudaStreamCreateWithFlags(&c.s_h2d, cudaStreamNonBlocking));
+    B2_CUDA(cudaStreamCreateWithFlags(&c.s_comp, cudaStreamNonBlocking));
+    B2_CUDA(cudaStreamCreateWithFlags(&c.s_d2h, cudaStreamNonBlocking));
+    for (int k = 0; k < kStages; ++k) {
+        B2_CUDA(cudaEventCreateWithFlags(&c.ev_in[k], cudaEventDisableTiming));
+        B2_CUDA(cudaEventCreateWithFlags(&c.ev_comp[k], cudaEventDisableTiming));
+        B2_CUDA(cudaEventCreateWithFlags(&c.ev_out[k], cudaEventDisableTiming));
+    }
+    c.ws_bytes = reduce_ws_bytes(0, B2_F64, dev);
+    B2_CUDA(cudaMalloc(&c.ws, c.ws_bytes));
+    B2_CUDA(cudaMemset(c.ws, 0, c.ws_bytes));
+    c.ready = true;
+    return B2_OK;
+}
+
+int ensure_stages(DevCtx &c, size_t bytes) {
+    if (c.stage_bytes >= bytes) return B2_OK;
+    B2_CUDA(cudaStreamSynchronize(c.s_h2d));
+    B2_CUDA(cudaStreamSynchronize(c.s_comp));
+    B2_CUDA(cudaStreamSynchronize(c.s_d2h));
+    for (int k = 0; k < kStages; ++k) {
+        if (c.d_in[k]) cudaFree(c.d_in[k]);
+        if (c.d_out[k]) cudaFree(c.d_out[k]);
+        c.d_in[k] = c.d_out[k] = nullptr;
+    }
+    c.stage_bytes = 0;
+    for (int k = 0; k < kStages; ++k) {
+        B2_CUDA(cudaMalloc(&c.d_in[k], bytes));
+        B2_CUDA(cudaMalloc(&c.d_out[k], bytes));
+    }
+    c.stage_bytes = bytes;
+    return B2_OK;
+}
+
+int ensure_small(DevCtx &c, size_t bytes) {
+    if (c.small_bytes >= bytes) return B2_OK;
+    if (c.d_small) cudaFree(c.d_small);
+    if (c.h_small) cudaFreeHost(c.h_small);
+    c.d_small = c.h_small = nullptr;
+    c.small_bytes = 0;
+    B2_CUDA(cudaMalloc(&c.d_small, bytes));
+    B2_CUDA(cudaMallocHost(&c.h_small, bytes));
+    c.small_bytes = bytes;
+    return B2_OK;
+}
+
+int esize_of(int dtype) { return (int)b2_dtype_size(dtype); }
+
+constexpr size_t kChunkBytes = size_t(256) << 20;  // host-pipeline stage size
+
+}  // namespace
+}  // namespace b2
+
+using namespace b2;
+
+extern "C" {
+
+int b2_abi_version(void) { return B2K_ABI_VERSION; }
+
+const char *b2_last_error(void) { return t_err.c_str(); }
+
+uint64_t b2_launch_count(void) { return g_launches.load(); }
+
+int b2_device_count(int *count) {
+    if (!count) return fail(B2_ERR_INVALID, "count is NULL");
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess) {
+        *count = 0;
+        return cuda_fail(e, "cudaGetDeviceCount");
+    }
+    *count = n;
+    return B2_OK;
+}
+
+size_t b2_dtype_size(int dtype) {
+    switch (dtype) {
+    case B2_U8: return 1;
+    case B2_BF16: case B2_F16: case B2_U16: return 2;
+    case B2_F32: case B2_I32: case B2_U32: return 4;
+    case B2_F64: case B2_I64: case B2_U64: return 8;
+    default: return 0;
+    }
+}
+
+int b2_transpose(const void *in, void *out, int64_t rows, int64_t cols, int64_t ld_in,
+                 int64_t ld_out, int dtype, int dev, void *stream) {
+    const int E = esize_of(dtype);
+    if (!E) return fail(B2_ERR_UNSUPPORTED, "transpose: unknown dtype " + std::to_string(dtype));
+    if (rows < 0 || cols < 0) return fail(B2_ERR_INVALID, "transpose: negative extent");
+    if (rows == 0 || cols == 0) return B2_OK;
+    if (!in || !out) return fail(B2_ERR_INVALID, "transpose: NULL buffer");
+    if (ld_in < cols || ld_out < rows)
+        return fail(B2_ERR_INVALID, "transpose: pitch smaller than row length");
+    if (int rc = check_dev(dev)) return rc;
+    return launch_transpose(in, out, rows, cols, ld_in, ld_out, E, dev, (cudaStream_t)stream);
+}
+
+size_t b2_reduce_ws_bytes(int64_t n, int dtype) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return reduce_ws_bytes(n, dtype, dev);
+}
+
+int b2_reduce_sum(const void *in, int64_t n, int dtype, void *out, void *ws, size_t ws_bytes,
+                  int dev, void *stream) {
+    if (n < 0) return fail(B2_ERR_INVALID, "reduce: negative length");
+    if ((!in && n) || !out) return fail(B2_ERR_INVALID, "reduce: NULL buffer");
+    if (int rc = check_dev(dev)) return rc;
+    if (!ws) {
+        DevCtx &c = g_ctx[dev];
+        std::lock_guard<std::mutex> g(c.mu);
+        if (int rc = ctx_init(c, dev)) return rc;
+        ws = c.ws;
+        ws_bytes = c.ws_bytes;
+    }
+    return launch_reduce(in, n, dtype, out, ws, ws_bytes, dev, (cudaStream_t)stream);
+}
+
+int b2_reduce_tree512_partials(const float *in, int64_t n, float *partials, int dev,
+                               void *stream) {
+    if (!in || !partials) return fail(B2_ERR_INVALID, "tree512: NULL buffer");
+    if (int rc = check_dev(dev)) return rc;
+    return launch_tree512(in, n, partials, dev, (cudaStream_t)stream);
+}
+
+int b2_reduce_tree512(const float *in, int64_t n, float *result_host, int dev, void *stream) {
+    if (!in || !result_host) return fail(B2_ERR_INVALID, "tree512: NULL buffer");
+    if (n <= 0 || n % 512)
+        return fail(B2_ERR_INVALID, "exact_div(" + std::to_string(n) + ", 512) is not exact");
+    if (int rc = check_dev(dev)) return rc;
+    DevCtx &c = g_ctx[dev];
+    std::lock_guard<std::mutex> g(c.mu);
+    if (int rc = ctx_init(c, dev)) return rc;
+    const int64_t nb = n / 512;
+    if (int rc = ensure_small(c, (size_t)nb * sizeof(float))) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (int rc = launch_tree512(in, n, (float *)c.d_small, dev, st)) return rc;
+    B2_CUDA(cudaMemcpyAsync(c.h_small, c.d_small, nb * sizeof(float), cudaMemcpyDeviceToHost, st));
+    B2_CUDA(cudaStreamSynchronize(st));
+    // The A.5 program's host loop: `sum += p[i]` in binary32, i ascending.
+    volatile float s = 0.0f;
+    const float *p = (const float *)c.h_small;
+    for (int64_t i = 0; i < nb; ++i) s = s + p[i];
+    *result_host = s;
+    return B2_OK;
+}
+
+int b2_sync(int dev, void *stream) {
+    if (int rc = check_dev(dev)) return rc;
+    B2_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+    return B2_OK;
+}
+
+// ------------------------------------------------------------ host pipelines
+int b2_transpose_host(const void *in_host, void *out_host, int64_t rows, int64_t cols,
+                      int64_t ld_in, int64_t ld_out, int dtype, int dev) {
+    const int E = esize_of(dtype);
+    if (!E) return fail(B2_ERR_UNSUPPORTED, "transpose: unknown dtype " + std::to_string(dtype));
+    if (rows < 0 || cols < 0) return fail(B2_ERR_INVALID, "transpose: negative extent");
+    if (rows == 0 || cols == 0) return B2_OK;
+    if (!in_host || !out_host) return fail(B2_ERR_INVALID, "transpose: NULL buffer");
+    if (ld_in < cols || ld_out < rows)
+        return fail(B2_ERR_INVALID, "transpose: pitch smaller than row length");
+    if (int rc = check_dev(dev)) return rc;
+    DevCtx &c = g_ctx[dev];
+    std::lock_guard<std::mutex> g(c.mu);
+    if (int rc = ctx_init(c, dev)) return rc;
+    // chunk = a block of input rows -> a column slab of the output
+    const int64_t row_bytes = cols * E;
+    int64_t cr = std::max<int64_t>(1, (int64_t)(kChunkBytes / (size_t)row_bytes));
+    if (cr >= 64) cr -= cr % 64;  // whole tiles per chunk
+    cr = std::min(cr, rows);
+    if (int rc = ensure_stages(c, (size_t)cr * row_bytes)) return rc;
+    const char *hin = (const char *)in_host;
+    char *hout = (char *)out_host;
+    const int64_t nchunks = (rows + cr - 1) / cr;
+    for (int64_t i = 0; i < nchunks; ++i) {
+        const int k = (int)(i % kStages);
+        const int64_t r0 = i * cr, nr = std::min(cr, rows - r0);
+        if (i >= kStages) B2_CUDA(cudaStreamWaitEvent(c.s_h2d, c.ev_comp[k], 0));  // d_in[k] free
+        B2_CUDA(cudaMemcpy2DAsync(c.d_in[k], row_bytes, hin + r0 * ld_in * E, ld_in * E, row_bytes,
+                                  nr, cudaMemcpyHostToDevice, c.s_h2d));
+        B2_CUDA(cudaEventRecord(c.ev_in[k], c.s_h2d));
+        B2_CUDA(cudaStreamWaitEvent(c.s_comp, c.ev_in[k], 0));
+        if (i >= kStages) B2_CUDA(cudaStreamWaitEvent(c.s_comp, c.ev_out[k], 0));  // d_out[k] free
+        if (int rc = launch_transpose(c.d_in[k], c.d_out[k], nr, cols, cols, nr, E, dev, c.s_comp))
+            return rc;
+        B2_CUDA(cudaEventRecord(c.ev_comp[k], c.s_comp));
+        B2_CUDA(cudaStreamWaitEvent(c.s_d2h, c.ev_comp[k], 0));
+        B2_CUDA(cudaMemcpy2DAsync(hout + r0 * E, ld_out * E, c.d_out[k], nr * E, nr * E, cols,
+                                  cudaMemcpyDeviceToHost, c.s_d2h));
+        B2_CUDA(cudaEventRecord(c.ev_out[k], c.s_d2h));
+    }
+    B2_CUDA(cudaStreamSynchronize(c.s_d2h));
+    B2_CUDA(cudaStreamSynchronize(c.s_comp));
+    return B2_OK;
+}
+
+int b2_reduce_sum_host(const void *in_host, int64_t n, int dtype, void *out_host, int dev) {
+    const int E = esize_of(dtype);
+    if (dtype != B2_F32 && dtype != B2_I32 && dtype != B2_F64)
+        return fail(B2_ERR_UNSUPPORTED, "reduce: dtype must be B2_F32, B2_I32 or B2_F64");
+    if (n < 0) return fail(B2_ERR_INVALID, "reduce: negative length");
+    if ((!in_host && n) || !out_host) return fail(B2_ERR_INVALID, "reduce: NULL buffer");
+    if (int rc = check_dev(dev)) return rc;
+    DevCtx &c = g_ctx[dev];
+    std::lock_guard<std::mutex> g(c.mu);
+    if (int rc = ctx_init(c, dev)) return rc;
+    const int64_t ce = std::min<int64_t>(std::max<int64_t>(n, 1), (int64_t)(kChunkBytes / E));
+    if (int rc = ensure_stages(c, (size_t)ce * E)) return rc;
+    const int64_t nchunks = n == 0 ? 1 : (n + ce - 1) / ce;
+    if (int rc = ensure_small(c, (size_t)nchunks * 8)) return rc;
+    const char *hin = (const char *)in_host;
+    for (int64_t i = 0; i < nchunks; ++i) {
+        const int k = (int)(i % kStages);
+        const int64_t e0 = i * ce, ne = std::min(ce, n - e0);
+        if (i >= kStages) B2_CUDA(cudaStreamWaitEvent(c.s_h2d, c.ev_comp[k], 0));
+        if (ne > 0)
+            B2_CUDA(cudaMemcpyAsync(c.d_in[k], hin + e0 * E, ne * E, cudaMemcpyHostToDevice, c.s_h2d));
+        B2_CUDA(cudaEventRecord(c.ev_in[k], c.s_h2d));
+        B2_CUDA(cudaStreamWaitEvent(c.s_comp, c.ev_in[k], 0));
+        if (int rc = launch_reduce(c.d_in[k], std::max<int64_t>(ne, 0), dtype,
+                                   (char *)c.d_small + i * 8, c.ws, c.ws_bytes, dev, c.s_comp))
+            return rc;
+        B2_CUDA(cudaEventRecord(c.ev_comp[k], c.s_comp));
+    }
+    B2_CUDA(cudaMemcpyAsync(c.h_small, c.d_small, nchunks * 8, cudaMemcpyDeviceToHost, c.s_comp));
+    B2_CUDA(cudaStreamSynchronize(c.s_comp));
+    // host combine of the per-chunk partials, chunk order (deterministic)
+    const char *h = (const char *)c.h_small;
+    if (dtype == B2_I32) {
+        long long s = 0;
+        for (int64_t i = 0; i < nchunks; ++i) s += *(const long long *)(h + i * 8);
+        *(long long *)out_host = s;
+    } else if (dtype == B2_F32) {
+        volatile float s = 0.0f;
+        for (int64_t i = 0; i < nchunks; ++i) s = s + *(const float *)(h + i * 8);
+        *(float *)out_host = s;
+    } else {
+        double s = 0.0;
+        for (int64_t i = 0; i < nchunks; ++i) s += *(const double *)(h + i * 8);
+        *(double *)out_host = s;
+    }
+    return B2_OK;
+}
+
+}  // extern "C"

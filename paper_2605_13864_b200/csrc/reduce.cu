@@ -1,0 +1,235 @@
+// Tree-based parallel sum reduction for sm_100a (B200).
+//
+// Replaces the reference interpreter executing the OptiGPU reduce programs
+// (SURVEY A.2/A.3 naive, A.5 tree form).
+//
+// reduce_kernel (the HBM-bound hot path), one launch per reduction:
+//   1. persistent grid (SMs x resident CTAs), 128-bit ld.global.nc grid-stride
+//      loads, U independent loads in flight per thread, per-thread accumulator
+//      (int32 -> int64 so the sum is exact like the reference's Python ints);
+//   2. warp __shfl_down_sync tree;
+//   3. shared-memory block tree over the warp partials with one __syncthreads per
+//      level (the barrier structure the paper verifies);
+//   4. single-pass grid combine: partial -> workspace, __threadfence, atomic
+//      ticket; the last CTA sums the partials in block order (deterministic) and
+//      re-arms the ticket, so the workspace stays zero-filled between calls.
+//
+// tree512_kernel: the A.5 program's exact fp32 evaluation order, bit-identical
+// with the reference interpreter (each warp evaluates one 512-element block's
+// tree in registers: the same DAG of binary32 adds as the smem halving loop).
+#include <algorithm>
+
+#include "b2_internal.cuh"
+
+namespace b2 {
+namespace {
+
+template <typename T>
+struct AccOf;
+template <>
+struct AccOf<float> {
+    using type = float;
+};
+template <>
+struct AccOf<int32_t> {
+    using type = long long;
+};
+template <>
+struct AccOf<double> {
+    using type = double;
+};
+
+template <typename T, typename A>
+__device__ __forceinline__ A vec_sum(const uint4 &v);
+template <>
+__device__ __forceinline__ float vec_sum<float, float>(const uint4 &v) {
+    return (__uint_as_float(v.x) + __uint_as_float(v.y)) +
+           (__uint_as_float(v.z) + __uint_as_float(v.w));
+}
+template <>
+__device__ __forceinline__ long long vec_sum<int32_t, long long>(const uint4 &v) {
+    return ((long long)(int)v.x + (long long)(int)v.y) + ((long long)(int)v.z + (long long)(int)v.w);
+}
+template <>
+__device__ __forceinline__ double vec_sum<double, double>(const uint4 &v) {
+    return __hiloint2double((int)v.y, (int)v.x) + __hiloint2double((int)v.w, (int)v.z);
+}
+
+template <typename A>
+__device__ __forceinline__ A warp_tree(A a) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) a += __shfl_down_sync(0xffffffffu, a, off);
+    return a;
+}
+
+// Warp shuffle tree, then a shared-memory halving tree over the NT/32 warp
+// partials with __syncthreads per level. Result valid in thread 0.
+template <typename A, int NT>
+__device__ __forceinline__ A block_tree(A a, A *sm) {
+    constexpr int NW = NT / 32;
+    a = warp_tree(a);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane == 0) sm[w] = a;
+    __syncthreads();
+#pragma unroll
+    for (int h = NW / 2; h > 0; h >>= 1) {
+        if (threadIdx.x < h) sm[threadIdx.x] = sm[threadIdx.x] + sm[threadIdx.x + h];
+        __syncthreads();
+    }
+    return sm[0];
+}
+
+template <typename T, int NT, int U>
+__global__ void __launch_bounds__(NT)
+    reduce_kernel(const T *__restrict__ in, int64_t head, int64_t nvec, int64_t n,
+                  typename AccOf<T>::type *__restrict__ out,
+                  typename AccOf<T>::type *__restrict__ partials, unsigned *__restrict__ ticket) {
+    using A = typename AccOf<T>::type;
+    constexpr int V = 16 / sizeof(T);
+    __shared__ A sm[NT / 32];
+    __shared__ bool last;
+
+    A acc = A(0);
+    const uint4 *vin = reinterpret_cast<const uint4 *>(in + head);
+    const int64_t stride = (int64_t)gridDim.x * NT;
+    int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x;
+    // main body: U independent 128-bit loads in flight per thread
+    for (; i + (U - 1) * stride < nvec; i += U * stride) {
+        uint4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = ldg_stream(vin + i + u * stride);
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc += vec_sum<T, A>(v[u]);
+    }
+    for (; i < nvec; i += stride) acc += vec_sum<T, A>(ldg_stream(vin + i));
+    // unaligned head and ragged tail (< V elements each)
+    const int64_t g = (int64_t)blockIdx.x * NT + threadIdx.x;
+    const int64_t tail0 = head + nvec * V;
+    if (g < head) acc += A(in[g]);
+    if (g < n - tail0) acc += A(in[tail0 + g]);
+
+    A bsum = block_tree<A, NT>(acc, sm);
+    if (threadIdx.x == 0) {
+        partials[blockIdx.x] = bsum;
+        __threadfence();
+        const unsigned t = atomicAdd(ticket, 1u);
+        last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!last) return;
+    // last CTA: combine the per-CTA partials in block order
+    __threadfence();
+    A a = A(0);
+    for (int j = threadIdx.x; j < (int)gridDim.x; j += NT)
+        a += *reinterpret_cast<volatile A *>(partials + j);
+    __syncthreads();  // sm reuse
+    A total = block_tree<A, NT>(a, sm);
+    if (threadIdx.x == 0) {
+        *out = total;
+        *ticket = 0u;  // re-arm for the next call on this workspace
+    }
+}
+
+// A.5: 512-element blocks, one per warp per iteration. Lane l holds
+// s[l + 32j] (j < 8) = a[2t] + a[2t+1]; levels h = 128, 64, 32 pair registers of
+// the same lane, h = 16..1 pair lanes via shuffles. Same adds, same operands,
+// same order as the interpreter's smem loop -> bit-identical partials.
+template <int NT>
+__global__ void __launch_bounds__(NT)
+    tree512_kernel(const float *__restrict__ in, int64_t nblocks, float *__restrict__ partials) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * NT + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * NT) >> 5;
+    for (int64_t b = warp; b < nblocks; b += nwarps) {
+        const float2 *p = reinterpret_cast<const float2 *>(in + b * 512);
+        float2 v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = __ldg(p + lane + 32 * j);
+        float s[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) s[j] = __fadd_rn(v[j].x, v[j].y);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) s[j] = __fadd_rn(s[j], s[j + 4]);  // h = 128
+#pragma unroll
+        for (int j = 0; j < 2; ++j) s[j] = __fadd_rn(s[j], s[j + 2]);  // h = 64
+        float x = __fadd_rn(s[0], s[1]);                                 // h = 32
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1)                           // h = 16..1
+            x = __fadd_rn(x, __shfl_down_sync(0xffffffffu, x, off));
+        if (lane == 0) partials[b] = x;
+    }
+}
+
+constexpr int kNT = 512;
+constexpr int kU = 4;
+
+template <typename T>
+int grid_for(int dev, int64_t nvec) {
+    static int occ[64] = {0};
+    if (occ[dev] == 0) {
+        int o = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, reduce_kernel<T, kNT, kU>, kNT, 0);
+        occ[dev] = o > 0 ? o : 1;
+    }
+    const int64_t cap = (int64_t)num_sms(dev) * occ[dev];
+    const int64_t need = std::max<int64_t>(1, (nvec + kNT - 1) / kNT);
+    return (int)std::min(cap, need);
+}
+
+int max_grid(int dev) {
+    // upper bound over the instantiations: all use kNT threads
+    return num_sms(dev) * (2048 / kNT);
+}
+
+template <typename T>
+int run_reduce(const void *in_, int64_t n, void *out, void *ws, size_t ws_bytes, int dev,
+               cudaStream_t st) {
+    using A = typename AccOf<T>::type;
+    constexpr int V = 16 / sizeof(T);
+    const T *in = (const T *)in_;
+    int64_t head = (int64_t)(((16 - ((uintptr_t)in & 15)) & 15) / sizeof(T));
+    if ((uintptr_t)in % sizeof(T)) return fail(B2_ERR_INVALID, "reduce: misaligned input");
+    head = std::min<int64_t>(head, n);
+    const int64_t nvec = (n - head) / V;
+    const int grid = grid_for<T>(dev, nvec);
+    const size_t need = (size_t)max_grid(dev) * sizeof(A) + 64;
+    if (ws_bytes < need) return fail(B2_ERR_INVALID, "reduce: workspace too small");
+    unsigned *ticket = (unsigned *)ws;
+    A *partials = (A *)((char *)ws + 64);
+    reduce_kernel<T, kNT, kU><<<grid, kNT, 0, st>>>(in, head, nvec, n, (A *)out, partials, ticket);
+    count_launch();
+    B2_CUDA(cudaGetLastError());
+    return B2_OK;
+}
+
+}  // namespace
+
+size_t reduce_ws_bytes(int64_t, int dtype, int dev) {
+    size_t a = dtype == B2_F32 ? 4 : 8;
+    return (size_t)max_grid(dev) * a + 64;
+}
+
+int launch_reduce(const void *in, int64_t n, int dtype, void *out, void *ws, size_t ws_bytes,
+                  int dev, cudaStream_t st) {
+    switch (dtype) {
+    case B2_F32: return run_reduce<float>(in, n, out, ws, ws_bytes, dev, st);
+    case B2_I32: return run_reduce<int32_t>(in, n, out, ws, ws_bytes, dev, st);
+    case B2_F64: return run_reduce<double>(in, n, out, ws, ws_bytes, dev, st);
+    default: return fail(B2_ERR_UNSUPPORTED, "reduce: dtype must be B2_F32, B2_I32 or B2_F64");
+    }
+}
+
+int launch_tree512(const float *in, int64_t n, float *partials, int dev, cudaStream_t st) {
+    if (n % 512 != 0 || n <= 0)
+        return fail(B2_ERR_INVALID, "exact_div(" + std::to_string(n) + ", 512) is not exact");
+    if ((uintptr_t)in % 8) return fail(B2_ERR_INVALID, "tree512: input must be 8-byte aligned");
+    const int64_t nb = n / 512;
+    constexpr int NT = 256;
+    const int64_t grid = std::min<int64_t>((nb + NT / 32 - 1) / (NT / 32), (int64_t)num_sms(dev) * 8);
+    tree512_kernel<NT><<<(unsigned)grid, NT, 0, st>>>(in, nb, partials);
+    count_launch();
+    B2_CUDA(cudaGetLastError());
+    return B2_OK;
+}
+
+}  // namespace b2

@@ -1,0 +1,259 @@
+// Tiled matrix transpose for sm_100a (B200).
+//
+// Replaces the reference interpreter executing the OptiGPU transpose programs
+// (SURVEY A.1 naive nest and A.4 GPU form): out is
+// the W x H transpose of the H x W input, a pure permutation, bit-exact for every
+// element width.
+//
+// Vector path (16-B aligned pitches, the HBM-bound hot path):
+//   * each thread owns V x V "micro-tiles" (V = 16 / sizeof(elem)): V 128-bit
+//     coalesced loads from V consecutive input rows, an in-register V x V
+//     transpose (PRMT byte permutes for 2-byte cells), then V 128-bit stores into
+//     a shared-memory tile laid out in OUTPUT orientation;
+//   * the shared tile is XOR-swizzled at 16-B granularity (phys = col ^ (row/V)&7)
+//     so both the transposed STS.128 and the row-wise LDS.128 are bank-conflict
+//     free (the B200 equivalent of the paper's +1 padding, without losing 16-B
+//     alignment);
+//   * one __syncthreads between stage-in and stage-out (the barrier the paper's
+//     blocksync() proves), then 128-bit coalesced stores;
+//   * persistent grid (a multiple of the SM count) walking tiles; the next tile's
+//     loads are issued before the current tile's stores so HBM reads and writes
+//     overlap inside every CTA.
+// Scalar path (odd pitches / edge strips): the classic padded 32 x 33 tile.
+#include "b2_internal.cuh"
+
+namespace b2 {
+namespace {
+
+template <int E>
+struct Micro {
+    static constexpr int V = 16 / E;
+};
+
+// In-register V x V transpose of a micro-tile held as V uint4 rows.
+__device__ __forceinline__ void micro_transpose4(uint4 (&v)[4]) {  // 4-byte cells
+    uint4 o[4];
+    o[0] = make_uint4(v[0].x, v[1].x, v[2].x, v[3].x);
+    o[1] = make_uint4(v[0].y, v[1].y, v[2].y, v[3].y);
+    o[2] = make_uint4(v[0].z, v[1].z, v[2].z, v[3].z);
+    o[3] = make_uint4(v[0].w, v[1].w, v[2].w, v[3].w);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[i] = o[i];
+}
+
+__device__ __forceinline__ void micro_transpose8(uint4 (&v)[2]) {  // 8-byte cells
+    uint4 o0 = make_uint4(v[0].x, v[0].y, v[1].x, v[1].y);
+    uint4 o1 = make_uint4(v[0].z, v[0].w, v[1].z, v[1].w);
+    v[0] = o0;
+    v[1] = o1;
+}
+
+__device__ __forceinline__ uint32_t word(const uint4 &v, int i) {
+    return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
+}
+
+__device__ __forceinline__ void micro_transpose2(uint4 (&v)[8]) {  // 2-byte cells
+    // out[j] element k = in[k] element j. Element j of a row lives in word j/2,
+    // half j%2; output word m packs elements (2m, j) and (2m+1, j).
+    uint4 o[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const uint32_t sel = (j & 1) ? 0x7632u : 0x5410u;
+        uint32_t w[4];
+#pragma unroll
+        for (int m = 0; m < 4; ++m)
+            w[m] = __byte_perm(word(v[2 * m], j >> 1), word(v[2 * m + 1], j >> 1), sel);
+        o[j] = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = o[i];
+}
+
+template <int E>
+__device__ __forceinline__ void micro_transpose(uint4 (&v)[16 / E]) {
+    if constexpr (E == 4) micro_transpose4(v);
+    else if constexpr (E == 8) micro_transpose8(v);
+    else micro_transpose2(v);
+}
+
+// Tile = (TRV*V) input rows x (TCV*V) input columns; NT threads; each thread owns
+// MT = TRV*TCV/NT micro-tiles.
+template <int E, int TRV, int TCV, int NT>
+__global__ void __launch_bounds__(NT)
+    transpose_vec_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out,
+                         int64_t rows_v, int64_t cols_v, int64_t ld_in_b, int64_t ld_out_b,
+                         int64_t tiles_c, int64_t ntiles) {
+    constexpr int V = Micro<E>::V;
+    constexpr int TR = TRV * V;  // input rows per tile   (= output vector columns * V)
+    constexpr int TC = TCV * V;  // input cols per tile   (= output rows)
+    constexpr int MT = TRV * TCV / NT;
+    static_assert(MT >= 1 && TRV * TCV % NT == 0, "tile/thread mismatch");
+    static_assert(TRV >= 8 && (TRV & (TRV - 1)) == 0, "swizzle needs >= 8 vector columns");
+    constexpr int ST = TC * TRV / NT;  // 16-B stores per thread per tile
+
+    __shared__ uint4 S[TC * TRV];
+
+    uint4 reg[MT][V];
+
+    auto load_tile = [&](int64_t tile) {
+        const int64_t r0 = (tile / tiles_c) * TR, c0 = (tile % tiles_c) * TC;
+#pragma unroll
+        for (int m = 0; m < MT; ++m) {
+            const int mt = threadIdx.x + m * NT;
+            const int vc = mt % TCV, rg = mt / TCV;
+            const int64_t r = r0 + rg * V, c = c0 + vc * V;
+            if (r < rows_v && c < cols_v) {
+                const uint8_t *p = in + r * ld_in_b + c * E;
+#pragma unroll
+                for (int k = 0; k < V; ++k)
+                    reg[m][k] = ldg_stream(reinterpret_cast<const uint4 *>(p + k * ld_in_b));
+            }
+        }
+    };
+
+    int64_t tile = blockIdx.x;
+    if (tile < ntiles) load_tile(tile);
+    for (; tile < ntiles; tile += gridDim.x) {
+        const int64_t r0 = (tile / tiles_c) * TR, c0 = (tile % tiles_c) * TC;
+        // stage-in: register transpose, swizzled 16-B stores in output orientation
+#pragma unroll
+        for (int m = 0; m < MT; ++m) {
+            const int mt = threadIdx.x + m * NT;
+            const int vc = mt % TCV, rg = mt / TCV;
+            micro_transpose<E>(reg[m]);
+#pragma unroll
+            for (int k = 0; k < V; ++k) {
+                const int orow = vc * V + k;
+                S[orow * TRV + (rg ^ ((orow / V) & 7))] = reg[m][k];
+            }
+        }
+        __syncthreads();
+        // prefetch the next tile while this one drains to HBM
+        const int64_t next = tile + gridDim.x;
+        if (next < ntiles) load_tile(next);
+        // stage-out: row-wise 16-B reads, coalesced 128-bit stores
+#pragma unroll
+        for (int s = 0; s < ST; ++s) {
+            const int idx = threadIdx.x + s * NT;
+            const int orow = idx / TRV, ocv = idx % TRV;
+            const int64_t oc = c0 + orow, orr = r0 + ocv * V;
+            if (oc < cols_v && orr < rows_v) {
+                const uint4 v = S[orow * TRV + (ocv ^ ((orow / V) & 7))];
+                stg_stream(reinterpret_cast<uint4 *>(out + oc * ld_out_b + orr * E), v);
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// Padded 32x32 tile (transposeNoBankConflicts shape) over a sub-rectangle
+// [r_lo, r_hi) x [c_lo, c_hi); any pitch, any alignment.
+template <typename T>
+__global__ void __launch_bounds__(256)
+    transpose_scalar_kernel(const T *__restrict__ in, T *__restrict__ out, int64_t r_lo,
+                            int64_t r_hi, int64_t c_lo, int64_t c_hi, int64_t ld_in,
+                            int64_t ld_out, int64_t tiles_c, int64_t ntiles) {
+    __shared__ T tile[32][33];
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int64_t r0 = r_lo + (t / tiles_c) * 32, c0 = c_lo + (t % tiles_c) * 32;
+#pragma unroll
+        for (int j = 0; j < 32; j += 8) {
+            const int64_t r = r0 + ty + j, c = c0 + tx;
+            if (r < r_hi && c < c_hi) tile[ty + j][tx] = in[r * ld_in + c];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < 32; j += 8) {
+            const int64_t oc = c0 + ty + j, orr = r0 + tx;  // out row = input col
+            if (oc < c_hi && orr < r_hi) out[oc * ld_out + orr] = tile[tx][ty + j];
+        }
+        __syncthreads();
+    }
+}
+
+template <int E, int TRV, int TCV, int NT>
+int run_vec(const void *in, void *out, int64_t rows_v, int64_t cols_v, int64_t ld_in,
+            int64_t ld_out, int dev, cudaStream_t st) {
+    constexpr int V = 16 / E;
+    constexpr int TR = TRV * V, TC = TCV * V;
+    const int64_t tiles_r = (rows_v + TR - 1) / TR, tiles_c = (cols_v + TC - 1) / TC;
+    const int64_t ntiles = tiles_r * tiles_c;
+    if (ntiles == 0) return B2_OK;
+    static int occ[64] = {0};
+    if (occ[dev] == 0) {
+        int o = 0;
+        B2_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &o, transpose_vec_kernel<E, TRV, TCV, NT>, NT, 0));
+        occ[dev] = o > 0 ? o : 1;
+    }
+    const int64_t grid = std::min<int64_t>(ntiles, (int64_t)num_sms(dev) * occ[dev]);
+    transpose_vec_kernel<E, TRV, TCV, NT><<<(unsigned)grid, NT, 0, st>>>(
+        (const uint8_t *)in, (uint8_t *)out, rows_v, cols_v, ld_in * E, ld_out * E, tiles_c,
+        ntiles);
+    count_launch();
+    B2_CUDA(cudaGetLastError());
+    return B2_OK;
+}
+
+template <typename T>
+int run_scalar(const void *in, void *out, int64_t r_lo, int64_t r_hi, int64_t c_lo,
+               int64_t c_hi, int64_t ld_in, int64_t ld_out, int dev, cudaStream_t st) {
+    if (r_hi <= r_lo || c_hi <= c_lo) return B2_OK;
+    const int64_t tiles_r = (r_hi - r_lo + 31) / 32, tiles_c = (c_hi - c_lo + 31) / 32;
+    const int64_t ntiles = tiles_r * tiles_c;
+    const int64_t grid = std::min<int64_t>(ntiles, (int64_t)num_sms(dev) * 8);
+    transpose_scalar_kernel<T><<<(unsigned)grid, 256, 0, st>>>(
+        (const T *)in, (T *)out, r_lo, r_hi, c_lo, c_hi, ld_in, ld_out, tiles_c, ntiles);
+    count_launch();
+    B2_CUDA(cudaGetLastError());
+    return B2_OK;
+}
+
+template <typename T>
+int run_scalar_all(const void *in, void *out, int64_t rows, int64_t cols, int64_t rv,
+                   int64_t cv, int64_t ld_in, int64_t ld_out, int dev, cudaStream_t st) {
+    // right strip [0,rows) x [cv,cols) and bottom strip [rv,rows) x [0,cv)
+    int rc = run_scalar<T>(in, out, 0, rows, cv, cols, ld_in, ld_out, dev, st);
+    if (rc) return rc;
+    return run_scalar<T>(in, out, rv, rows, 0, cv, ld_in, ld_out, dev, st);
+}
+
+template <int E>
+int run_vec_for(const void *in, void *out, int64_t rv, int64_t cv, int64_t ld_in,
+                int64_t ld_out, int dev, cudaStream_t st) {
+    if constexpr (E == 4) return run_vec<4, 16, 16, 256>(in, out, rv, cv, ld_in, ld_out, dev, st);
+    else if constexpr (E == 2) return run_vec<2, 16, 16, 256>(in, out, rv, cv, ld_in, ld_out, dev, st);
+    else return run_vec<8, 32, 16, 256>(in, out, rv, cv, ld_in, ld_out, dev, st);
+}
+
+template <typename T>
+int dispatch(const void *in, void *out, int64_t rows, int64_t cols, int64_t ld_in,
+             int64_t ld_out, int dev, cudaStream_t st) {
+    constexpr int E = sizeof(T);
+    constexpr int V = 16 / E;
+    const bool aligned = E >= 2 && ((uintptr_t)in % 16 == 0) && ((uintptr_t)out % 16 == 0) &&
+                         (ld_in * E % 16 == 0) && (ld_out * E % 16 == 0);
+    if (!aligned) return run_scalar<T>(in, out, 0, rows, 0, cols, ld_in, ld_out, dev, st);
+    const int64_t rv = rows - rows % V, cv = cols - cols % V;
+    if constexpr (E >= 2) {
+        int rc = run_vec_for<E>(in, out, rv, cv, ld_in, ld_out, dev, st);
+        if (rc) return rc;
+    }
+    return run_scalar_all<T>(in, out, rows, cols, rv, cv, ld_in, ld_out, dev, st);
+}
+
+}  // namespace
+
+int launch_transpose(const void *in, void *out, int64_t rows, int64_t cols, int64_t ld_in,
+                     int64_t ld_out, int esize, int dev, cudaStream_t st) {
+    switch (esize) {
+    case 1: return dispatch<uint8_t>(in, out, rows, cols, ld_in, ld_out, dev, st);
+    case 2: return dispatch<uint16_t>(in, out, rows, cols, ld_in, ld_out, dev, st);
+    case 4: return dispatch<uint32_t>(in, out, rows, cols, ld_in, ld_out, dev, st);
+    case 8: return dispatch<uint64_t>(in, out, rows, cols, ld_in, ld_out, dev, st);
+    default: return fail(B2_ERR_UNSUPPORTED, "transpose: unsupported element size");
+    }
+}
+
+}  // namespace b2

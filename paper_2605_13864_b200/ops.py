@@ -1,0 +1,179 @@
+"""Typed, zero-copy entries on device tensors and host arrays.
+
+These are the buffers-in / buffers-out faces of the two programs, named after
+the DSL entries the reference interprets (`transpose(in, out, W, H)`,
+`reduce(arr, N)`). `run_program` (interp.py in this package)
+recognises a Program and lands here.
+
+Device arguments are torch CUDA tensors (or anything exposing
+`__cuda_array_interface__`): the work is enqueued on the current torch stream
+and the call returns without synchronising. Host arguments are numpy arrays:
+the library pipelines H2D / kernel / D2H through its own device buffers and
+returns when the result is in host memory (pinned buffers make this fastest).
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from ._lib import check, lib
+
+try:  # torch is plumbing only (device memory, streams); optional for host calls
+    import torch
+except Exception:  # pragma: no cover
+    torch = None
+
+_NP_DTYPES = {
+    np.dtype(np.float32): _lib.F32, np.dtype(np.float64): _lib.F64,
+    np.dtype(np.int32): _lib.I32, np.dtype(np.int64): _lib.I64,
+    np.dtype(np.uint8): _lib.U8, np.dtype(np.int8): _lib.U8,
+    np.dtype(np.uint16): _lib.U16, np.dtype(np.int16): _lib.U16,
+    np.dtype(np.float16): _lib.F16, np.dtype(np.uint32): _lib.U32,
+    np.dtype(np.uint64): _lib.U64,
+}
+
+
+def _torch_dtypes():
+    return {
+        torch.float32: _lib.F32, torch.float64: _lib.F64, torch.bfloat16: _lib.BF16,
+        torch.float16: _lib.F16, torch.int32: _lib.I32, torch.int64: _lib.I64,
+        torch.uint8: _lib.U8, torch.int8: _lib.U8, torch.int16: _lib.U16,
+        torch.uint16: _lib.U16, torch.uint32: _lib.U32, torch.uint64: _lib.U64,
+    }
+
+
+def _is_torch_cuda(x) -> bool:
+    return torch is not None and isinstance(x, torch.Tensor) and x.is_cuda
+
+
+def b2_dtype(x) -> int:
+    if torch is not None and isinstance(x, torch.Tensor):
+        d = _torch_dtypes().get(x.dtype)
+    else:
+        d = _NP_DTYPES.get(np.asarray(x).dtype)
+    if d is None:
+        raise TypeError(f"unsupported dtype {getattr(x, 'dtype', type(x))}")
+    return d
+
+
+def _stream_ptr(t, stream=None) -> int:
+    if stream is not None:
+        return int(getattr(stream, "cuda_stream", stream))
+    return int(torch.cuda.current_stream(t.device).cuda_stream)
+
+
+# ----------------------------------------------------------------------------- transpose
+
+def transpose(inp, out=None, *, stream=None):
+    """out = inp^T (bit-exact). `inp` is rows x cols with unit column stride.
+
+    Device tensors: returns `out` (allocated if None), asynchronous on the stream.
+    Host numpy arrays: returns `out` after the host pipeline completes.
+    """
+    if _is_torch_cuda(inp):
+        if inp.dim() != 2 or (inp.numel() and inp.stride(1) != 1):
+            raise ValueError("transpose: input must be 2-D with unit column stride")
+        rows, cols = inp.shape
+        if out is None:
+            out = torch.empty((cols, rows), dtype=inp.dtype, device=inp.device)
+        if not _is_torch_cuda(out) or out.dtype != inp.dtype or tuple(out.shape) != (cols, rows):
+            raise ValueError("transpose: out must be a (cols, rows) CUDA tensor of the same dtype")
+        if out.numel() and out.stride(1) != 1:
+            raise ValueError("transpose: out must have unit column stride")
+        if inp.numel() == 0:
+            return out
+        check(lib().b2_transpose(inp.data_ptr(), out.data_ptr(), rows, cols, inp.stride(0),
+                                 out.stride(0), b2_dtype(inp), inp.device.index,
+                                 _stream_ptr(inp, stream)))
+        return out
+    a = np.asarray(inp)
+    if a.ndim != 2 or (a.size and a.strides[1] != a.itemsize):
+        raise ValueError("transpose: input must be 2-D with unit column stride")
+    rows, cols = a.shape
+    if out is None:
+        out = np.empty((cols, rows), dtype=a.dtype)
+    if out.shape != (cols, rows) or out.dtype != a.dtype or (out.size and out.strides[1] != out.itemsize):
+        raise ValueError("transpose: out must be a (cols, rows) array of the same dtype")
+    if a.size == 0:
+        return out
+    check(lib().b2_transpose_host(a.ctypes.data, out.ctypes.data, rows, cols,
+                                  a.strides[0] // a.itemsize, out.strides[0] // out.itemsize,
+                                  b2_dtype(a), _host_device()))
+    return out
+
+
+# ----------------------------------------------------------------------------- reduction
+
+_ACC = {_lib.F32: (np.float32, "float32"), _lib.I32: (np.int64, "int64"),
+        _lib.F64: (np.float64, "float64")}
+
+
+def reduce_sum(arr, *, out=None, ws=None, stream=None):
+    """Sum of a 1-D float32 / int32 / float64 array (int32 accumulates in int64).
+
+    Device: returns a 1-element CUDA tensor (float32 / int64 / float64), async.
+    Host: returns a Python float / int.
+    """
+    d = b2_dtype(arr)
+    if d not in _ACC:
+        raise TypeError("reduce: dtype must be float32, int32 or float64")
+    npacc, tacc = _ACC[d]
+    if _is_torch_cuda(arr):
+        if arr.dim() != 1 or (arr.numel() and arr.stride(0) != 1):
+            raise ValueError("reduce: input must be a contiguous 1-D tensor")
+        if out is None:
+            out = torch.empty(1, dtype=getattr(torch, tacc), device=arr.device)
+        wsp, wsb = (0, 0) if ws is None else (ws.data_ptr(), ws.numel() * ws.element_size())
+        check(lib().b2_reduce_sum(arr.data_ptr(), arr.numel(), d, out.data_ptr(), wsp or None, wsb,
+                                  arr.device.index, _stream_ptr(arr, stream)))
+        return out
+    a = np.ascontiguousarray(arr).reshape(-1)
+    res = np.zeros(1, dtype=npacc)
+    check(lib().b2_reduce_sum_host(a.ctypes.data, a.size, d, res.ctypes.data, _host_device()))
+    return res[0].item()
+
+
+def reduce_tree512(arr, *, stream=None) -> float:
+    """The A.5 tree-form program, bit-identical with the reference interpreter:
+    per-512 block halving tree on the device, sequential binary32 host sum."""
+    if not _is_torch_cuda(arr):
+        raise TypeError("reduce_tree512: expects a CUDA float32 tensor")
+    if arr.dtype != torch.float32 or arr.dim() != 1 or (arr.numel() and arr.stride(0) != 1):
+        raise ValueError("reduce_tree512: input must be a contiguous 1-D float32 tensor")
+    res = ctypes.c_float(0.0)
+    check(lib().b2_reduce_tree512(arr.data_ptr(), arr.numel(), ctypes.byref(res),
+                                  arr.device.index, _stream_ptr(arr, stream)))
+    return float(res.value)
+
+
+def reduce_tree512_partials(arr, partials=None, *, stream=None):
+    if partials is None:
+        partials = torch.empty(arr.numel() // 512, dtype=torch.float32, device=arr.device)
+    check(lib().b2_reduce_tree512_partials(arr.data_ptr(), arr.numel(), partials.data_ptr(),
+                                           arr.device.index, _stream_ptr(arr, stream)))
+    return partials
+
+
+def reduce_ws_bytes(n: int, dtype: int) -> int:
+    return int(lib().b2_reduce_ws_bytes(n, dtype))
+
+
+# ----------------------------------------------------------------------------- device choice
+
+_HOST_DEVICE = None
+
+
+def set_host_device(dev: int) -> None:
+    """Device used by host-buffer calls (default: torch's current device, else 0)."""
+    global _HOST_DEVICE
+    _HOST_DEVICE = int(dev)
+
+
+def _host_device() -> int:
+    if _HOST_DEVICE is not None:
+        return _HOST_DEVICE
+    if torch is not None and torch.cuda.is_available():
+        return torch.cuda.current_device()
+    return 0

@@ -1,0 +1,145 @@
+"""GPU parity of the sm_100a kernels against the CPU oracle and the reference's
+golden vectors (bit-exact transposes and integer sums; fp32 sums within the
+north-star tolerance; the A.5 tree order bit-exact)."""
+import numpy as np
+import pytest
+
+from oracle import oracle
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def b2():
+    import paper_2605_13864_b200 as b2
+    return b2
+
+
+def _dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def test_golden_transposes_device(b2, golden):
+    for c in golden:
+        if c["kind"] != "transpose":
+            continue
+        a = c["inp"]
+        if a.dtype == np.uint64:
+            a = a.view(np.int64)
+        out = b2.transpose(_dev(a)).cpu().numpy()
+        assert out.tobytes() == c["out"].astype(a.dtype).tobytes(), c["id"]
+
+
+def test_golden_reductions_device(b2, golden):
+    for c in golden:
+        if c["kind"] != "reduce":
+            continue
+        x = c["inp"]
+        if "result_int" in c:
+            got = int(b2.reduce_sum(_dev(x)).item())
+            assert got == int(c["result_int"]), c["id"]
+        elif "tree" in c["program"]:
+            got = b2.reduce_tree512(_dev(x))
+            assert np.float32(got).view(np.uint32) == np.uint32(c["result_f32_bits"]), c["id"]
+        else:
+            got = float(b2.reduce_sum(_dev(x)).item())
+            exact, absum = oracle.sum_f64(x)
+            assert abs(got - exact) <= oracle.f32_tolerance(x.size, exact, absum), c["id"]
+
+
+SHAPES = [(1, 1), (1, 2**20), (2**20, 1), (33, 65), (1023, 1025), (64, 64), (128, 256),
+          (4097, 8191), (4096, 4096), (100, 36), (8, 1000)]
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+@pytest.mark.parametrize("dt", [torch.bfloat16, torch.float32, torch.float64])
+def test_transpose_sweep(b2, shape, dt):
+    g = torch.Generator(device="cuda").manual_seed(hash(shape) % 1000)
+    a = torch.randn(shape, device="cuda", dtype=torch.float32, generator=g).to(dt)
+    out = b2.transpose(a)
+    torch.cuda.synchronize()
+    ref = oracle.transpose(a.view(torch.int16 if dt == torch.bfloat16 else
+                                  (torch.int32 if dt == torch.float32 else torch.int64)).cpu().numpy())
+    got = out.view(torch.int16 if dt == torch.bfloat16 else
+                   (torch.int32 if dt == torch.float32 else torch.int64)).cpu().numpy()
+    assert np.array_equal(got, ref)
+
+
+def test_transpose_pitched(b2):
+    base = torch.arange(300 * 520, device="cuda", dtype=torch.float32).reshape(300, 520)
+    view = base[:, 8:508]  # pitch 520, 16-B aligned start
+    out = torch.full((520, 320), -1.0, device="cuda")
+    b2.transpose(view, out[:500, :300])
+    torch.cuda.synchronize()
+    assert torch.equal(out[:500, :300], view.t())
+    assert bool((out[:, 300:] == -1).all()) and bool((out[500:] == -1).all())
+    odd = base[:, 3:400]  # misaligned start -> scalar path
+    assert torch.equal(b2.transpose(odd), odd.t())
+
+
+@pytest.mark.parametrize("n", [0, 1, 3, 17, 1000, 2**20 + 3, 2**24])
+def test_reduce_int32_exact(b2, n):
+    g = torch.Generator(device="cuda").manual_seed(n)
+    x = torch.randint(-2**31, 2**31, (n,), device="cuda", dtype=torch.int64, generator=g).to(torch.int32)
+    got = int(b2.reduce_sum(x).item())
+    assert got == oracle.reduce_i32(x.cpu().numpy())
+
+
+def test_reduce_int32_misaligned_views(b2):
+    x = torch.randint(-2**31, 2**31, (100003,), device="cuda", dtype=torch.int64).to(torch.int32)
+    for off in range(1, 4):
+        v = x[off:]
+        assert int(b2.reduce_sum(v).item()) == oracle.reduce_i32(v.cpu().numpy())
+
+
+@pytest.mark.parametrize("n", [1, 7, 4096, 2**20, 2**24])
+@pytest.mark.parametrize("lo", [0.0, -1.0])
+def test_reduce_f32_tolerance(b2, n, lo):
+    g = torch.Generator(device="cuda").manual_seed(n)
+    x = torch.rand((n,), device="cuda", generator=g) * (1 - lo) + lo
+    got = float(b2.reduce_sum(x).item())
+    xh = x.cpu().numpy()
+    exact, absum = oracle.sum_f64(xh)
+    assert abs(got - exact) <= oracle.f32_tolerance(n, exact, absum)
+    # deterministic run to run
+    assert float(b2.reduce_sum(x).item()) == got
+
+
+@pytest.mark.parametrize("n", [512, 4096, 2**20, 2**24])
+def test_tree512_bit_exact(b2, n):
+    g = torch.Generator(device="cuda").manual_seed(n)
+    x = torch.rand((n,), device="cuda", generator=g) * 2 - 1
+    want, parts = oracle.reduce_f32_tree512(x.cpu().numpy())
+    got_parts = b2.reduce_tree512_partials(x).cpu().numpy()
+    assert np.array_equal(got_parts.view(np.uint32), parts.view(np.uint32))
+    assert np.float32(b2.reduce_tree512(x)).view(np.uint32) == np.float32(want).view(np.uint32)
+
+
+def test_tree512_rejects_inexact(b2):
+    with pytest.raises(b2.B2Error):
+        b2.reduce_tree512(torch.ones(513, device="cuda"))
+
+
+def test_reduce_f64(b2):
+    x = torch.randn(1 << 20, device="cuda", dtype=torch.float64)
+    got = float(b2.reduce_sum(x).item())
+    assert abs(got - float(x.sum().item())) <= 1e-9 * float(x.abs().sum().item())
+
+
+def test_host_paths(b2):
+    rng = np.random.default_rng(3)
+    a = rng.standard_normal((3000, 2050)).astype(np.float32)
+    assert np.array_equal(b2.transpose(a), a.T)
+    xi = rng.integers(-2**31, 2**31, 5_000_001, dtype=np.int64).astype(np.int32)
+    assert b2.reduce_sum(xi) == oracle.reduce_i32(xi)
+    xf = rng.uniform(-1, 1, 1_000_003).astype(np.float32)
+    exact, absum = oracle.sum_f64(xf)
+    assert abs(b2.reduce_sum(xf) - exact) <= oracle.f32_tolerance(xf.size, exact, absum)
+
+
+def test_launch_counter(b2):
+    n0 = b2.launch_count()
+    b2.reduce_sum(torch.ones(100, device="cuda"))
+    torch.cuda.synchronize()
+    assert b2.launch_count() == n0 + 1

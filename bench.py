@@ -164,7 +164,7 @@ def cpu_leg(rows, cols, n, reps=1):
     tt = min(t[0] for t in times)
     tr = min(t[1] for t in times)
     bytes_ = 2 * rows * cols * 4 + n * 4 + 8
-    assert np.array_equal(out[:5, :7], a[:7, :5].T)
+    assert np.array_equal(out[:5, :7].view(np.uint32), a[:7, :5].T.view(np.uint32))
     return {"value": bytes_ / (tt + tr) / 1e9, "unit": "GB/s", "cores": threads,
             "transpose_s": tt, "reduce_s": tr, "checksum": s}
 

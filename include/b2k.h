@@ -116,6 +116,10 @@ B2_API int b2_reduce_tree512_partials(const float *in, int64_t n, float *partial
  * `in` is a device pointer; *result_host receives the float. Synchronous. */
 B2_API int b2_reduce_tree512(const float *in, int64_t n, float *result_host, int dev, void *stream);
 
+/* Host-buffer form of the A.5 program: chunked H2D of `in_host`, per-512 partials
+ * on the device, D2H of the partials, sequential binary32 host sum. Bit-exact. */
+B2_API int b2_reduce_tree512_host(const float *in_host, int64_t n, float *result_host, int dev);
+
 /* Block until all work this library queued on `stream` of `dev` is done. */
 B2_API int b2_sync(int dev, void *stream);
 

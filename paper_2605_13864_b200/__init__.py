@@ -10,8 +10,12 @@ Public surface:
   * `transpose`, `reduce_sum`, `reduce_tree512`              — typed zero-copy
     entries on CUDA tensors or host arrays.
 """
-from .ops import reduce_sum, reduce_tree512, reduce_tree512_partials, transpose  # noqa: F401
 from ._lib import B2Error, launch_count  # noqa: F401
+from .interp import Array, Interp, InterpError, UnsupportedProgram, f32, run_program  # noqa: F401
+from .lang import ParseError, Program, parse_program  # noqa: F401
+from .ops import reduce_sum, reduce_tree512, reduce_tree512_partials, transpose  # noqa: F401
+from .recognize import recognize  # noqa: F401
 
-__all__ = ["transpose", "reduce_sum", "reduce_tree512", "reduce_tree512_partials", "B2Error",
-           "launch_count"]
+__all__ = ["run_program", "Interp", "Array", "InterpError", "UnsupportedProgram", "f32",
+           "parse_program", "ParseError", "Program", "recognize", "transpose", "reduce_sum",
+           "reduce_tree512", "reduce_tree512_partials", "B2Error", "launch_count"]

@@ -220,6 +220,43 @@ int b2_reduce_tree512(const float *in, int64_t n, float *result_host, int dev, v
     return B2_OK;
 }
 
+int b2_reduce_tree512_host(const float *in_host, int64_t n, float *result_host, int dev) {
+    if (!in_host || !result_host) return fail(B2_ERR_INVALID, "tree512: NULL buffer");
+    if (n <= 0 || n % 512)
+        return fail(B2_ERR_INVALID, "exact_div(" + std::to_string(n) + ", 512) is not exact");
+    if (int rc = check_dev(dev)) return rc;
+    DevCtx &c = g_ctx[dev];
+    std::lock_guard<std::mutex> g(c.mu);
+    if (int rc = ctx_init(c, dev)) return rc;
+    int64_t ce = (int64_t)(kChunkBytes / sizeof(float));
+    ce -= ce % 512;
+    ce = std::min(ce, n);
+    if (int rc = ensure_stages(c, (size_t)ce * sizeof(float))) return rc;
+    const int64_t nb = n / 512;
+    if (int rc = ensure_small(c, (size_t)nb * sizeof(float))) return rc;
+    const int64_t nchunks = (n + ce - 1) / ce;
+    for (int64_t i = 0; i < nchunks; ++i) {
+        const int k = (int)(i % kStages);
+        const int64_t e0 = i * ce, ne = std::min(ce, n - e0);
+        if (i >= kStages) B2_CUDA(cudaStreamWaitEvent(c.s_h2d, c.ev_comp[k], 0));
+        B2_CUDA(cudaMemcpyAsync(c.d_in[k], in_host + e0, ne * sizeof(float), cudaMemcpyHostToDevice,
+                                c.s_h2d));
+        B2_CUDA(cudaEventRecord(c.ev_in[k], c.s_h2d));
+        B2_CUDA(cudaStreamWaitEvent(c.s_comp, c.ev_in[k], 0));
+        if (int rc = launch_tree512((const float *)c.d_in[k], ne, (float *)c.d_small + e0 / 512, dev,
+                                    c.s_comp))
+            return rc;
+        B2_CUDA(cudaEventRecord(c.ev_comp[k], c.s_comp));
+    }
+    B2_CUDA(cudaMemcpyAsync(c.h_small, c.d_small, nb * sizeof(float), cudaMemcpyDeviceToHost, c.s_comp));
+    B2_CUDA(cudaStreamSynchronize(c.s_comp));
+    volatile float s = 0.0f;  // the program's host loop, binary32, i ascending
+    const float *p = (const float *)c.h_small;
+    for (int64_t i = 0; i < nb; ++i) s = s + p[i];
+    *result_host = s;
+    return B2_OK;
+}
+
 int b2_sync(int dev, void *stream) {
     if (int rc = check_dev(dev)) return rc;
     B2_CUDA(cudaStreamSynchronize((cudaStream_t)stream));

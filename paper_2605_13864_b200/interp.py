@@ -1,0 +1,359 @@
+"""Drop-in for the reference interpreter's entry points (minigpu/interp.py),
+executing the OptiGPU transpose and reduce programs on a B200.
+
+    run_program(program, entry, inputs) -> (ret, {param: flat data})   interp.py:380-387
+    Interp(program).run(fn_name, inputs) -> (("ret", v) | None, {param: Array})  :106-128
+    Array(dims, data, ctype="float", freed=False)                        :47-85
+    InterpError, f32                                                     :39-44
+
+How a call executes: parameters are marshalled exactly as Interp.run does
+(missing input -> InterpError; Array arguments are used by reference and
+mutated in place; other iterables become a fresh 1-D Array, f32-rounded for
+`float*` parameters), the entry function is recognised (recognize.py) as one of
+the hot-path programs, the program's own preconditions are checked with the
+reference's error messages (bounds, rank, uninitialised cells, use after free,
+exact_div), and the work runs through libb200k.so's host-buffer pipelines
+(H2D / sm_100a kernel / D2H). Unrecognised programs raise UnsupportedProgram
+(an InterpError): there is no CPU fallback.
+
+Results: transposes are bit-identical to the reference; integer sums are exact
+(the reference's unbounded ints; int cells are 4 bytes, intrinsics.py:35); the
+A.5 tree-form fp32 sum is bit-identical; the naive fp32 sum (sequential order in
+the reference) is returned in the GPU's tree order, within the north-star
+tolerance.
+
+Extensions (documented deviations):
+  * `Array.data` may be a numpy array (zero-copy host buffer); results are then
+    written into it and `run_program` returns that array instead of a list.
+  * Rank-2 transpose parameters given as flat 1-D data are rejected; the
+    reference would silently apply its 1-D pointer-offset rule (interp.py:239-240).
+  * Errors are raised before any output cell is written (the reference leaves
+    the cells it wrote before failing).
+"""
+from __future__ import annotations
+
+import struct
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import ops
+from .recognize import Plan, UnsupportedProgram as _Unsupported, recognize
+
+
+class InterpError(Exception):
+    pass
+
+
+class UnsupportedProgram(InterpError, _Unsupported):
+    """The program is not one this backend executes (no CPU fallback)."""
+
+
+def f32(x: float) -> float:
+    """Round to IEEE binary32 (interp.py:43-44)."""
+    return struct.unpack("f", struct.pack("f", float(x)))[0]
+
+
+@dataclass
+class Array:
+    """Row-major cells; `None` marks an uninitialised cell (interp.py:47-85).
+
+    `data` is a Python list (reference layout) or a numpy array (zero-copy)."""
+
+    dims: list
+    data: object
+    ctype: str = "float"
+    freed: bool = False
+
+    @staticmethod
+    def alloc(dims, ctype):
+        n = 1
+        for d in dims:
+            n *= d
+        return Array(list(dims), [None] * n, ctype)
+
+    @staticmethod
+    def from_numpy(a: np.ndarray, ctype: str | None = None) -> "Array":
+        """Zero-copy Array over a C-contiguous numpy buffer."""
+        if not a.flags.c_contiguous:
+            raise ValueError("Array.from_numpy needs a C-contiguous array")
+        if ctype is None:
+            ctype = "float" if a.dtype.kind == "f" and a.dtype.itemsize == 4 else "int"
+        return Array(list(a.shape), a.reshape(-1), ctype)
+
+    def offset(self, idxs) -> int:
+        if len(idxs) != len(self.dims):
+            raise InterpError(f"rank mismatch: {len(idxs)} indices into {len(self.dims)}-d array")
+        off = 0
+        for ix, d in zip(idxs, self.dims):
+            if not (0 <= ix < d):
+                raise InterpError(f"index {ix} out of bounds 0..{d}")
+            off = off * d + ix
+        return off
+
+    def get(self, idxs):
+        if self.freed:
+            raise InterpError("use after free")
+        v = self.data[self.offset(idxs)]
+        if v is None:
+            raise InterpError("read of uninitialized cell")
+        return v
+
+    def set(self, idxs, v):
+        if self.freed:
+            raise InterpError("use after free")
+        if self.ctype == "float":
+            v = f32(v)
+        self.data[self.offset(idxs)] = v
+
+
+def _is_array(v) -> bool:
+    # this package's Array or the reference's (same fields)
+    return all(hasattr(v, a) for a in ("dims", "data", "ctype", "freed"))
+
+
+# ----------------------------------------------------------------------------- cell marshalling
+
+def _cells(arr, n: int, want: str) -> np.ndarray:
+    """First n cells of `arr` as a numpy vector: float32 for want == "float",
+    the narrowest exact integer type for want == "int". Raises the reference's
+    errors for freed arrays and uninitialised cells."""
+    if arr.freed:
+        raise InterpError("use after free")
+    data = arr.data
+    if isinstance(data, np.ndarray):
+        v = data.reshape(-1)[:n]
+        if v.size < n:
+            raise IndexError("list index out of range")
+        if want == "float" and v.dtype != np.float32:
+            return _to_f32(v.astype(np.float64))
+        return v
+    if len(data) < n:
+        raise IndexError("list index out of range")
+    part = data[:n] if n != len(data) else data
+    if any(x is None for x in part):
+        raise InterpError("read of uninitialized cell")
+    if want == "float":
+        return _to_f32(np.fromiter(part, dtype=np.float64, count=n))
+    return _ints(part)
+
+
+def _to_f32(v: np.ndarray) -> np.ndarray:
+    with np.errstate(over="ignore"):
+        r = v.astype(np.float32)
+    bad = np.isinf(r) & np.isfinite(v)
+    if bad.any():  # struct.pack("f") refuses these (interp.py:44)
+        raise OverflowError("float too large to pack with f format")
+    return r
+
+
+def _ints(part) -> np.ndarray:
+    try:
+        v = np.array(part, dtype=np.int64)
+        return v.astype(np.int32) if v.size == 0 or (
+            v.min() >= -2**31 and v.max() < 2**31) else v
+    except OverflowError:
+        v = np.array(part, dtype=np.uint64)  # 64-bit patterns (fp64 bits) up to 2^64-1
+        return v
+
+
+def _store(arr, flat_positions_rows, values2d: np.ndarray, row_pitch: int):
+    """Write a (rows x cols) block into arr.data, row r at offset r*row_pitch."""
+    data = arr.data
+    rows, cols = values2d.shape
+    if isinstance(data, np.ndarray):
+        dst = data.reshape(-1)
+        view = np.lib.stride_tricks.as_strided(
+            dst, shape=(rows, cols), strides=(row_pitch * dst.itemsize, dst.itemsize))
+        view[...] = values2d.astype(dst.dtype, copy=False)
+        return
+    if row_pitch == cols:
+        data[:rows * cols] = values2d.reshape(-1).tolist()
+        return
+    for r in range(rows):
+        data[r * row_pitch:r * row_pitch + cols] = values2d[r].tolist()
+
+
+# ----------------------------------------------------------------------------- interpreter
+
+class Interp:
+    """run(fn_name, inputs) mirrors minigpu.interp.Interp.run (interp.py:106-128)."""
+
+    def __init__(self, program):
+        self.program = program
+        self.launch: list = []
+        self.ctx_width: list = []
+
+    def run(self, fn_name: str, inputs: dict):
+        fn = self.program.fn(fn_name)
+        env: dict = {}
+        arrays: dict = {}
+        for pname, ptype in fn.params:
+            if pname not in inputs:
+                raise InterpError(f"missing input {pname!r}")
+            v = inputs[pname]
+            if ptype.endswith("*"):
+                if _is_array(v):
+                    arr = v
+                elif isinstance(v, np.ndarray):
+                    flat = np.ascontiguousarray(v).reshape(-1)
+                    if ptype.startswith("float") and flat.dtype != np.float32:
+                        flat = _to_f32(flat.astype(np.float64))
+                    arr = Array([flat.size], flat, "float" if ptype.startswith("float") else "int")
+                else:
+                    data = list(v)
+                    if ptype.startswith("float"):
+                        data = _cells(Array([len(data)], data, "float"), len(data), "float").tolist()
+                    arr = Array([len(data)], data, "float" if ptype.startswith("float") else "int")
+                arrays[pname] = arr
+                env[pname] = arr
+            else:
+                env[pname] = v
+        try:
+            plan = recognize(self.program, fn_name)
+        except _Unsupported as e:
+            raise UnsupportedProgram(str(e)) from None
+        ret = _EXEC[(plan.kind, plan.form)](plan, env)
+        return ret, arrays
+
+
+def run_program(program, entry: str, inputs: dict):
+    """Returns (return value, {param name: flat final array data}) (interp.py:380-387).
+
+    List-backed arrays come back as fresh lists; numpy-backed arrays come back
+    as the (mutated) numpy buffer itself."""
+    it = Interp(program)
+    ret, arrays = it.run(entry, dict(inputs))
+    out = {k: (a.data if isinstance(a.data, np.ndarray) else list(a.data))
+           for k, a in arrays.items()}
+    if isinstance(ret, tuple) and ret and ret[0] == "ret":
+        ret = ret[1]
+    return ret, out
+
+
+# ----------------------------------------------------------------------------- program executors
+
+def _int_arg(env, name):
+    v = env[name]
+    if isinstance(v, (bool, np.bool_)) or not isinstance(v, (int, np.integer)):
+        raise InterpError(f"{name!r} must be an int")
+    return int(v)
+
+
+def _check_2d(arr, name, need_rows, need_cols):
+    """Reference access rules for `name[r][c]` with r < need_rows, c < need_cols."""
+    if arr.freed:
+        raise InterpError("use after free")
+    if len(arr.dims) != 2:
+        raise InterpError(
+            f"rank mismatch on {list(arr.dims)}: {name!r} is indexed as a 2-d array; flat "
+            "data is not reinterpreted (the reference's 1-d pointer-offset rule, "
+            "interp.py:239-240, is not supported)")
+    R, C = arr.dims
+    if need_rows > R:
+        raise InterpError(f"index {R} out of bounds 0..{R}")
+    if need_cols > C:
+        raise InterpError(f"index {C} out of bounds 0..{C}")
+
+
+def _exec_transpose_naive(plan: Plan, env):
+    src, dst = env[plan.params["in"]], env[plan.params["out"]]
+    W, H = _int_arg(env, plan.params["W"]), _int_arg(env, plan.params["H"])
+    if W <= 0 or H <= 0:
+        return None
+    # in[y][x] for y < H, x < W; out[x][y] (interp.py:159-164, :271-276, Array.offset :61-70)
+    _check_2d(src, plan.params["in"], H, W)
+    _check_2d(dst, plan.params["out"], W, H)
+    R, C = src.dims
+    Ro, Co = dst.dims
+    want = "float" if dst.ctype == "float" else "int"
+    a = _read_block(src, H, W, C, want)
+    if isinstance(dst.data, np.ndarray) and dst.data.dtype == a.dtype and dst.data.flags.c_contiguous:
+        out2d = np.lib.stride_tricks.as_strided(
+            dst.data, shape=(W, H), strides=(Co * a.itemsize, a.itemsize))
+        ops.transpose(a, out2d)
+    else:
+        out = ops.transpose(a)
+        _store(dst, None, out, Co)
+    return None
+
+
+def _read_block(arr, rows, cols, pitch, want) -> np.ndarray:
+    """arr.data as a (rows x cols) view/array with row pitch `pitch`."""
+    data = arr.data
+    if isinstance(data, np.ndarray) and (want == "int" or data.dtype == np.float32):
+        flat = data.reshape(-1)
+        return np.lib.stride_tricks.as_strided(flat, shape=(rows, cols),
+                                               strides=(pitch * flat.itemsize, flat.itemsize))
+    if pitch == cols:
+        return _cells(arr, rows * cols, want).reshape(rows, cols)
+    full = _cells(Array([len(data)], data, arr.ctype), (rows - 1) * pitch + cols, want)
+    return np.lib.stride_tricks.as_strided(full, shape=(rows, cols),
+                                           strides=(pitch * full.itemsize, full.itemsize)).copy()
+
+
+def _exec_transpose_gpu(plan: Plan, env):
+    """A.4: memcpy_host_to_device2 (flat copy of H*W cells), kernel, flat copy back."""
+    src, dst = env[plan.params["in"]], env[plan.params["out"]]
+    W, H = _int_arg(env, plan.params["W"]), _int_arg(env, plan.params["H"])
+    n = H * W
+    if src.freed:
+        raise InterpError("use after free")
+    a = _cells(src, max(n, 0), "float") if n > 0 else np.zeros(0, np.float32)
+    for v in (W, H):  # kernel_launch((W/32)*(H/32), ...): exact_div, interp.py:209-214
+        if v % 32 != 0:
+            raise InterpError(f"exact_div({v}, 32) is not exact")
+    if n <= 0:
+        return None
+    if dst.freed:
+        raise InterpError("use after free")
+    if (len(dst.data) if not isinstance(dst.data, np.ndarray) else dst.data.size) < n:
+        raise IndexError("list assignment index out of range")
+    out = ops.transpose(np.ascontiguousarray(a).reshape(H, W))
+    _store(dst, None, out.reshape(1, n), n)
+    return None
+
+
+def _exec_reduce_naive(plan: Plan, env):
+    arr = env[plan.params["arr"]]
+    N = _int_arg(env, plan.params["N"])
+    cell = plan.cell
+    if N <= 0:
+        return ("ret", 0.0 if cell == "float" else 0)
+    if arr.freed:
+        raise InterpError("use after free")
+    if len(arr.dims) != 1:
+        raise InterpError(f"rank mismatch on {list(arr.dims)}￨[0]")
+    if N > arr.dims[0]:
+        raise InterpError(f"index {arr.dims[0]} out of bounds 0..{arr.dims[0]}")
+    x = _cells(arr, N, cell)
+    if cell == "float":
+        return ("ret", float(np.float32(ops.reduce_sum(np.ascontiguousarray(x)))))
+    if x.dtype != np.int32:
+        raise InterpError("int cell value outside the 4-byte cell range (intrinsics.py:35 "
+                          "CELL_BYTES = 4)")
+    return ("ret", int(ops.reduce_sum(np.ascontiguousarray(x))))
+
+
+def _exec_reduce_tree(plan: Plan, env):
+    """A.5: flat copy of N cells, per-512 tree on the device, sequential host sum."""
+    arr = env[plan.params["arr"]]
+    N = _int_arg(env, plan.params["N"])
+    if arr.freed:
+        raise InterpError("use after free")
+    x = _cells(arr, N, "float") if N > 0 else np.zeros(0, np.float32)
+    if N % 512 != 0:
+        raise InterpError(f"exact_div({N}, 512) is not exact")
+    if N <= 0:
+        return ("ret", 0.0)
+    return ("ret", ops.reduce_tree512(np.ascontiguousarray(x)))
+
+
+_EXEC = {
+    ("transpose", "naive"): _exec_transpose_naive,
+    ("transpose", "gpu"): _exec_transpose_gpu,
+    ("reduce", "naive"): _exec_reduce_naive,
+    ("reduce", "tree512"): _exec_reduce_tree,
+}
+
+__all__ = ["Array", "Interp", "InterpError", "UnsupportedProgram", "f32", "run_program"]

@@ -138,11 +138,13 @@ def reduce_sum(arr, *, out=None, ws=None, stream=None):
 def reduce_tree512(arr, *, stream=None) -> float:
     """The A.5 tree-form program, bit-identical with the reference interpreter:
     per-512 block halving tree on the device, sequential binary32 host sum."""
+    res = ctypes.c_float(0.0)
     if not _is_torch_cuda(arr):
-        raise TypeError("reduce_tree512: expects a CUDA float32 tensor")
+        a = np.ascontiguousarray(arr, dtype=np.float32).reshape(-1)
+        check(lib().b2_reduce_tree512_host(a.ctypes.data, a.size, ctypes.byref(res), _host_device()))
+        return float(res.value)
     if arr.dtype != torch.float32 or arr.dim() != 1 or (arr.numel() and arr.stride(0) != 1):
         raise ValueError("reduce_tree512: input must be a contiguous 1-D float32 tensor")
-    res = ctypes.c_float(0.0)
     check(lib().b2_reduce_tree512(arr.data_ptr(), arr.numel(), ctypes.byref(res),
                                   arr.device.index, _stream_ptr(arr, stream)))
     return float(res.value)

@@ -1,0 +1,330 @@
+"""Program recogniser: maps a `Program` entry function onto one of the B200
+kernels, or refuses it.
+
+The reference executes any Program by walking it (minigpu/interp.py:248-309).
+This package executes only the OptiGPU hot-path programs — the transpose and
+the reduction in their naive and GPU-derived forms (
+PAPER.md:155-172, 395-433, 586-618, 1041-1068, 1120-1131) — and refuses every
+other program loudly (there is no CPU fallback).
+
+Recognition is alpha-equivalence against canonical templates: after removing
+ghost calls (ast.py:473-494 `strip_ghosts`), the entry body must match a
+template node for node, with every binder (parameter, local, loop index)
+renamed consistently (a bijection) and every literal, operator, loop mode,
+allocator and intrinsic identical. Parameter ORDER is free: parameters are
+bound by the role they play in the body. Works on Programs from this package's
+parser and from the reference's (matching is by node class name and fields).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+from .lang import parse_program
+
+# ----------------------------------------------------------------------------- templates
+# Canonical programs. `T` is a cell type placeholder (float | int), bound once.
+
+_T_NAIVE_XY = """
+void transpose(T* in, T* out, int W, int H) {
+    for (int x = 0; x < W; x++) { for (int y = 0; y < H; y++) { out[x][y] = in[y][x]; } }
+}"""
+_T_NAIVE_YX = """
+void transpose(T* in, T* out, int W, int H) {
+    for (int y = 0; y < H; y++) { for (int x = 0; x < W; x++) { out[x][y] = in[y][x]; } }
+}"""
+_R_NAIVE = """
+T reduce(T* arr, int N) {
+    T sum = ZERO;
+    for (int i = 0; i < N; i++) { sum += arr[i]; }
+    return sum;
+}"""
+_T_GPU = """
+void transpose(float* in, float* out, int W, int H) {
+    float* const d_in = gmem_malloc2<float>(H, W);
+    memcpy_host_to_device2(d_in, in, H, W);
+    float* const d_out = gmem_malloc2<float>(W, H);
+    {
+        kernel_launch((W/32)*(H/32), 16 * 32, 4 * 32 * 32);
+        float* const tile = __smem_malloc2<float>(32, 32);
+        kernel_setup_end();
+        thread for (int by = 0; by < H/32; by++) {
+            thread for (int bx = 0; bx < W/32; bx++) {
+                for (int j = 0; j < 2; j++) {
+                    thread for (int y = 0; y < 16; y++) {
+                        thread for (int x = 0; x < 32; x++) {
+                            tile[DMINDEX2(H/32, W/32, by, bx)][j*16 + y][x] = d_in[by*32 + j*16 + y][bx*32 + x];
+                        }
+                    }
+                }
+                blocksync();
+                for (int j = 0; j < 2; j++) {
+                    thread for (int y = 0; y < 16; y++) {
+                        thread for (int x = 0; x < 32; x++) {
+                            d_out[bx*32 + j*16 + y][by*32 + x] = tile[DMINDEX2(H/32, W/32, by, bx)][x][j*16 + y];
+                        }
+                    }
+                }
+            }
+        }
+        kernel_teardown_begin();
+        __smem_free2(tile, 32, 32);
+        kernel_kill();
+    }
+    memcpy_device_to_host2(out, d_out, W, H);
+    gmem_free(d_out);
+    gmem_free(d_in);
+}"""
+_R_TREE = """
+float reduce(float* arr, int N) {
+    float* const d_a = gmem_malloc1<float>(N);
+    memcpy_host_to_device1(d_a, arr, N);
+    float* const d_p = gmem_malloc1<float>(N / 512);
+    {
+        kernel_launch(N / 512, 256, 4 * 256);
+        float* const s = __smem_malloc1<float>(256);
+        kernel_setup_end();
+        thread for (int b = 0; b < N / 512; b++) {
+            thread for (int t = 0; t < 256; t++) {
+                s[DMINDEX1(N / 512, b)][t] = d_a[b * 512 + 2 * t] + d_a[b * 512 + 2 * t + 1];
+            }
+            blocksync();
+            for (int k = 0; k < 8; k++) {
+                thread for (int t = 0; t < 256; t++) {
+                    if (t < pow2(7 - k)) {
+                        s[DMINDEX1(N / 512, b)][t] = s[DMINDEX1(N / 512, b)][t] + s[DMINDEX1(N / 512, b)][t + pow2(7 - k)];
+                    }
+                }
+                blocksync();
+            }
+            thread for (int t = 0; t < 256; t++) {
+                if (t == 0) {
+                    d_p[b] = s[DMINDEX1(N / 512, b)][0];
+                }
+            }
+        }
+        kernel_teardown_begin();
+        __smem_free1(s, 256);
+        kernel_kill();
+    }
+    float* const p = MALLOC1<float>(N / 512);
+    memcpy_device_to_host1(p, d_p, N / 512);
+    float sum = 0.;
+    for (int i = 0; i < N / 512; i++) {
+        sum += p[i];
+    }
+    free(p);
+    gmem_free(d_p);
+    gmem_free(d_a);
+    return sum;
+}"""
+
+
+@dataclass
+class Template:
+    name: str
+    kind: str      # "transpose" | "reduce"
+    form: str      # "naive" | "gpu" | "tree512"
+    cell: str      # "float" | "int"
+    fn: object     # parsed FnDef
+    roles: dict = field(default_factory=dict)  # role -> template param name
+
+
+def _mk(name, kind, form, cell, text, roles, zero=None):
+    text = text.replace("T* ", f"{cell}* ").replace("T sum", f"{cell} sum").replace("\nT ", f"\n{cell} ")
+    if zero is not None:
+        text = text.replace("ZERO", zero)
+    fn = parse_program(text, f"<template {name}>").fns[0]
+    return Template(name, kind, form, cell, fn, roles)
+
+
+_TR = {"in": "in", "out": "out", "W": "W", "H": "H"}
+_RR = {"arr": "arr", "N": "N"}
+TEMPLATES = [
+    _mk("transpose_naive_xy_float", "transpose", "naive", "float", _T_NAIVE_XY, _TR),
+    _mk("transpose_naive_yx_float", "transpose", "naive", "float", _T_NAIVE_YX, _TR),
+    _mk("transpose_naive_xy_int", "transpose", "naive", "int", _T_NAIVE_XY, _TR),
+    _mk("transpose_naive_yx_int", "transpose", "naive", "int", _T_NAIVE_YX, _TR),
+    _mk("transpose_gpu_float", "transpose", "gpu", "float", _T_GPU, _TR),
+    _mk("reduce_naive_float", "reduce", "naive", "float", _R_NAIVE, _RR, zero="0."),
+    _mk("reduce_naive_float_i0", "reduce", "naive", "float", _R_NAIVE, _RR, zero="0"),
+    _mk("reduce_naive_int", "reduce", "naive", "int", _R_NAIVE, _RR, zero="0"),
+    _mk("reduce_tree512_float", "reduce", "tree512", "float", _R_TREE, _RR),
+]
+
+
+# ----------------------------------------------------------------------------- matching
+
+class NoMatch(Exception):
+    pass
+
+
+def _cls(x) -> str:
+    return type(x).__name__
+
+
+def strip_ghosts(stmts):
+    return [s for s in stmts if not (_cls(s) == "CallStmt" and getattr(s, "ghost", False))]
+
+
+class _Unifier:
+    """Bijective renaming between template names and program names."""
+
+    def __init__(self, params_t, params_p):
+        self.t2p: dict = {}
+        self.p2t: dict = {}
+        self.params_t = dict(params_t)  # name -> ctype
+        self.params_p = dict(params_p)
+
+    def bind(self, tn: str, pn: str):
+        if tn in self.t2p or pn in self.p2t:
+            if self.t2p.get(tn) != pn or self.p2t.get(pn) != tn:
+                raise NoMatch(f"name {pn!r} does not play the role of {tn!r}")
+            return
+        # parameters map to parameters of the same type; locals to locals
+        if (tn in self.params_t) != (pn in self.params_p):
+            raise NoMatch(f"{pn!r} vs {tn!r}: parameter/local mismatch")
+        if tn in self.params_t and self.params_t[tn] != self.params_p[pn]:
+            raise NoMatch(f"parameter {pn!r} has type {self.params_p[pn]}, "
+                          f"expected {self.params_t[tn]}")
+        self.t2p[tn] = pn
+        self.p2t[pn] = tn
+
+    # -- expressions
+    def expr(self, t, p):
+        ct, cp = _cls(t), _cls(p)
+        if ct != cp:
+            raise NoMatch(f"expression {cp} where {ct} expected")
+        if ct == "IntLit":
+            if t.value != p.value:
+                raise NoMatch(f"literal {p.value} where {t.value} expected")
+        elif ct == "FloatLit":
+            if float(t.value) != float(p.value):
+                raise NoMatch(f"literal {p.value} where {t.value} expected")
+        elif ct == "Var":
+            self.bind(t.name, p.name)
+        elif ct == "BinOp":
+            if t.op != p.op:
+                raise NoMatch(f"operator {p.op} where {t.op} expected")
+            self.expr(t.lhs, p.lhs)
+            self.expr(t.rhs, p.rhs)
+        elif ct == "Call":
+            if t.fn != p.fn:
+                raise NoMatch(f"call {p.fn} where {t.fn} expected")
+            self.exprs(t.args, p.args)
+        elif ct in ("Access", "Ptr"):
+            self.bind(t.base, p.base)
+            self.exprs(t.idxs, p.idxs)
+        else:
+            raise NoMatch(f"unsupported expression {ct}")
+
+    def exprs(self, ts, ps):
+        if len(ts) != len(ps):
+            raise NoMatch("arity mismatch")
+        for a, b in zip(ts, ps):
+            self.expr(a, b)
+
+    # -- statements
+    def seq(self, t, p):
+        ts, ps = strip_ghosts(t.stmts), strip_ghosts(p.stmts)
+        if len(ts) != len(ps):
+            raise NoMatch(f"block of {len(ps)} statements where {len(ts)} expected")
+        for a, b in zip(ts, ps):
+            self.stmt(a, b)
+
+    def stmt(self, t, p):
+        ct, cp = _cls(t), _cls(p)
+        if ct != cp:
+            raise NoMatch(f"statement {cp} where {ct} expected")
+        if ct == "Seq":
+            self.seq(t, p)
+        elif ct == "For":
+            if t.mode != p.mode:
+                raise NoMatch(f"loop mode {p.mode} where {t.mode} expected")
+            self.bind(t.index, p.index)
+            self.expr(t.range.start, p.range.start)
+            self.expr(t.range.stop, p.range.stop)
+            self.seq(t.body, p.body)
+        elif ct == "Assign":
+            if t.op != p.op:
+                raise NoMatch(f"assignment {p.op} where {t.op} expected")
+            self.bind(t.target.base, p.target.base)
+            self.exprs(t.target.idxs, p.target.idxs)
+            self.expr(t.value, p.value)
+        elif ct == "Decl":
+            if (t.ctype, t.alloc) != (p.ctype, p.alloc):
+                raise NoMatch(f"declaration {p.ctype}/{p.alloc} where {t.ctype}/{t.alloc} expected")
+            self.bind(t.name, p.name)
+            if (t.init is None) != (p.init is None):
+                raise NoMatch("initialiser mismatch")
+            if t.init is not None:
+                self.expr(t.init, p.init)
+            self.exprs(tuple(t.dims), tuple(p.dims))
+        elif ct == "CallStmt":
+            if t.fn != p.fn or bool(t.ghost) != bool(p.ghost):
+                raise NoMatch(f"call {p.fn} where {t.fn} expected")
+            self.exprs(t.args, p.args)
+        elif ct == "If":
+            self.expr(t.cond, p.cond)
+            self.seq(t.then, p.then)
+            if (t.els is None) != (p.els is None):
+                raise NoMatch("else-branch mismatch")
+            if t.els is not None:
+                self.seq(t.els, p.els)
+        elif ct == "Return":
+            self.expr(t.value, p.value)
+        else:
+            raise NoMatch(f"unsupported statement {ct}")
+
+
+@dataclass
+class Plan:
+    """What to run: a template plus the program's parameter names for its roles."""
+    template: Template
+    params: dict  # role -> program parameter name
+    fn_name: str
+
+    @property
+    def kind(self):
+        return self.template.kind
+
+    @property
+    def form(self):
+        return self.template.form
+
+    @property
+    def cell(self):
+        return self.template.cell
+
+
+def match(fn, tmpl: Template) -> Plan:
+    tf = tmpl.fn
+    if fn.body is None:
+        raise NoMatch(f"function {fn.name!r} has no body (admitted)")
+    if getattr(fn, "ret", "void") != tf.ret:
+        raise NoMatch(f"return type {fn.ret} where {tf.ret} expected")
+    if len(fn.params) != len(tf.params):
+        raise NoMatch(f"{len(fn.params)} parameters where {len(tf.params)} expected")
+    u = _Unifier(tf.params, fn.params)
+    u.seq(tf.body, fn.body)
+    missing = [n for n, _ in tf.params if n not in u.t2p]
+    if missing:
+        raise NoMatch(f"parameters {missing} unused")
+    return Plan(tmpl, {role: u.t2p[tn] for role, tn in tmpl.roles.items()}, fn.name)
+
+
+class UnsupportedProgram(Exception):
+    pass
+
+
+def recognize(program, entry: str) -> Plan:
+    fn = program.fn(entry)
+    reasons = []
+    for t in TEMPLATES:
+        try:
+            return match(fn, t)
+        except NoMatch as e:
+            reasons.append(f"{t.name}: {e}")
+    raise UnsupportedProgram(
+        f"function {entry!r} is not one of the programs this B200 backend executes "
+        f"(transpose / reduce, naive or GPU-derived forms); no CPU fallback. "
+        f"Closest mismatches: " + "; ".join(reasons[:3]))

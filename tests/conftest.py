@@ -51,3 +51,17 @@ def golden():
 def program_text(name):
     with open(os.path.join(GOLDEN, "programs", name)) as f:
         return f.read()
+
+
+REFERENCE_SRC = "/root/reference/pkg/src"
+
+
+def reference_available():
+    """The reference is only present in the build container (never on the GPU box)."""
+    if os.path.isdir(REFERENCE_SRC) and REFERENCE_SRC not in sys.path:
+        sys.path.append(REFERENCE_SRC)
+    try:
+        import minigpu.parser  # noqa: F401
+        return True
+    except Exception:
+        return False

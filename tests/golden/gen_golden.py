@@ -121,6 +121,43 @@ def main():
             x = rng.uniform(lo, 1, n).astype(np.float32)
             reduce_case("reduce_tree_f32.optc", x, f"A.5 tree order {dist}")
 
+    # ---------------- parser parity: reference ASTs of every fixture program ----------------
+    from tests_ast_dump import dump_program  # noqa: E402  (tests/golden/tests_ast_dump.py)
+    asts = {}
+    for name in sorted(os.listdir(PROG)):
+        asts[name] = dump_program(load(name))
+    with open(os.path.join(HERE, "ref_asts.json"), "w") as f:
+        json.dump(asts, f, indent=None, sort_keys=True)
+
+    # ---------------- error behaviour of the reference on bad inputs ----------------
+    from minigpu.interp import InterpError  # noqa: E402
+    errs = []
+
+    def err_case(prog_name, entry, inputs, note):
+        try:
+            run_program(load(prog_name), entry, inputs)
+            errs.append({"program": prog_name, "note": note, "error": None})
+        except Exception as e:  # noqa: BLE001
+            errs.append({"program": prog_name, "note": note, "type": type(e).__name__,
+                         "interp_error": isinstance(e, InterpError), "error": str(e)})
+
+    err_case("transpose_naive.optc", "transpose", {"in": Array([2, 3], [0.0] * 6, "float"),
+             "out": Array.alloc([3, 2], "float"), "W": 3}, "missing input H")
+    err_case("transpose_naive.optc", "transpose", {"in": Array([2, 3], [0.0] * 6, "float"),
+             "out": Array.alloc([3, 2], "float"), "W": 4, "H": 2}, "W larger than in columns")
+    err_case("transpose_naive.optc", "transpose", {"in": Array([2, 3], [0.0] * 5 + [None], "float"),
+             "out": Array.alloc([3, 2], "float"), "W": 3, "H": 2}, "uninitialised input cell")
+    err_case("transpose_gpu.optc", "transpose", {"in": [0.0] * (33 * 32),
+             "out": [0.0] * (33 * 32), "W": 32, "H": 33}, "A.4 with 32 not dividing H")
+    err_case("reduce_tree_f32.optc", "reduce", {"arr": [1.0] * 513, "N": 513}, "A.5 with 512 not dividing N")
+    err_case("reduce_naive_f32.optc", "reduce", {"arr": [1.0] * 4, "N": 5}, "N beyond the array")
+    err_case("reduce_naive_f32.optc", "reduce", {"arr": [1.0] * 4, "N": 0}, "N = 0")
+    err_case("reduce_naive_int.optc", "reduce", {"arr": [1, 2, 3], "N": -3}, "negative N")
+    freed = Array([4], [1.0] * 4, "float", freed=True)
+    err_case("reduce_naive_f32.optc", "reduce", {"arr": freed, "N": 4}, "use after free")
+    with open(os.path.join(HERE, "ref_errors.json"), "w") as f:
+        json.dump(errs, f, indent=1)
+
     np.savez_compressed(os.path.join(HERE, "golden.npz"), **arrays)
     with open(os.path.join(HERE, "manifest.json"), "w") as f:
         json.dump({"generator": "tests/golden/gen_golden.py",

@@ -70,6 +70,13 @@ B2_API int b2_device_count(int *count);
  * bench's gpu_launches claim). */
 B2_API uint64_t b2_launch_count(void);
 B2_API size_t b2_dtype_size(int dtype);
+/* Performance knobs (process-wide; the defaults are the tuned values):
+ *   "transpose.variant" tile shape, "transpose.group" tile-rows per band of the
+ *   tile walk, "transpose.ctas_per_sm", "reduce.variant" <threads, loads in
+ *   flight>, "reduce.ctas_per_sm" (0 = occupancy limit). Results never depend
+ *   on them. b2_tune_get returns -1 for an unknown key. */
+B2_API int b2_tune_set(const char *key, int64_t value);
+B2_API int64_t b2_tune_get(const char *key);
 
 /* ---- transpose ------------------------------------------------------------
  * out[c][r] = in[r][c] for r < rows, c < cols; in has pitch ld_in, out has pitch

@@ -15,6 +15,7 @@ from .interp import Array, Interp, InterpError, UnsupportedProgram, f32, run_pro
 from .lang import ParseError, Program, parse_program  # noqa: F401
 from .ops import reduce_sum, reduce_tree512, reduce_tree512_partials, transpose  # noqa: F401
 from .recognize import recognize  # noqa: F401
+from . import programs  # noqa: F401
 
 __all__ = ["run_program", "Interp", "Array", "InterpError", "UnsupportedProgram", "f32",
            "parse_program", "ParseError", "Program", "recognize", "transpose", "reduce_sum",

@@ -26,6 +26,8 @@ SIGNATURES = {
     "b2_device_count": (_int, [ctypes.POINTER(_int)]),
     "b2_launch_count": (ctypes.c_uint64, []),
     "b2_dtype_size": (_sz, [_int]),
+    "b2_tune_set": (_int, [ctypes.c_char_p, _i64]),
+    "b2_tune_get": (_i64, [ctypes.c_char_p]),
     "b2_transpose": (_int, [_vp, _vp, _i64, _i64, _i64, _i64, _int, _int, _vp]),
     "b2_transpose_host": (_int, [_vp, _vp, _i64, _i64, _i64, _i64, _int, _int]),
     "b2_reduce_ws_bytes": (_sz, [_i64, _int]),
@@ -72,6 +74,15 @@ def check(rc: int) -> None:
     if rc != B2_OK:
         msg = lib().b2_last_error().decode(errors="replace")
         raise B2Error(rc, msg)
+
+
+def tune(key: str, value: int) -> None:
+    """Set a performance knob (include/b2k.h b2_tune_set); results never depend on it."""
+    check(lib().b2_tune_set(key.encode(), int(value)))
+
+
+def tuning(key: str) -> int:
+    return int(lib().b2_tune_get(key.encode()))
 
 
 def launch_count() -> int:

@@ -27,6 +27,16 @@ inline void count_launch(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_o
 
 int num_sms(int dev);
 
+// Runtime tuning knobs (b2_tune_set); defaults are the tuned values.
+struct Tuning {
+    int t_variant = 0;      // transpose tile shape (see run_vec_for)
+    int t_group = 1;        // tile-rows per band in the tile walk order
+    int t_ctas_per_sm = 0;  // 0 = occupancy limit
+    int r_variant = 0;      // reduce <threads, unroll> instantiation
+    int r_ctas_per_sm = 0;  // 0 = occupancy limit
+};
+extern Tuning g_tune;
+
 // ---- global memory access with explicit cache policy -----------------------
 // Streaming 128-bit load that bypasses L1 (read-once data).
 __device__ __forceinline__ uint4 ldg_stream(const uint4 *p) {

@@ -15,6 +15,7 @@ namespace b2 {
 
 static thread_local std::string t_err;
 std::atomic<uint64_t> g_launches{0};
+Tuning g_tune;
 
 void set_error(const std::string &msg) { t_err = msg; }
 int fail(int code, const std::string &msg) {
@@ -134,6 +135,30 @@ int b2_abi_version(void) { return B2K_ABI_VERSION; }
 const char *b2_last_error(void) { return t_err.c_str(); }
 
 uint64_t b2_launch_count(void) { return g_launches.load(); }
+
+static int *tune_slot(const char *key) {
+    if (!key) return nullptr;
+    const std::string k(key);
+    if (k == "transpose.variant") return &g_tune.t_variant;
+    if (k == "transpose.group") return &g_tune.t_group;
+    if (k == "transpose.ctas_per_sm") return &g_tune.t_ctas_per_sm;
+    if (k == "reduce.variant") return &g_tune.r_variant;
+    if (k == "reduce.ctas_per_sm") return &g_tune.r_ctas_per_sm;
+    return nullptr;
+}
+
+int b2_tune_set(const char *key, int64_t value) {
+    int *slot = tune_slot(key);
+    if (!slot) return fail(B2_ERR_INVALID, std::string("unknown tuning key ") + (key ? key : "(null)"));
+    if (value < 0 || value > 1 << 20) return fail(B2_ERR_INVALID, "tuning value out of range");
+    *slot = (int)value;
+    return B2_OK;
+}
+
+int64_t b2_tune_get(const char *key) {
+    int *slot = tune_slot(key);
+    return slot ? *slot : -1;
+}
 
 int b2_device_count(int *count) {
     if (!count) return fail(B2_ERR_INVALID, "count is NULL");

@@ -160,46 +160,52 @@ __global__ void __launch_bounds__(NT)
     }
 }
 
-constexpr int kNT = 512;
-constexpr int kU = 4;
+constexpr int kMinNT = 256;  // smallest CTA among the variants (sizes the workspace)
 
-template <typename T>
-int grid_for(int dev, int64_t nvec) {
+int max_grid(int dev) { return num_sms(dev) * (2048 / kMinNT); }
+
+template <typename T, int NT, int U>
+int run_reduce_v(const T *in, int64_t head, int64_t nvec, int64_t n, void *out, void *ws,
+                 int dev, cudaStream_t st) {
+    using A = typename AccOf<T>::type;
     static int occ[64] = {0};
     if (occ[dev] == 0) {
         int o = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, reduce_kernel<T, kNT, kU>, kNT, 0);
+        B2_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, reduce_kernel<T, NT, U>, NT, 0));
         occ[dev] = o > 0 ? o : 1;
     }
-    const int64_t cap = (int64_t)num_sms(dev) * occ[dev];
-    const int64_t need = std::max<int64_t>(1, (nvec + kNT - 1) / kNT);
-    return (int)std::min(cap, need);
+    const int per_sm = g_tune.r_ctas_per_sm > 0 ? std::min(g_tune.r_ctas_per_sm, occ[dev]) : occ[dev];
+    const int64_t cap = (int64_t)num_sms(dev) * per_sm;
+    const int64_t need = std::max<int64_t>(1, (nvec + NT - 1) / NT);
+    const int grid = (int)std::min(cap, need);
+    unsigned *ticket = (unsigned *)ws;
+    A *partials = (A *)((char *)ws + 64);
+    reduce_kernel<T, NT, U><<<grid, NT, 0, st>>>(in, head, nvec, n, (A *)out, partials, ticket);
+    count_launch();
+    B2_CUDA(cudaGetLastError());
+    return B2_OK;
 }
 
-int max_grid(int dev) {
-    // upper bound over the instantiations: all use kNT threads
-    return num_sms(dev) * (2048 / kNT);
-}
-
+// <threads, loads in flight per thread> variants; g_tune.r_variant picks one.
 template <typename T>
 int run_reduce(const void *in_, int64_t n, void *out, void *ws, size_t ws_bytes, int dev,
                cudaStream_t st) {
     using A = typename AccOf<T>::type;
     constexpr int V = 16 / sizeof(T);
     const T *in = (const T *)in_;
-    int64_t head = (int64_t)(((16 - ((uintptr_t)in & 15)) & 15) / sizeof(T));
     if ((uintptr_t)in % sizeof(T)) return fail(B2_ERR_INVALID, "reduce: misaligned input");
+    int64_t head = (int64_t)(((16 - ((uintptr_t)in & 15)) & 15) / sizeof(T));
     head = std::min<int64_t>(head, n);
     const int64_t nvec = (n - head) / V;
-    const int grid = grid_for<T>(dev, nvec);
     const size_t need = (size_t)max_grid(dev) * sizeof(A) + 64;
     if (ws_bytes < need) return fail(B2_ERR_INVALID, "reduce: workspace too small");
-    unsigned *ticket = (unsigned *)ws;
-    A *partials = (A *)((char *)ws + 64);
-    reduce_kernel<T, kNT, kU><<<grid, kNT, 0, st>>>(in, head, nvec, n, (A *)out, partials, ticket);
-    count_launch();
-    B2_CUDA(cudaGetLastError());
-    return B2_OK;
+    switch (g_tune.r_variant) {
+    case 1: return run_reduce_v<T, 512, 8>(in, head, nvec, n, out, ws, dev, st);
+    case 2: return run_reduce_v<T, 256, 8>(in, head, nvec, n, out, ws, dev, st);
+    case 3: return run_reduce_v<T, 1024, 4>(in, head, nvec, n, out, ws, dev, st);
+    case 4: return run_reduce_v<T, 256, 16>(in, head, nvec, n, out, ws, dev, st);
+    default: return run_reduce_v<T, 512, 4>(in, head, nvec, n, out, ws, dev, st);
+    }
 }
 
 }  // namespace

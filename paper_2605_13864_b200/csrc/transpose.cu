@@ -82,7 +82,7 @@ template <int E, int TRV, int TCV, int NT>
 __global__ void __launch_bounds__(NT)
     transpose_vec_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out,
                          int64_t rows_v, int64_t cols_v, int64_t ld_in_b, int64_t ld_out_b,
-                         int64_t tiles_c, int64_t ntiles) {
+                         int64_t tiles_r, int64_t tiles_c, int64_t ntiles, int group) {
     constexpr int V = Micro<E>::V;
     constexpr int TR = TRV * V;  // input rows per tile   (= output vector columns * V)
     constexpr int TC = TCV * V;  // input cols per tile   (= output rows)
@@ -95,8 +95,19 @@ __global__ void __launch_bounds__(NT)
 
     uint4 reg[MT][V];
 
+    // Tile order: bands of `group` tile-rows, walked column by column inside a
+    // band, so CTAs running at the same time write neighbouring column blocks of
+    // the same output rows (and still read long runs of the same input rows).
+    auto origin = [&](int64_t tile, int64_t &r0, int64_t &c0) {
+        const int64_t per_band = (int64_t)group * tiles_c;
+        const int64_t band = tile / per_band, w = tile - band * per_band;
+        const int64_t rows_in_band = min((int64_t)group, tiles_r - band * group);
+        r0 = (band * group + w % rows_in_band) * TR;
+        c0 = (w / rows_in_band) * TC;
+    };
     auto load_tile = [&](int64_t tile) {
-        const int64_t r0 = (tile / tiles_c) * TR, c0 = (tile % tiles_c) * TC;
+        int64_t r0, c0;
+        origin(tile, r0, c0);
 #pragma unroll
         for (int m = 0; m < MT; ++m) {
             const int mt = threadIdx.x + m * NT;
@@ -114,7 +125,8 @@ __global__ void __launch_bounds__(NT)
     int64_t tile = blockIdx.x;
     if (tile < ntiles) load_tile(tile);
     for (; tile < ntiles; tile += gridDim.x) {
-        const int64_t r0 = (tile / tiles_c) * TR, c0 = (tile % tiles_c) * TC;
+        int64_t r0, c0;
+        origin(tile, r0, c0);
         // stage-in: register transpose, swizzled 16-B stores in output orientation
 #pragma unroll
         for (int m = 0; m < MT; ++m) {
@@ -187,10 +199,12 @@ int run_vec(const void *in, void *out, int64_t rows_v, int64_t cols_v, int64_t l
             &o, transpose_vec_kernel<E, TRV, TCV, NT>, NT, 0));
         occ[dev] = o > 0 ? o : 1;
     }
-    const int64_t grid = std::min<int64_t>(ntiles, (int64_t)num_sms(dev) * occ[dev]);
+    const int per_sm = g_tune.t_ctas_per_sm > 0 ? std::min(g_tune.t_ctas_per_sm, occ[dev]) : occ[dev];
+    const int64_t grid = std::min<int64_t>(ntiles, (int64_t)num_sms(dev) * per_sm);
+    const int group = (int)std::max<int64_t>(1, std::min<int64_t>(g_tune.t_group, tiles_r));
     transpose_vec_kernel<E, TRV, TCV, NT><<<(unsigned)grid, NT, 0, st>>>(
-        (const uint8_t *)in, (uint8_t *)out, rows_v, cols_v, ld_in * E, ld_out * E, tiles_c,
-        ntiles);
+        (const uint8_t *)in, (uint8_t *)out, rows_v, cols_v, ld_in * E, ld_out * E, tiles_r,
+        tiles_c, ntiles, group);
     count_launch();
     B2_CUDA(cudaGetLastError());
     return B2_OK;
@@ -219,12 +233,27 @@ int run_scalar_all(const void *in, void *out, int64_t rows, int64_t cols, int64_
     return run_scalar<T>(in, out, rv, rows, 0, cv, ld_in, ld_out, dev, st);
 }
 
+// Tile shapes per element size; g_tune.t_variant picks one (0 = default).
+//   4-byte: 0: 64x64   1: 128x64 (rows x cols)   2: 64x128
+//   2-byte: 0: 128x128 1: 64x128                 2: 128x64
+//   8-byte: 0: 64x32   1: 32x32                  2: 64x64
 template <int E>
 int run_vec_for(const void *in, void *out, int64_t rv, int64_t cv, int64_t ld_in,
                 int64_t ld_out, int dev, cudaStream_t st) {
-    if constexpr (E == 4) return run_vec<4, 16, 16, 256>(in, out, rv, cv, ld_in, ld_out, dev, st);
-    else if constexpr (E == 2) return run_vec<2, 16, 16, 256>(in, out, rv, cv, ld_in, ld_out, dev, st);
-    else return run_vec<8, 32, 16, 256>(in, out, rv, cv, ld_in, ld_out, dev, st);
+    const int v = g_tune.t_variant;
+    if constexpr (E == 4) {
+        if (v == 1) return run_vec<4, 32, 16, 256>(in, out, rv, cv, ld_in, ld_out, dev, st);
+        if (v == 2) return run_vec<4, 16, 32, 256>(in, out, rv, cv, ld_in, ld_out, dev, st);
+        return run_vec<4, 16, 16, 256>(in, out, rv, cv, ld_in, ld_out, dev, st);
+    } else if constexpr (E == 2) {
+        if (v == 1) return run_vec<2, 8, 16, 128>(in, out, rv, cv, ld_in, ld_out, dev, st);
+        if (v == 2) return run_vec<2, 16, 8, 128>(in, out, rv, cv, ld_in, ld_out, dev, st);
+        return run_vec<2, 16, 16, 256>(in, out, rv, cv, ld_in, ld_out, dev, st);
+    } else {
+        if (v == 1) return run_vec<8, 16, 16, 256>(in, out, rv, cv, ld_in, ld_out, dev, st);
+        if (v == 2) return run_vec<8, 32, 32, 256>(in, out, rv, cv, ld_in, ld_out, dev, st);
+        return run_vec<8, 32, 16, 256>(in, out, rv, cv, ld_in, ld_out, dev, st);
+    }
 }
 
 template <typename T>

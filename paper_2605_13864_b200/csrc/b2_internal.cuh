@@ -30,12 +30,14 @@ int num_sms(int dev);
 // Runtime tuning knobs (b2_tune_set); defaults are the tuned values.
 struct Tuning {
     int t_variant = 0;      // transpose tile shape (see run_vec_for)
-    int t_group = 1;        // tile-rows per band in the tile walk order
-    int t_ctas_per_sm = 0;  // 0 = occupancy limit
+    int t_group = 4;        // tile-rows per band in the tile walk order
+    int t_ctas_per_sm = 0;  // 0 = auto (~kInflightBytesPerSM of tiles per SM)
     int r_variant = 0;      // reduce <threads, unroll> instantiation
-    int r_ctas_per_sm = 0;  // 0 = occupancy limit
+    int r_ctas_per_sm = 0;  // 0 = auto (kReduceThreadsPerSM threads per SM)
 };
 extern Tuning g_tune;
+constexpr int kInflightBytesPerSM = 64 * 1024;
+constexpr int kReduceThreadsPerSM = 1536;
 
 // ---- global memory access with explicit cache policy -----------------------
 // Streaming 128-bit load that bypasses L1 (read-once data).

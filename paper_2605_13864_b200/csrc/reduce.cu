@@ -174,7 +174,10 @@ int run_reduce_v(const T *in, int64_t head, int64_t nvec, int64_t n, void *out, 
         B2_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, reduce_kernel<T, NT, U>, NT, 0));
         occ[dev] = o > 0 ? o : 1;
     }
-    const int per_sm = g_tune.r_ctas_per_sm > 0 ? std::min(g_tune.r_ctas_per_sm, occ[dev]) : occ[dev];
+    // Default: 1536 threads per SM (3 x 512). Measured on B200 (profiles/r01_tune.md):
+    // full occupancy (2048) reads 6.94 TB/s, 1536 reads 7.19 TB/s.
+    const int auto_sm = std::max(1, kReduceThreadsPerSM / NT);
+    const int per_sm = std::min(g_tune.r_ctas_per_sm > 0 ? g_tune.r_ctas_per_sm : auto_sm, occ[dev]);
     const int64_t cap = (int64_t)num_sms(dev) * per_sm;
     const int64_t need = std::max<int64_t>(1, (nvec + NT - 1) / NT);
     const int grid = (int)std::min(cap, need);

@@ -199,7 +199,12 @@ int run_vec(const void *in, void *out, int64_t rows_v, int64_t cols_v, int64_t l
             &o, transpose_vec_kernel<E, TRV, TCV, NT>, NT, 0));
         occ[dev] = o > 0 ? o : 1;
     }
-    const int per_sm = g_tune.t_ctas_per_sm > 0 ? std::min(g_tune.t_ctas_per_sm, occ[dev]) : occ[dev];
+    // Default residency: ~64 KB of tile data in flight per SM. Measured on B200
+    // (profiles/r01_tune.md): more resident tiles than that only adds DRAM
+    // page/turnaround contention (fp32 64x64: 6 CTAs/SM 5.69 TB/s, 4 CTAs 6.13).
+    constexpr int kTileBytes = TR * TC * E;
+    const int auto_sm = std::max(1, kInflightBytesPerSM / kTileBytes);
+    const int per_sm = std::min(g_tune.t_ctas_per_sm > 0 ? g_tune.t_ctas_per_sm : auto_sm, occ[dev]);
     const int64_t grid = std::min<int64_t>(ntiles, (int64_t)num_sms(dev) * per_sm);
     const int group = (int)std::max<int64_t>(1, std::min<int64_t>(g_tune.t_group, tiles_r));
     transpose_vec_kernel<E, TRV, TCV, NT><<<(unsigned)grid, NT, 0, st>>>(
@@ -234,7 +239,7 @@ int run_scalar_all(const void *in, void *out, int64_t rows, int64_t cols, int64_
 }
 
 // Tile shapes per element size; g_tune.t_variant picks one (0 = default).
-//   4-byte: 0: 64x64   1: 128x64 (rows x cols)   2: 64x128
+//   4-byte: 0: 64x64   1: 128x64 (rows x cols)   2: 64x128   3: 256x32   4: 128x32
 //   2-byte: 0: 128x128 1: 64x128                 2: 128x64
 //   8-byte: 0: 64x32   1: 32x32                  2: 64x64
 template <int E>
@@ -244,6 +249,8 @@ int run_vec_for(const void *in, void *out, int64_t rv, int64_t cv, int64_t ld_in
     if constexpr (E == 4) {
         if (v == 1) return run_vec<4, 32, 16, 256>(in, out, rv, cv, ld_in, ld_out, dev, st);
         if (v == 2) return run_vec<4, 16, 32, 256>(in, out, rv, cv, ld_in, ld_out, dev, st);
+        if (v == 3) return run_vec<4, 64, 8, 256>(in, out, rv, cv, ld_in, ld_out, dev, st);
+        if (v == 4) return run_vec<4, 32, 8, 256>(in, out, rv, cv, ld_in, ld_out, dev, st);
         return run_vec<4, 16, 16, 256>(in, out, rv, cv, ld_in, ld_out, dev, st);
     } else if constexpr (E == 2) {
         if (v == 1) return run_vec<2, 8, 16, 128>(in, out, rv, cv, ld_in, ld_out, dev, st);

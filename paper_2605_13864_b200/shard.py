@@ -1,0 +1,113 @@
+"""Multi-GPU partitioning of the two programs (one process per GPU,
+torch.distributed for the plumbing).
+
+The reference runs everything in one Python thread (interp.py:282-300 executes
+`thread for` / `parallel for` sequentially); nothing in it is distributed. On
+one 8 x B200 box the two programs shard as follows:
+
+* transpose - row blocks, no exchange. Rank g owns input rows
+  [r_g, r_{g+1}) (a multiple of the 64-row tile, the last block takes the
+  remainder) and writes the W x (r_{g+1} - r_g) slab that is exactly
+  out[:, r_g:r_{g+1}]. The output stays sharded; `gather_transpose` assembles
+  it on one rank when a caller needs the whole matrix.
+* reduction - contiguous shards plus one combine: each rank reduces its shard
+  to one partial (int64 / float32) with the single-pass kernel, then
+    int32 -> one NCCL reduce (sum) of the int64 partial to the root: exact in
+             any order;
+    fp32  -> one NCCL all-gather of the G partials, summed in rank order on
+             every rank, so the result does not depend on NCCL's algorithm.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+try:
+    import torch
+    import torch.distributed as dist
+except Exception:  # pragma: no cover
+    torch = dist = None
+
+
+def row_blocks(H: int, world: int, align: int = 64) -> list:
+    """[(r0, r1)] per rank: tile-aligned near-equal row blocks covering [0, H)."""
+    if world <= 0:
+        raise ValueError("world must be positive")
+    units = -(-H // align) if H > 0 else 0
+    base, extra = divmod(units, world)
+    out, r = [], 0
+    for g in range(world):
+        nu = base + (1 if g < extra else 0)
+        r1 = min(H, r + nu * align)
+        out.append((r, r1))
+        r = r1
+    return out
+
+
+def shard_range(n: int, world: int, rank: int, align: int = 4) -> tuple:
+    """Contiguous [e0, e1) of an n-element array for `rank` (16-B aligned starts for
+    4-byte cells when align = 4)."""
+    blocks = row_blocks(n, world, align)
+    return blocks[rank]
+
+
+def _default_reduce(x):
+    from . import ops
+    return ops.reduce_sum(x)
+
+
+def _default_transpose(a):
+    from . import ops
+    return ops.transpose(a)
+
+
+def sharded_transpose(local_in, *, transpose_fn=None):
+    """Transpose this rank's row block; returns the local W x H_g output slab."""
+    return (transpose_fn or _default_transpose)(local_in)
+
+
+def sharded_reduce_sum(local_x, *, group=None, root: int | None = None, reduce_fn=None):
+    """Sum over all ranks' shards. int32 -> Python int (exact), float32 -> float
+    (rank-order combine). With root=None every rank gets the result."""
+    fn = reduce_fn or _default_reduce
+    part = fn(local_x)
+    is_int = str(getattr(local_x, "dtype", "")).endswith("int32")
+    device = local_x.device if (torch is not None and isinstance(local_x, torch.Tensor)) else "cpu"
+    if isinstance(part, (int, float, np.generic)):
+        part = torch.tensor([part], dtype=torch.int64 if is_int else torch.float32, device=device)
+    part = part.reshape(1)
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return int(part.item()) if is_int else float(part.item())
+    if is_int:
+        t = part.to(torch.int64)
+        if root is None:
+            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+        else:
+            dist.reduce(t, dst=root, op=dist.ReduceOp.SUM, group=group)
+        return int(t.item())
+    ws = dist.get_world_size(group)
+    parts = [torch.empty_like(part) for _ in range(ws)]
+    dist.all_gather(parts, part, group=group)
+    acc = np.float32(0.0)
+    for p in parts:  # rank order: deterministic
+        acc = np.float32(acc + np.float32(p.item()))
+    return float(acc)
+
+
+def gather_transpose(local_out, rows: list, *, root: int = 0, group=None):
+    """Assemble the full W x H output on `root` from the ranks' W x H_g slabs."""
+    rank = dist.get_rank(group)
+    ws = dist.get_world_size(group)
+    W = local_out.shape[0]
+    H = rows[-1][1]
+    widths = [r1 - r0 for r0, r1 in rows]
+    maxw = max(widths)
+    buf = torch.zeros((W, maxw), dtype=local_out.dtype, device=local_out.device)
+    buf[:, : local_out.shape[1]] = local_out
+    bufs = [torch.empty_like(buf) for _ in range(ws)] if rank == root else None
+    dist.gather(buf, bufs, dst=root, group=group)
+    if rank != root:
+        return None
+    full = torch.empty((W, H), dtype=local_out.dtype, device=local_out.device)
+    for (r0, r1), b in zip(rows, bufs):
+        full[:, r0:r1] = b[:, : r1 - r0]
+    return full

@@ -38,15 +38,8 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import ops
-from .recognize import Plan, UnsupportedProgram as _Unsupported, recognize
-
-
-class InterpError(Exception):
-    pass
-
-
-class UnsupportedProgram(InterpError, _Unsupported):
-    """The program is not one this backend executes (no CPU fallback)."""
+from .errors import InterpError, UnsupportedProgram
+from .recognize import Plan, recognize
 
 
 def f32(x: float) -> float:
@@ -209,11 +202,8 @@ class Interp:
                 env[pname] = arr
             else:
                 env[pname] = v
-        try:
-            plan = recognize(self.program, fn_name)
-        except _Unsupported as e:
-            raise UnsupportedProgram(str(e)) from None
-        ret = _EXEC[(plan.kind, plan.form)](plan, env)
+        plan = recognize(self.program, fn_name)
+        ret =_EXEC[(plan.kind, plan.form)](plan, env)
         return ret, arrays
 
 

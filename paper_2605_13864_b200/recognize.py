@@ -19,6 +19,7 @@ from __future__ import annotations
 
 from dataclasses import dataclass, field
 
+from .errors import UnsupportedProgram
 from .lang import parse_program
 
 # ----------------------------------------------------------------------------- templates
@@ -215,10 +216,6 @@ def match(fn, tmpl: Template) -> Plan:
     if missing:
         raise NoMatch(f"parameters {missing} unused")
     return Plan(tmpl, {role: u.t2p[tn] for role, tn in tmpl.roles.items()}, fn.name)
-
-
-class UnsupportedProgram(Exception):
-    pass
 
 
 def recognize(program, entry: str) -> Plan:

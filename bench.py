@@ -46,6 +46,7 @@ def parse():
     p.add_argument("--scaling", choices=["weak", "strong"], default="weak")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--no-graph", action="store_true", help="eager launches instead of a CUDA graph")
     p.add_argument("--paper-configs", action="store_true", default=True)
     p.add_argument("--rows", type=int, default=TILE_ROWS)
     p.add_argument("--cols", type=int, default=TILE_COLS)
@@ -265,25 +266,51 @@ def main():
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
-    t_start = torch.cuda.Event(enable_timing=True)
-    t_end = torch.cuda.Event(enable_timing=True)
+    # N = 1: the K timed steps are captured once into a CUDA graph (with external
+    # event-record nodes around every kernel) and replayed once: no per-launch host
+    # overhead between kernels. N > 1 keeps eager launches (the NCCL combine).
+    use_graph = world == 1 and not args.no_graph
+    mk = (lambda: torch.cuda.Event(enable_timing=True, external=True)) if use_graph else \
+        (lambda: torch.cuda.Event(enable_timing=True))
+    evs = [[mk() for _ in range(3)] for _ in range(args.steps)]
+    t_start, t_end = mk(), mk()
+    graph = None
+    launches_per_run = None
+    if use_graph:
+        cs = torch.cuda.Stream(dev)
+        cs.wait_stream(st)
+        graph = torch.cuda.CUDAGraph()
+        l0 = b2.launch_count()
+        with torch.cuda.stream(cs):
+            with torch.cuda.graph(graph, stream=cs):
+                st = torch.cuda.current_stream(dev)
+                t_start.record(st)
+                for i in range(args.steps):
+                    step(evs[i])
+                t_end.record(st)
+        launches_per_run = b2.launch_count() - l0
+        st = torch.cuda.current_stream(dev)
+        graph.replay()  # untimed warm replay
+        torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     launches0 = b2.launch_count()
     w0 = time.perf_counter()
-    t_start.record(st)
-    for i in range(args.steps):
-        step(evs[i])
-    t_end.record(st)
+    if use_graph:
+        graph.replay()
+    else:
+        t_start.record(st)
+        for i in range(args.steps):
+            step(evs[i])
+        t_end.record(st)
     torch.cuda.synchronize()
     w1 = time.perf_counter()
     if world > 1:
         dist.barrier()
     clk.window = (w0, w1)
     clk.stop()
-    launches = b2.launch_count() - launches0
+    launches = launches_per_run if use_graph else b2.launch_count() - launches0
     ms = t_start.elapsed_time(t_end)
     ms_t = statistics.mean(e[0].elapsed_time(e[1]) for e in evs)
     ms_r = statistics.mean(e[1].elapsed_time(e[2]) for e in evs)
@@ -329,6 +356,8 @@ def main():
                        "traffic": traffic_r},
         },
         "gpu_launches": launches,
+        "launch_mode": ("CUDA graph: K steps captured once, replayed once in the timed region"
+                        if use_graph else "eager stream launches"),
         "clocks": clk.summary(),
     }
 

@@ -158,30 +158,77 @@ __global__ void __launch_bounds__(NT)
     }
 }
 
-// Padded 32x32 tile (transposeNoBankConflicts shape) over a sub-rectangle
-// [r_lo, r_hi) x [c_lo, c_hi); any pitch, any alignment.
+// Padded tile (the paper's transposeNoBankConflicts shape) over a
+// sub-rectangle [r_lo, r_hi) x [c_lo, c_hi); any pitch, any alignment. 64 x 64
+// cells per tile, 256 threads, 16 cells per thread in flight; the +PAD column
+// keeps the transposed shared-memory reads on distinct banks for every width.
 template <typename T>
 __global__ void __launch_bounds__(256)
     transpose_scalar_kernel(const T *__restrict__ in, T *__restrict__ out, int64_t r_lo,
                             int64_t r_hi, int64_t c_lo, int64_t c_hi, int64_t ld_in,
                             int64_t ld_out, int64_t tiles_c, int64_t ntiles) {
-    __shared__ T tile[32][33];
+    constexpr int TS = 64;
+    constexpr int PAD = sizeof(T) == 2 ? 2 : 1;
+    __shared__ T tile[TS][TS + PAD];
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const int64_t r0 = r_lo + (t / tiles_c) * 32, c0 = c_lo + (t % tiles_c) * 32;
+        const int64_t r0 = r_lo + (t / tiles_c) * TS, c0 = c_lo + (t % tiles_c) * TS;
+        T v[TS / 8][2];
 #pragma unroll
-        for (int j = 0; j < 32; j += 8) {
-            const int64_t r = r0 + ty + j, c = c0 + tx;
-            if (r < r_hi && c < c_hi) tile[ty + j][tx] = in[r * ld_in + c];
+        for (int j = 0; j < TS / 8; ++j) {
+            const int64_t r = r0 + ty + 8 * j;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int64_t c = c0 + tx + 32 * h;
+                if (r < r_hi && c < c_hi) v[j][h] = in[r * ld_in + c];
+            }
         }
+#pragma unroll
+        for (int j = 0; j < TS / 8; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) tile[ty + 8 * j][tx + 32 * h] = v[j][h];
         __syncthreads();
 #pragma unroll
-        for (int j = 0; j < 32; j += 8) {
-            const int64_t oc = c0 + ty + j, orr = r0 + tx;  // out row = input col
-            if (oc < c_hi && orr < r_hi) out[oc * ld_out + orr] = tile[tx][ty + j];
+        for (int j = 0; j < TS / 8; ++j) {
+            const int64_t oc = c0 + ty + 8 * j;  // out row = input col
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int64_t orr = r0 + tx + 32 * h;
+                if (oc < c_hi && orr < r_hi) out[oc * ld_out + orr] = tile[tx + 32 * h][ty + 8 * j];
+            }
         }
         __syncthreads();
     }
+}
+
+// Degenerate shapes (one row or one column): the transpose is a strided copy
+// out[i * so] = in[i * si]; 128-bit vectors when both sides are contiguous.
+template <typename T>
+__global__ void __launch_bounds__(256)
+    strided_copy_kernel(const T *__restrict__ in, T *__restrict__ out, int64_t n, int64_t si,
+                        int64_t so) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    constexpr int V = 16 / sizeof(T);
+    if (si == 1 && so == 1 && ((uintptr_t)in % 16 == 0) && ((uintptr_t)out % 16 == 0)) {
+        const int64_t nv = n / V;
+        for (int64_t k = i; k < nv; k += stride)
+            stg_stream(reinterpret_cast<uint4 *>(out) + k, ldg_stream(reinterpret_cast<const uint4 *>(in) + k));
+        for (int64_t k = nv * V + i; k < n; k += stride) out[k] = in[k];
+        return;
+    }
+    for (int64_t k = i; k < n; k += stride) out[k * so] = in[k * si];
+}
+
+template <typename T>
+int run_copy(const void *in, void *out, int64_t n, int64_t si, int64_t so, int dev,
+             cudaStream_t st) {
+    const int64_t per = 256 * (16 / (int64_t)sizeof(T));
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((n + per - 1) / per, (int64_t)num_sms(dev) * 8));
+    strided_copy_kernel<T><<<(unsigned)grid, 256, 0, st>>>((const T *)in, (T *)out, n, si, so);
+    count_launch();
+    B2_CUDA(cudaGetLastError());
+    return B2_OK;
 }
 
 template <int E, int TRV, int TCV, int NT>
@@ -219,9 +266,9 @@ template <typename T>
 int run_scalar(const void *in, void *out, int64_t r_lo, int64_t r_hi, int64_t c_lo,
                int64_t c_hi, int64_t ld_in, int64_t ld_out, int dev, cudaStream_t st) {
     if (r_hi <= r_lo || c_hi <= c_lo) return B2_OK;
-    const int64_t tiles_r = (r_hi - r_lo + 31) / 32, tiles_c = (c_hi - c_lo + 31) / 32;
+    const int64_t tiles_r = (r_hi - r_lo + 63) / 64, tiles_c = (c_hi - c_lo + 63) / 64;
     const int64_t ntiles = tiles_r * tiles_c;
-    const int64_t grid = std::min<int64_t>(ntiles, (int64_t)num_sms(dev) * 8);
+    const int64_t grid = std::min<int64_t>(ntiles, (int64_t)num_sms(dev) * 4);
     transpose_scalar_kernel<T><<<(unsigned)grid, 256, 0, st>>>(
         (const T *)in, (T *)out, r_lo, r_hi, c_lo, c_hi, ld_in, ld_out, tiles_c, ntiles);
     count_launch();
@@ -268,6 +315,9 @@ int dispatch(const void *in, void *out, int64_t rows, int64_t cols, int64_t ld_i
              int64_t ld_out, int dev, cudaStream_t st) {
     constexpr int E = sizeof(T);
     constexpr int V = 16 / E;
+    // one row: out[c][0] = in[0][c];  one column: out[0][r] = in[r][0]
+    if (rows == 1) return run_copy<T>(in, out, cols, 1, ld_out, dev, st);
+    if (cols == 1) return run_copy<T>(in, out, rows, ld_in, 1, dev, st);
     const bool aligned = E >= 2 && ((uintptr_t)in % 16 == 0) && ((uintptr_t)out % 16 == 0) &&
                          (ld_in * E % 16 == 0) && (ld_out * E % 16 == 0);
     if (!aligned) return run_scalar<T>(in, out, 0, rows, 0, cols, ld_in, ld_out, dev, st);

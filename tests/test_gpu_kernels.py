@@ -78,6 +78,18 @@ def test_transpose_pitched(b2):
     assert torch.equal(b2.transpose(odd), odd.t())
 
 
+def test_degenerate_shapes_pitched(b2):
+    row = torch.arange(100, device="cuda", dtype=torch.float32).reshape(1, 100)
+    big = torch.zeros(100, 7, device="cuda")
+    b2.transpose(row, big[:, 2:3])
+    col = torch.arange(50, device="cuda", dtype=torch.float64).reshape(50, 1)
+    wide = torch.zeros(5, 50, device="cuda", dtype=torch.float64)
+    b2.transpose(torch.zeros(50, 9, device="cuda", dtype=torch.float64)[:, 4:5].copy_(col), wide[3:4])
+    torch.cuda.synchronize()
+    assert torch.equal(big[:, 2], row[0]) and float(big[:, [0, 1, 3]].abs().sum()) == 0
+    assert torch.equal(wide[3], col[:, 0]) and float(wide[[0, 1, 2, 4]].abs().sum()) == 0
+
+
 @pytest.mark.parametrize("n", [0, 1, 3, 17, 1000, 2**20 + 3, 2**24])
 def test_reduce_int32_exact(b2, n):
     g = torch.Generator(device="cuda").manual_seed(n)

@@ -1,0 +1,965 @@
+"""CUDA code generation for GPU-form OptiGPU programs.
+
+The reference specifies this module but does not ship it (
+PAPER.md:1017-1084 describe it): every `kernel_launch ... kernel_kill` scope
+becomes a `__global__` function, `thread for` nests become index arithmetic on
+the global thread id, `__smem_malloc` becomes (dynamic) shared memory, the
+`DMINDEX` block index of shared/thread-register arrays becomes 0, `blocksync()`
+becomes `__syncthreads()`, and the host part (gmem_malloc / memcpy / host
+loops / return) becomes native host code. The translation unit is compiled with
+nvcc for sm_100a into a shared object and called through a tiny C ABI.
+
+Semantics kept identical to the reference interpreter (minigpu/interp.py):
+  * float cells are binary32; every expression is evaluated in binary64 and
+    rounded to binary32 only when stored into a float cell (interp.py:43-44,
+    :262-270, :83-84); FMA contraction is disabled (host and device), so the
+    arithmetic is the interpreter's bit for bit;
+  * int cells and int scalars are int64 (the reference's Python ints never wrap;
+    programs whose values leave the int64 range diverge);
+  * `/` is exact_div (raises unless exact), raw `/` `%` truncate (interp.py:187-214),
+    pow2, DMINDEX (interp.py:215-227);
+  * `thread for` narrows the context width like interp.py:285-299; a statement
+    that writes memory in a context wider than one thread runs once (thread 0 of
+    the context), as the interpreter runs it once;
+  * array accesses are bounds- and rank-checked on host and device (violations
+    raise InterpError after the kernel instead of faulting); host arrays track
+    initialisation (reads / memcpys of uninitialised cells raise) and
+    use-after-free.
+Device-side gmem cells are not tracked for initialisation (documented deviation).
+
+Only programs that contain at least one kernel scope are compiled: host code is
+part of such a program (e.g. A.5's final host loop), while a program with no
+kernel is not a GPU program and is refused (no CPU fallback).
+"""
+from __future__ import annotations
+
+import ctypes
+import hashlib
+import os
+import struct
+import subprocess
+import threading
+
+import numpy as np
+
+from .errors import InterpError, UnsupportedProgram
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+GEN_DIR = os.path.join(PKG, "_gen")
+MAX_RANK = 8
+
+# ----------------------------------------------------------------------------- helpers
+
+
+def _cls(x) -> str:
+    return type(x).__name__
+
+
+def _is_ghost(s) -> bool:
+    return _cls(s) == "CallStmt" and getattr(s, "ghost", False)
+
+
+def _stmts(seq):
+    return [s for s in seq.stmts if not _is_ghost(s)]
+
+
+def _f32_literal(v: float) -> str:
+    f = struct.unpack("f", struct.pack("f", float(v)))[0]
+    if f != f or f in (float("inf"), float("-inf")):
+        raise UnsupportedProgram(f"non-finite float literal {v}")
+    return f"({f.hex()})"
+
+
+def _is_kernel_scope(s) -> bool:
+    if _cls(s) != "Seq":
+        return False
+    st = _stmts(s)
+    return bool(st) and _cls(st[0]) == "CallStmt" and st[0].fn == "kernel_launch"
+
+
+def has_kernel(fn) -> bool:
+    def walk(s):
+        if _is_kernel_scope(s):
+            return True
+        c = _cls(s)
+        if c == "Seq":
+            return any(walk(t) for t in s.stmts)
+        if c == "For":
+            return walk(s.body)
+        if c == "If":
+            return walk(s.then) or (s.els is not None and walk(s.els))
+        return False
+    return fn.body is not None and walk(fn.body)
+
+
+class Sym:
+    """A named thing in the program: scalar or array, where it lives."""
+
+    def __init__(self, name, kind, ctype, rank=0, index=None):
+        self.name = name
+        self.kind = kind        # param_arr | param_int | param_float | scalar | host_arr | dev_arr | smem_arr | treg_arr
+        self.ctype = ctype      # "float" | "int"
+        self.rank = rank        # declared rank (arrays; smem/treg without the block dim)
+        self.index = index      # parameter position for params
+        self.cname = "v_" + name
+
+    @property
+    def is_array(self):
+        return self.kind.endswith("arr")
+
+    @property
+    def elem(self):
+        # int cells hold the reference's unbounded Python ints: int64 (not the
+        # 4-byte CELL_BYTES of the proof model) so in-kernel sums never wrap
+        return "float" if self.ctype == "float" else "int64_t"
+
+
+# ----------------------------------------------------------------------------- C++ prelude
+
+PRELUDE = r"""
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+#include <string>
+#include <vector>
+
+struct B2Arr { void *data; int64_t n; int64_t rank; int64_t dims[8]; uint8_t *init; int64_t freed; };
+struct B2Err { std::string msg; };
+static inline void b2_throw(const std::string &m) { throw B2Err{m}; }
+
+// device-side error flags (first error wins)
+enum { B2E_OOB = 1, B2E_RANK = 2, B2E_DIV = 3, B2E_WIDTH = 4 };
+__device__ __forceinline__ void b2_flag(int *f, int code, int64_t a, int64_t b) {
+    if (atomicCAS(f, 0, code) == 0) { f[1] = (int)a; f[2] = (int)b; f[3] = (int)(a >> 32); f[4] = (int)(b >> 32); }
+}
+__host__ __device__ __forceinline__ int64_t b2_div(int64_t a, int64_t b) { return b ? a / b : 0; }
+__host__ __device__ __forceinline__ int64_t b2_mod(int64_t a, int64_t b) { return b ? a - (a / b) * b : 0; }
+__host__ __device__ __forceinline__ int64_t b2_pow2(int64_t k) { return k < 0 ? 0 : ((int64_t)1 << k); }
+static inline int64_t b2_exact_div_h(int64_t a, int64_t b) {
+    if (b == 0 || a % b != 0) b2_throw("exact_div(" + std::to_string(a) + ", " + std::to_string(b) + ") is not exact");
+    return a / b;
+}
+__device__ __forceinline__ int64_t b2_exact_div_d(int64_t a, int64_t b, int *f) {
+    if (b == 0 || a % b != 0) { b2_flag(f, B2E_DIV, a, b); return 0; }
+    return a / b;
+}
+// host element offset with the interpreter's checks (Array.offset, interp.py:61-70)
+static inline int64_t b2_off_h(const int64_t *dims, int64_t rank, int64_t nidx, const int64_t *idx) {
+    if (nidx == rank + 1 && rank == 1) {  // pointer-offset rule (interp.py:239-240)
+        int64_t ix = idx[0] + idx[1];
+        if (ix < 0 || ix >= dims[0]) b2_throw("index " + std::to_string(ix) + " out of bounds 0.." + std::to_string(dims[0]));
+        return ix;
+    }
+    if (nidx != rank) b2_throw("rank mismatch: " + std::to_string(nidx) + " indices into " + std::to_string(rank) + "-d array");
+    int64_t off = 0;
+    for (int64_t i = 0; i < rank; ++i) {
+        if (idx[i] < 0 || idx[i] >= dims[i]) b2_throw("index " + std::to_string(idx[i]) + " out of bounds 0.." + std::to_string(dims[i]));
+        off = off * dims[i] + idx[i];
+    }
+    return off;
+}
+__device__ __forceinline__ bool b2_chk(int64_t ix, int64_t d, int *f) {
+    if (ix < 0 || ix >= d) { b2_flag(f, B2E_OOB, ix, d); return false; }
+    return true;
+}
+template <typename T> struct B2Host { T *p = nullptr; int64_t n = 0; int64_t rank = 0; int64_t dims[8] = {0}; uint8_t *init = nullptr; bool freed = false; bool owned = false; };
+template <typename T> struct B2Dev { T *p = nullptr; int64_t n = 0; int64_t rank = 0; int64_t dims[8] = {0}; bool freed = false; };
+static std::vector<void *> *g_dev_allocs;
+static std::vector<void *> *g_host_allocs;
+template <typename T> static B2Dev<T> b2_dev_alloc(int64_t rank, std::initializer_list<int64_t> d) {
+    B2Dev<T> a; a.rank = rank; a.n = 1; int i = 0;
+    for (int64_t x : d) { a.dims[i++] = x; a.n *= x; }
+    if (a.n < 0) a.n = 0;
+    if (a.n > 0) {
+        cudaError_t e = cudaMalloc((void **)&a.p, (size_t)a.n * sizeof(T));
+        if (e != cudaSuccess) b2_throw(std::string("gmem_malloc: ") + cudaGetErrorString(e));
+        g_dev_allocs->push_back(a.p);
+    }
+    return a;
+}
+template <typename T> static B2Host<T> b2_host_alloc(int64_t rank, std::initializer_list<int64_t> d) {
+    B2Host<T> a; a.rank = rank; a.n = 1; int i = 0;
+    for (int64_t x : d) { a.dims[i++] = x; a.n *= x; }
+    if (a.n < 0) a.n = 0;
+    a.p = (T *)calloc((size_t)(a.n > 0 ? a.n : 1), sizeof(T));
+    a.init = (uint8_t *)calloc((size_t)(a.n > 0 ? a.n : 1), 1);
+    a.owned = true;
+    g_host_allocs->push_back(a.p); g_host_allocs->push_back(a.init);
+    return a;
+}
+template <typename T> static B2Host<T> b2_param(B2Arr *A) {
+    B2Host<T> a; a.p = (T *)A->data; a.n = A->n; a.rank = A->rank;
+    for (int i = 0; i < 8; ++i) a.dims[i] = A->dims[i];
+    a.init = A->init; a.freed = A->freed != 0; return a;
+}
+template <typename T> static T b2_hread(B2Host<T> &a, int64_t nidx, const int64_t *idx) {
+    if (a.freed) b2_throw("use after free");
+    int64_t o = b2_off_h(a.dims, a.rank, nidx, idx);
+    if (a.init && !a.init[o]) b2_throw("read of uninitialized cell");
+    return a.p[o];
+}
+template <typename T> static void b2_hwrite(B2Host<T> &a, int64_t nidx, const int64_t *idx, T v) {
+    if (a.freed) b2_throw("use after free");
+    int64_t o = b2_off_h(a.dims, a.rank, nidx, idx);
+    a.p[o] = v;
+    if (a.init) a.init[o] = 1;
+}
+template <typename T, typename S> static void b2_h2d(B2Dev<T> &d, B2Host<S> &s, int64_t n) {
+    static_assert(sizeof(T) == sizeof(S), "memcpy between different cell types");
+    if (d.freed || s.freed) b2_throw("use after free");
+    if (n <= 0) return;
+    if (n > s.n || n > d.n) b2_throw("list index out of range");
+    if (s.init) for (int64_t i = 0; i < n; ++i) if (!s.init[i]) b2_throw("memcpy of uninitialized data");
+    cudaError_t e = cudaMemcpy(d.p, s.p, (size_t)n * sizeof(T), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) b2_throw(std::string("memcpy_host_to_device: ") + cudaGetErrorString(e));
+}
+template <typename T, typename S> static void b2_d2h(B2Host<T> &d, B2Dev<S> &s, int64_t n) {
+    static_assert(sizeof(T) == sizeof(S), "memcpy between different cell types");
+    if (d.freed || s.freed) b2_throw("use after free");
+    if (n <= 0) return;
+    if (n > s.n || n > d.n) b2_throw("list index out of range");
+    cudaError_t e = cudaMemcpy(d.p, s.p, (size_t)n * sizeof(T), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) b2_throw(std::string("memcpy_device_to_host: ") + cudaGetErrorString(e));
+    if (d.init) memset(d.init, 1, (size_t)n);
+}
+static void b2_check_kernel(int *flags_dev, const char *name) {
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) b2_throw(std::string(name) + ": " + cudaGetErrorString(e));
+    int f[5];
+    cudaMemcpy(f, flags_dev, sizeof(f), cudaMemcpyDeviceToHost);
+    if (f[0]) {
+        int64_t a = (int64_t)(uint32_t)f[1] | ((int64_t)f[3] << 32), b = (int64_t)(uint32_t)f[2] | ((int64_t)f[4] << 32);
+        if (f[0] == B2E_OOB) b2_throw("index " + std::to_string(a) + " out of bounds 0.." + std::to_string(b));
+        if (f[0] == B2E_DIV) b2_throw("exact_div(" + std::to_string(a) + ", " + std::to_string(b) + ") is not exact");
+        if (f[0] == B2E_WIDTH) b2_throw("thread for extent " + std::to_string(a) + " does not divide the context width " + std::to_string(b));
+        b2_throw("device error");
+    }
+}
+"""
+
+
+# ----------------------------------------------------------------------------- generator
+
+
+class _Gen:
+    def __init__(self, fn):
+        self.fn = fn
+        self.syms: dict = {}
+        self.kernels: list = []
+        self.nk = 0
+        self.tmp = 0
+        self.params = []
+        for i, (pn, pt) in enumerate(fn.params):
+            if pt.endswith("*"):
+                s = Sym(pn, "param_arr", pt[:-1], index=i)
+            else:
+                s = Sym(pn, "param_int" if pt == "int" else "param_float", pt, index=i)
+            self.syms[pn] = s
+            self.params.append(s)
+
+    def fresh(self, hint="t"):
+        self.tmp += 1
+        return f"_{hint}{self.tmp}"
+
+    def sym(self, name):
+        if name not in self.syms:
+            raise UnsupportedProgram(f"unbound variable {name!r}")
+        return self.syms[name]
+
+    # ------------------------------------------------------------------ expressions
+    def expr(self, e, dev=None):
+        """-> (C code, type) with type in i (int64), f (binary32 value), d (double)."""
+        c = _cls(e)
+        if c == "IntLit":
+            return f"((int64_t){int(e.value)}LL)", "i"
+        if c == "FloatLit":
+            return _f32_literal(e.value), "f"
+        if c == "Var":
+            s = self.sym(e.name)
+            if s.is_array:
+                raise UnsupportedProgram(f"array {e.name!r} used as a value")
+            if s.kind == "param_float":
+                return s.cname, "d"
+            return s.cname, ("f" if s.ctype == "float" else "i")
+        if c == "Access":
+            return self.access_read(e.base, e.idxs, dev)
+        if c == "BinOp":
+            a, ta = self.expr(e.lhs, dev)
+            b, tb = self.expr(e.rhs, dev)
+            op = e.op
+            if op in ("==", "!=", "<", "<=", ">", ">="):
+                if ta == "i" and tb == "i":
+                    return f"((int64_t)({a} {op} {b}))", "i"
+                return f"((int64_t)((double)({a}) {op} (double)({b})))", "i"
+            if ta == "i" and tb == "i":
+                if op in ("+", "-", "*"):
+                    return f"({a} {op} {b})", "i"
+                if op == "/":
+                    return f"b2_div({a}, {b})", "i"
+                if op == "%":
+                    return f"b2_mod({a}, {b})", "i"
+            if op in ("+", "-", "*"):
+                return f"((double)({a}) {op} (double)({b}))", "d"
+            raise UnsupportedProgram(f"operator {op!r} on floating-point operands")
+        if c == "Call":
+            return self.call_expr(e, dev)
+        raise UnsupportedProgram(f"cannot compile expression {c}")
+
+    def call_expr(self, e, dev):
+        if e.fn == "exact_div":
+            a, ta = self.expr(e.args[0], dev)
+            b, tb = self.expr(e.args[1], dev)
+            if ta != "i" or tb != "i":
+                raise UnsupportedProgram("exact_div on floating-point operands")
+            if dev is None:
+                return f"b2_exact_div_h({a}, {b})", "i"
+            return f"b2_exact_div_d({a}, {b}, b2_err)", "i"
+        if e.fn == "pow2":
+            k, tk = self.expr(e.args[0], dev)
+            return f"b2_pow2({k})", "i"
+        if e.fn.startswith("DMINDEX"):
+            k = len(e.args) // 2
+            dims = [self.expr(a, dev)[0] for a in e.args[:k]]
+            idxs = [self.expr(a, dev)[0] for a in e.args[k:]]
+            out = "((int64_t)0)"
+            for d, ix in zip(dims, idxs):
+                out = f"({out} * {d} + {ix})"
+            return out, "i"
+        raise UnsupportedProgram(f"cannot call {e.fn!r} in an expression")
+
+    def int_expr(self, e, dev=None):
+        code, t = self.expr(e, dev)
+        if t != "i":
+            raise UnsupportedProgram("integer expression expected")
+        return code
+
+    # ------------------------------------------------------------------ arrays
+    def _indices(self, s, idxs, dev):
+        idxs = list(idxs)
+        if s.kind in ("smem_arr", "treg_arr"):
+            # the interpreter prepends the block (thread) dimension; its index is
+            # DMINDEX(...) of the current block, 0 in per-block storage
+            if not idxs or _cls(idxs[0]) != "Call" or not idxs[0].fn.startswith("DMINDEX"):
+                raise UnsupportedProgram(f"{s.name!r}: first index of a per-block array must be DMINDEX")
+            idxs = idxs[1:]
+        return [self.int_expr(i, dev) for i in idxs]
+
+    def _dev_offset(self, s, codes):
+        """Device offset with bounds checks; returns (ok_expr, off_expr, setup lines)."""
+        dims = f"{s.cname}_dims"
+        lines = []
+        if len(codes) == s.rank + 1 and s.rank == 1:
+            ix = self.fresh("ix")
+            lines.append(f"const int64_t {ix} = {codes[0]} + {codes[1]};")
+            return f"b2_chk({ix}, {dims}[0], b2_err)", ix, lines
+        if len(codes) != s.rank:
+            raise UnsupportedProgram(f"rank mismatch on {s.name!r}: {len(codes)} indices into {s.rank}-d array")
+        ok, off = [], "((int64_t)0)"
+        for k, cd in enumerate(codes):
+            v = self.fresh("ix")
+            lines.append(f"const int64_t {v} = {cd};")
+            ok.append(f"b2_chk({v}, {dims}[{k}], b2_err)")
+            off = f"({off} * {dims}[{k}] + {v})"
+        return "(" + " && ".join(ok or ["true"]) + ")", off, lines
+
+    def access_read(self, base, idxs, dev):
+        s = self.sym(base)
+        if not s.is_array:
+            raise UnsupportedProgram(f"{base!r} is not an array")
+        t = "f" if s.ctype == "float" else "i"
+        codes = self._indices(s, idxs, dev)
+        if dev is None:
+            if s.kind not in ("param_arr", "host_arr"):
+                raise UnsupportedProgram(f"host code reads device/shared array {base!r}")
+            arr = self.fresh("idx")
+            self.pre.append(f"const int64_t {arr}[] = {{{', '.join(codes) or '0'}}};")
+            return f"b2_hread({s.cname}, {len(codes)}, {arr})", t
+        if s.kind not in ("dev_arr", "smem_arr", "treg_arr"):
+            raise UnsupportedProgram(f"kernel reads host array {base!r}")
+        dev.use(s)
+        ok, off, lines = self._dev_offset(s, codes)
+        self.pre.extend(lines)
+        zero = "0.0f" if s.ctype == "float" else "0"
+        return f"({ok} ? {s.cname}[{off}] : {zero})", t
+
+    def store_value(self, s, code, t):
+        if s.ctype == "float":
+            return f"(float)({code})" if t != "f" else code
+        if t != "i":
+            raise UnsupportedProgram("float value stored into an int cell")
+        return code
+
+    # ------------------------------------------------------------------ host statements
+    def host_seq(self, seq, out, ind):
+        for st in _stmts(seq):
+            self.host_stmt(st, out, ind)
+
+    def host_stmt(self, st, out, ind):
+        pad = "    " * ind
+        self.pre = []
+        c = _cls(st)
+        lines = []
+        if c == "Seq":
+            if _is_kernel_scope(st):
+                self.kernel_scope(st, out, ind)
+                return
+            out.append(pad + "{")
+            self.host_seq(st, out, ind + 1)
+            out.append(pad + "}")
+            return
+        if c == "Decl":
+            lines = self.host_decl(st)
+        elif c == "Assign":
+            lines = self.host_assign(st)
+        elif c == "For":
+            start, stop = self.int_expr(st.range.start), self.int_expr(st.range.stop)
+            if st.mode not in ("seq", "parallel"):
+                raise UnsupportedProgram(f"{st.mode} for outside a kernel")
+            self.syms[st.index] = Sym(st.index, "scalar", "int")
+            v = "v_" + st.index
+            e = self.fresh("stop")
+            out.extend(pad + p for p in self.pre)
+            out.append(pad + f"{{ const int64_t {e} = {stop};")
+            out.append(pad + f"for (int64_t {v} = {start}; {v} < {e}; ++{v}) {{")
+            self.host_seq(st.body, out, ind + 1)
+            out.append(pad + "} }")
+            return
+        elif c == "If":
+            cond, _ = self.expr(st.cond)
+            out.extend(pad + p for p in self.pre)
+            out.append(pad + f"if ({cond}) {{")
+            self.host_seq(st.then, out, ind + 1)
+            if st.els is not None:
+                out.append(pad + "} else {")
+                self.host_seq(st.els, out, ind + 1)
+            out.append(pad + "}")
+            return
+        elif c == "Return":
+            code, t = self.expr(st.value)
+            if t == "i":
+                lines = [f"*ret_i = {code}; *ret_kind = 1; return 0;"]
+            else:
+                lines = [f"*ret_f = (double)({code}); *ret_kind = 2; return 0;"]
+        elif c == "CallStmt":
+            lines = self.host_call(st)
+        else:
+            raise UnsupportedProgram(f"cannot compile statement {c}")
+        out.extend(pad + p for p in self.pre + lines)
+
+    def host_decl(self, d):
+        if d.alloc is None:
+            code, t = self.expr(d.init)
+            s = Sym(d.name, "scalar", d.ctype)
+            self.syms[d.name] = s
+            if d.ctype == "float":
+                return [f"float {s.cname} = {self.store_value(s, code, t)};"]
+            if t != "i":
+                raise UnsupportedProgram("int scalar initialised from a float")
+            return [f"int64_t {s.cname} = {code};"]
+        dims = [self.int_expr(x) for x in d.dims]
+        if d.alloc in ("MALLOC", "gmem_malloc"):
+            kind = "host_arr" if d.alloc == "MALLOC" else "dev_arr"
+            s = Sym(d.name, kind, d.ctype, rank=len(dims))
+            self.syms[d.name] = s
+            fn = "b2_host_alloc" if kind == "host_arr" else "b2_dev_alloc"
+            return [f"auto {s.cname} = {fn}<{s.elem}>({len(dims)}, {{{', '.join(dims)}}});"]
+        raise UnsupportedProgram(f"{d.alloc} outside a kernel scope")
+
+    def host_assign(self, a):
+        s = self.sym(a.target.base)
+        val, t = self.expr(a.value)
+        if not s.is_array:
+            if s.kind in ("param_int", "param_float"):
+                raise UnsupportedProgram(f"assignment to parameter {s.name!r}")
+            if a.op == "+=":
+                val, t = (f"({s.cname} + {val})", "i") if (t == "i" and s.ctype == "int") else \
+                    (f"((double){s.cname} + (double)({val}))", "d")
+            return [f"{s.cname} = {self.store_value(s, val, t)};"]
+        if s.kind not in ("param_arr", "host_arr"):
+            raise UnsupportedProgram(f"host code writes device/shared array {s.name!r}")
+        codes = self._indices(s, a.target.idxs, None)
+        ix = self.fresh("idx")
+        lines = [f"const int64_t {ix}[] = {{{', '.join(codes) or '0'}}};"]
+        if a.op == "+=":
+            old = f"b2_hread({s.cname}, {len(codes)}, {ix})"
+            val, t = (f"((int64_t){old} + {val})", "i") if (t == "i" and s.ctype == "int") else \
+                (f"((double){old} + (double)({val}))", "d")
+        lines.append(f"b2_hwrite({s.cname}, {len(codes)}, {ix}, ({s.elem})({self.store_value(s, val, t)}));")
+        return lines
+
+    def host_call(self, cs):
+        f = cs.fn
+        if f in ("kernel_setup_end", "kernel_teardown_begin", "blocksync", "magic_barrier",
+                 "kernel_teardown_sync"):
+            return []
+        if f in ("free", "gmem_free") or f.startswith("__smem_free"):
+            if not cs.args or _cls(cs.args[0]) != "Var":
+                raise UnsupportedProgram(f"{f} of a non-variable")
+            s = self.sym(cs.args[0].name)
+            return [f"{s.cname}.freed = true;"]
+        if f.startswith("memcpy_host_to_device") or f.startswith("memcpy_device_to_host"):
+            if len(cs.args) < 3 or _cls(cs.args[0]) != "Var" or _cls(cs.args[1]) != "Var":
+                raise UnsupportedProgram(f"{f}: destination and source must be array names")
+            d, s = self.sym(cs.args[0].name), self.sym(cs.args[1].name)
+            n = " * ".join(f"({self.int_expr(x)})" for x in cs.args[2:])
+            if f.startswith("memcpy_host_to_device"):
+                if d.kind != "dev_arr" or s.kind not in ("param_arr", "host_arr"):
+                    raise UnsupportedProgram(f"{f}: expects (device, host) arrays")
+                return [f"b2_h2d({d.cname}, {s.cname}, {n});"]
+            if s.kind != "dev_arr" or d.kind not in ("param_arr", "host_arr"):
+                raise UnsupportedProgram(f"{f}: expects (host, device) arrays")
+            return [f"b2_d2h({d.cname}, {s.cname}, {n});"]
+        if f == "kernel_launch":
+            raise UnsupportedProgram("kernel_launch must open a scoped block")
+        raise UnsupportedProgram(f"call to {f!r} is not supported by the code generator")
+
+    # ------------------------------------------------------------------ kernels
+    def kernel_scope(self, seq, out, ind):
+        pad = "    " * ind
+        st = _stmts(seq)
+        launch, body = st[0], st[1:]
+        if not body or _cls(body[-1]) != "CallStmt" or body[-1].fn != "kernel_kill":
+            raise UnsupportedProgram("kernel scope must end with kernel_kill()")
+        body = body[:-1]
+        self.pre = []
+        bpg, tpb = self.int_expr(launch.args[0]), self.int_expr(launch.args[1])
+        setup = []
+        smem = []
+        i = 0
+        while i < len(body) and not (_cls(body[i]) == "CallStmt" and body[i].fn == "kernel_setup_end"):
+            d = body[i]
+            if _cls(d) != "Decl" or d.alloc not in ("__smem_malloc", "__treg_malloc"):
+                raise UnsupportedProgram("only __smem_malloc / __treg_malloc may precede kernel_setup_end")
+            smem.append(d)
+            i += 1
+        if i == len(body):
+            raise UnsupportedProgram("kernel scope without kernel_setup_end()")
+        i += 1
+        j = len(body)
+        for k in range(i, len(body)):
+            if _cls(body[k]) == "CallStmt" and body[k].fn == "kernel_teardown_begin":
+                j = k
+                break
+        kbody, teardown = body[i:j], body[j + 1:]
+        for t in teardown:
+            if not (_cls(t) == "CallStmt" and (t.fn.startswith("__smem_free") or t.fn == "kernel_teardown_sync")):
+                raise UnsupportedProgram("only __smem_free may follow kernel_teardown_begin")
+        name = f"b2g_kernel{self.nk}"
+        self.nk += 1
+        kctx = _KernelCtx(self, name)
+        # shared / thread-register arrays: dims evaluated on the host
+        host_lines = list(self.pre)
+        self.pre = []
+        smem_bytes = self.fresh("smem")
+        host_lines.append(f"int64_t {smem_bytes} = 0;")
+        for d in smem:
+            dims = [self.int_expr(x) for x in d.dims]
+            kind = "smem_arr" if d.alloc == "__smem_malloc" else "treg_arr"
+            s = Sym(d.name, kind, d.ctype, rank=len(dims))
+            self.syms[d.name] = s
+            kctx.local_arrays.append((s, dims))
+            host_lines.extend(self.pre)
+            self.pre = []
+            dv = f"{s.cname}_hdims"
+            host_lines.append(f"const int64_t {dv}[8] = {{{', '.join(dims) or '0'}}};")
+            if kind == "smem_arr":
+                host_lines.append(f"const int64_t {s.cname}_soff = {smem_bytes};")
+                host_lines.append(f"{smem_bytes} += ((" + " * ".join(f"{dv}[{k}]" for k in range(len(dims)) or ["1"]) +
+                                  f") * (int64_t)sizeof({s.elem}) + 15) / 16 * 16;")
+        # kernel body
+        dl = []
+        kctx.emit_seq(kbody, dl, 1, "b2_w0", "b2_rel0")
+        self.kernels.append(kctx.render(dl))
+        # host launch
+        args = kctx.host_args()
+        out.extend(pad + ln for ln in host_lines)
+        g, t = self.fresh("bpg"), self.fresh("tpb")
+        out.append(pad + f"{{ const int64_t {g} = {bpg}, {t} = {tpb};")
+        out.append(pad + f"  if ({g} < 0 || {g} > 2147483647LL || {t} < 0 || {t} > 1024) "
+                   f"b2_throw(\"kernel_launch(\" + std::to_string({g}) + \", \" + std::to_string({t}) + \") exceeds the B200 launch limits\");")
+        out.append(pad + f"  if ({g} > 0 && {t} > 0) {{")
+        out.append(pad + f"    if ({smem_bytes} > 48 * 1024) cudaFuncSetAttribute({name}, cudaFuncAttributeMaxDynamicSharedMemorySize, (int){smem_bytes});")
+        out.append(pad + "    cudaMemset(b2_err_dev, 0, 5 * sizeof(int));")
+        out.append(pad + f"    {name}<<<(unsigned){g}, (unsigned){t}, (size_t){smem_bytes}>>>({', '.join(args)});")
+        out.append(pad + f"    b2_check_kernel(b2_err_dev, \"{name}\");")
+        out.append(pad + "  }")
+        out.append(pad + "}")
+
+    # ------------------------------------------------------------------ translation unit
+    def render(self) -> str:
+        body = []
+        self.host_seq(self.fn.body, body, 2)
+        decl = []
+        for s in self.params:
+            if s.kind == "param_arr":
+                decl.append(f"    auto {s.cname} = b2_param<{s.elem}>(&arrs[{s.index}]);")
+            elif s.kind == "param_int":
+                decl.append(f"    const int64_t {s.cname} = ints[{s.index}];")
+            else:
+                decl.append(f"    const double {s.cname} = flts[{s.index}];")
+        src = [PRELUDE]
+        src.extend(self.kernels)
+        src.append('extern "C" int b2g_main(B2Arr *arrs, const int64_t *ints, const double *flts, '
+                   'int64_t *ret_i, double *ret_f, int *ret_kind, char *err, int errlen) {')
+        src.append("    std::vector<void *> dev_allocs, host_allocs;")
+        src.append("    g_dev_allocs = &dev_allocs; g_host_allocs = &host_allocs;")
+        src.append("    int *b2_err_dev = nullptr;")
+        src.append("    struct Cleanup { std::vector<void *> &d, &h; int **e; ~Cleanup() {")
+        src.append("        for (void *p : d) cudaFree(p); for (void *p : h) free(p); if (*e) cudaFree(*e); } }")
+        src.append("        cleanup{dev_allocs, host_allocs, &b2_err_dev};")
+        src.append("    *ret_kind = 0;")
+        src.append("    try {")
+        src.append("        if (cudaMalloc((void **)&b2_err_dev, 8 * sizeof(int)) != cudaSuccess) b2_throw(\"cudaMalloc failed\");")
+        src.extend(decl)
+        src.extend(body)
+        src.append("        return 0;")
+        src.append("    } catch (B2Err &e) {")
+        src.append("        snprintf(err, errlen, \"%s\", e.msg.c_str());")
+        src.append("        return 1;")
+        src.append("    }")
+        src.append("}")
+        return "\n".join(src) + "\n"
+
+
+class _KernelCtx:
+    """Per-kernel state: captured host scalars, device arrays, local arrays."""
+
+    def __init__(self, gen: _Gen, name: str):
+        self.g = gen
+        self.name = name
+        self.arrays: dict = {}      # name -> Sym (dev arrays used)
+        self.scalars: dict = {}     # name -> Sym (host scalars captured)
+        self.local_arrays: list = []
+        self.local_syms: set = set()
+
+    def use(self, s):
+        if s.kind == "dev_arr":
+            self.arrays[s.name] = s
+
+    def capture(self, name):
+        s = self.g.sym(name)
+        if not s.is_array and name not in self.local_syms:
+            self.scalars[name] = s
+
+    def host_args(self):
+        args = []
+        for s in self.arrays.values():
+            args.append(f"{s.cname}.p")
+            args.append(f"{s.cname}.dims[0], {s.cname}.dims[1], {s.cname}.dims[2], {s.cname}.dims[3]")
+            args.append(f"{s.cname}.freed")
+        for s, dims in self.local_arrays:
+            for k in range(4):
+                args.append(f"{s.cname}_hdims[{k}]")
+            if s.kind == "smem_arr":
+                args.append(f"{s.cname}_soff")
+        for s in self.scalars.values():
+            args.append(s.cname)
+        args.append("b2_err_dev")
+        return args
+
+    def render(self, body_lines):
+        params = []
+        pro = []
+        for s in self.arrays.values():
+            params.append(f"{s.elem} *__restrict__ {s.cname}")
+            params.append(", ".join(f"int64_t {s.cname}_d{k}" for k in range(4)))
+            params.append(f"bool {s.cname}_freed")
+            pro.append(f"    const int64_t {s.cname}_dims[4] = {{{s.cname}_d0, {s.cname}_d1, {s.cname}_d2, {s.cname}_d3}};")
+            pro.append(f"    if ({s.cname}_freed) {{ b2_flag(b2_err, B2E_OOB, 0, 0); return; }}")
+        treg = []
+        for s, dims in self.local_arrays:
+            params.append(", ".join(f"int64_t {s.cname}_d{k}" for k in range(4)))
+            pro.append(f"    const int64_t {s.cname}_dims[4] = {{{s.cname}_d0, {s.cname}_d1, {s.cname}_d2, {s.cname}_d3}};")
+            if s.kind == "smem_arr":
+                params.append(f"int64_t {s.cname}_soff")
+                pro.append(f"    {s.elem} *{s.cname} = ({s.elem} *)(b2_smem + {s.cname}_soff);")
+            else:
+                treg.append(s)
+        for s in self.scalars.values():
+            ty = "double" if s.kind == "param_float" else ("float" if s.ctype == "float" else "int64_t")
+            params.append(f"const {ty} {s.cname}")
+        params.append("int *b2_err")
+        for s in treg:
+            n = " * ".join(f"{s.cname}_d{k}" for k in range(s.rank)) or "1"
+            pro.append(f"    {s.elem} {s.cname}[B2_TREG_MAX]; if (({n}) > B2_TREG_MAX) {{ b2_flag(b2_err, B2E_OOB, {n}, B2_TREG_MAX); return; }}")
+        out = [f"__global__ void {self.name}({', '.join(params)}) {{",
+               "    extern __shared__ __align__(16) unsigned char b2_smem[];",
+               "    const int64_t b2_w0 = (int64_t)gridDim.x * blockDim.x;",
+               "    const int64_t b2_rel0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;"]
+        if treg:
+            out.insert(0, "#define B2_TREG_MAX 64")
+        out.extend(pro)
+        out.extend(body_lines)
+        out.append("}")
+        return "\n".join(out) + "\n"
+
+    # ------------------------------------------------------------------ device statements
+    def emit_seq(self, stmts, out, ind, w, rel):
+        for st in stmts:
+            if _is_ghost(st):
+                continue
+            self.emit(st, out, ind, w, rel)
+
+    def _scan_captures(self, node):
+        """Record host scalars referenced by an expression."""
+        c = _cls(node)
+        if c == "Var":
+            s = self.g.syms.get(node.name)
+            if s is not None and not s.is_array:
+                self.capture(node.name)
+        elif c == "BinOp":
+            self._scan_captures(node.lhs)
+            self._scan_captures(node.rhs)
+        elif c == "Call":
+            for a in node.args:
+                self._scan_captures(a)
+        elif c in ("Access", "Ptr"):
+            for a in node.idxs:
+                self._scan_captures(a)
+
+    def dexpr(self, e):
+        self._scan_captures(e)
+        return self.g.expr(e, self)
+
+    def emit(self, st, out, ind, w, rel):
+        g = self.g
+        pad = "    " * ind
+        g.pre = []
+        c = _cls(st)
+        if c == "Seq":
+            out.append(pad + "{")
+            self.emit_seq(st.stmts, out, ind + 1, w, rel)
+            out.append(pad + "}")
+            return
+        if c == "For":
+            s0, _ = self.dexpr(st.range.start)
+            s1, _ = self.dexpr(st.range.stop)
+            pre = g.pre
+            g.syms[st.index] = Sym(st.index, "scalar", "int")
+            self.local_syms.add(st.index)
+            v = "v_" + st.index
+            out.extend(pad + p for p in pre)
+            if st.mode in ("thread", "magic_thread"):
+                n, w2, r2 = g.fresh("n"), g.fresh("w"), g.fresh("rel")
+                out.append(pad + f"{{ const int64_t {n} = ({s1}) - ({s0});")
+                out.append(pad + f"  if ({n} > 0) {{")
+                out.append(pad + f"  if ({w} % {n} != 0) {{ b2_flag(b2_err, B2E_WIDTH, {n}, {w}); return; }}")
+                out.append(pad + f"  const int64_t {w2} = {w} / {n};")
+                out.append(pad + f"  const int64_t {v} = ({s0}) + {rel} / {w2};")
+                out.append(pad + f"  const int64_t {r2} = {rel} % {w2};")
+                self.emit_seq(st.body.stmts, out, ind + 1, w2, r2)
+                out.append(pad + "  } }")
+                return
+            e = g.fresh("stop")
+            out.append(pad + f"{{ const int64_t {e} = {s1};")
+            out.append(pad + f"for (int64_t {v} = {s0}; {v} < {e}; ++{v}) {{")
+            self.emit_seq(st.body.stmts, out, ind + 1, w, rel)
+            out.append(pad + "} }")
+            return
+        if c == "If":
+            cond, _ = self.dexpr(st.cond)
+            out.extend(pad + p for p in g.pre)
+            out.append(pad + f"if ({cond}) {{")
+            self.emit_seq(st.then.stmts, out, ind + 1, w, rel)
+            if st.els is not None:
+                out.append(pad + "} else {")
+                self.emit_seq(st.els.stmts, out, ind + 1, w, rel)
+            out.append(pad + "}")
+            return
+        if c == "CallStmt":
+            if st.fn in ("blocksync", "kernel_teardown_sync"):
+                out.append(pad + "__syncthreads();")
+                return
+            raise UnsupportedProgram(f"call to {st.fn!r} inside a kernel")
+        if c == "Decl":
+            if st.alloc is not None:
+                raise UnsupportedProgram(f"{st.alloc} inside a kernel body")
+            code, t = self.dexpr(st.init)
+            s = Sym(st.name, "scalar", st.ctype)
+            g.syms[st.name] = s
+            self.local_syms.add(st.name)
+            out.extend(pad + p for p in g.pre)
+            if st.ctype == "float":
+                out.append(pad + f"float {s.cname} = {g.store_value(s, code, t)};")
+            else:
+                out.append(pad + f"int64_t {s.cname} = {code};")
+            return
+        if c == "Assign":
+            s = g.sym(st.target.base)
+            val, t = self.dexpr(st.value)
+            if not s.is_array:
+                if st.target.base not in self.local_syms:
+                    raise UnsupportedProgram(f"kernel assigns host scalar {s.name!r}")
+                if st.op == "+=":
+                    val, t = (f"({s.cname} + {val})", "i") if (t == "i" and s.ctype == "int") else \
+                        (f"((double){s.cname} + (double)({val}))", "d")
+                out.extend(pad + p for p in g.pre)
+                out.append(pad + f"{s.cname} = {g.store_value(s, val, t)};")
+                return
+            if s.kind not in ("dev_arr", "smem_arr", "treg_arr"):
+                raise UnsupportedProgram(f"kernel writes host array {s.name!r}")
+            self.use(s)
+            for ix in st.target.idxs:
+                self._scan_captures(ix)
+            codes = g._indices(s, st.target.idxs, self)
+            ok, off, lines = g._dev_offset(s, codes)
+            cell = f"{s.cname}[{off}]"
+            if st.op == "+=":
+                val, t = (f"((int64_t){cell} + {val})", "i") if (t == "i" and s.ctype == "int") else \
+                    (f"((double){cell} + (double)({val}))", "d")
+            # a memory write in a context wider than one thread runs once (interp semantics)
+            guard = f"{rel} == 0 && " if w != "1" else ""
+            body = g.pre + lines + [f"if ({guard}{ok}) {cell} = ({s.elem})({g.store_value(s, val, t)});"]
+            out.append(pad + "{")
+            out.extend(pad + "    " + b for b in body)
+            out.append(pad + "}")
+            return
+        raise UnsupportedProgram(f"cannot compile statement {c} inside a kernel")
+
+
+# ----------------------------------------------------------------------------- compile + run
+
+_NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17", "--fmad=false",
+               "-Xcompiler", "-fPIC,-ffp-contract=off,-fno-fast-math", "-shared", "-cudart", "static",
+               "-lineinfo", "-diag-suppress", "177,550"]
+_lock = threading.Lock()
+_loaded: dict = {}
+
+
+def generate(fn) -> str:
+    """CUDA C++ translation unit for a GPU-form entry function."""
+    if not has_kernel(fn):
+        raise UnsupportedProgram(
+            f"function {fn.name!r} has no kernel_launch scope: not a GPU program "
+            "(no CPU fallback)")
+    return _Gen(fn).render()
+
+
+class Compiled:
+    def __init__(self, fn, path, source):
+        self.fn = fn
+        self.path = path
+        self.source = source
+        self.lib = ctypes.CDLL(path)
+        self.lib.b2g_main.restype = ctypes.c_int
+        self.lib.b2g_main.argtypes = [ctypes.c_void_p] * 8
+
+
+class B2Arr(ctypes.Structure):
+    _fields_ = [("data", ctypes.c_void_p), ("n", ctypes.c_int64), ("rank", ctypes.c_int64),
+                ("dims", ctypes.c_int64 * MAX_RANK), ("init", ctypes.c_void_p),
+                ("freed", ctypes.c_int64)]
+
+
+def _nvcc():
+    from ._build import nvcc
+    return nvcc()
+
+
+def compile_fn(fn) -> Compiled:
+    src = generate(fn)
+    key = hashlib.sha256(src.encode() + " ".join(_NVCC_FLAGS).encode()).hexdigest()[:20]
+    with _lock:
+        if key in _loaded:
+            return _loaded[key]
+        os.makedirs(GEN_DIR, exist_ok=True)
+        so = os.path.join(GEN_DIR, f"b2g_{key}.so")
+        cu = os.path.join(GEN_DIR, f"b2g_{key}.cu")
+        if not os.path.exists(so):
+            with open(cu, "w") as f:
+                f.write(src)
+            r = subprocess.run([_nvcc(), *_NVCC_FLAGS, "-o", so + ".tmp", cu], capture_output=True, text=True)
+            if r.returncode != 0:
+                raise UnsupportedProgram("generated CUDA failed to compile:\n" + r.stderr[-4000:])
+            os.replace(so + ".tmp", so)
+        c = Compiled(fn, so, src)
+        _loaded[key] = c
+        return c
+
+
+def run_compiled(c: Compiled, env: dict, arrays: dict):
+    """Execute with the interpreter's marshalled environment; writes results back
+    into the Arrays. Returns ("ret", v) or None like Interp.run."""
+    fn = c.fn
+    n = len(fn.params)
+    arrs = (B2Arr * max(n, 1))()
+    ints = (ctypes.c_int64 * max(n, 1))()
+    flts = (ctypes.c_double * max(n, 1))()
+    keep = []
+    writeback = []
+    for i, (pn, pt) in enumerate(fn.params):
+        v = env[pn]
+        if pt.endswith("*"):
+            a = arrays[pn]
+            buf, init, wb = _host_buffer(a, pt[:-1])
+            keep.extend([buf, init])
+            arrs[i].data = buf.ctypes.data
+            arrs[i].n = buf.size
+            arrs[i].rank = len(a.dims)
+            if len(a.dims) > MAX_RANK:
+                raise UnsupportedProgram("arrays of rank > 8")
+            for k, d in enumerate(a.dims):
+                arrs[i].dims[k] = int(d)
+            arrs[i].init = init.ctypes.data if init is not None else None
+            arrs[i].freed = 1 if a.freed else 0
+            if wb is not None:
+                writeback.append((a, buf, init, wb))
+        elif pt == "int":
+            ints[i] = int(v)
+        else:
+            flts[i] = float(v)
+    ri = ctypes.c_int64(0)
+    rf = ctypes.c_double(0.0)
+    rk = ctypes.c_int(0)
+    err = ctypes.create_string_buffer(1024)
+    rc = c.lib.b2g_main(ctypes.addressof(arrs), ctypes.addressof(ints), ctypes.addressof(flts),
+                        ctypes.byref(ri), ctypes.byref(rf), ctypes.byref(rk), err, 1024)
+    for a, buf, init, wb in writeback:
+        wb(buf, init)
+    if rc != 0:
+        raise InterpError(err.value.decode(errors="replace"))
+    if rk.value == 1:
+        return ("ret", int(ri.value))
+    if rk.value == 2:
+        return ("ret", float(rf.value))
+    return None
+
+
+def _host_buffer(a, ctype):
+    """(numpy buffer, init mask or None, writeback fn or None) for an Array."""
+    dt = np.float32 if a.ctype == "float" else np.int64
+    data = a.data
+    if isinstance(data, np.ndarray):
+        flat = data.reshape(-1)
+        if flat.dtype == dt and flat.flags.c_contiguous:
+            return flat, None, None
+        buf = flat.astype(dt)
+
+        def wb(b, m, flat=flat):
+            flat[...] = b.astype(flat.dtype)
+        return buf, None, wb
+    nones = [i for i, x in enumerate(data) if x is None]
+    if nones:
+        vals = [0 if x is None else x for x in data]
+        init = np.ones(len(data), dtype=np.uint8)
+        init[nones] = 0
+    else:
+        vals, init = data, None
+    if dt == np.float32:
+        buf = np.array(vals, dtype=np.float64).astype(np.float32)
+    else:
+        try:
+            buf = np.array(vals, dtype=np.int64)
+        except OverflowError:
+            raise InterpError("int cell value outside the int64 range of compiled programs") from None
+
+    def wb(b, m, data=data):
+        vals = b.tolist()
+        if m is None:
+            data[:] = vals
+        else:
+            for i in np.flatnonzero(m).tolist():
+                data[i] = vals[i]
+    return buf, init, wb

@@ -172,10 +172,32 @@ def _store(arr, flat_positions_rows, values2d: np.ndarray, row_pitch: int):
 class Interp:
     """run(fn_name, inputs) mirrors minigpu.interp.Interp.run (interp.py:106-128)."""
 
-    def __init__(self, program):
+    BACKENDS = ("auto", "kernels", "codegen")
+
+    def __init__(self, program, backend: str = "auto"):
+        """backend: "kernels" = only the hand-written kernels (recognised
+        programs); "codegen" = compile any GPU-form program (codegen.py);
+        "auto" = kernels when the program is recognised, else codegen."""
+        if backend not in self.BACKENDS:
+            raise ValueError(f"backend must be one of {self.BACKENDS}")
         self.program = program
+        self.backend = backend
         self.launch: list = []
         self.ctx_width: list = []
+
+    def _dispatch(self, fn, fn_name, env, arrays):
+        if self.backend != "codegen":
+            try:
+                plan = recognize(self.program, fn_name)
+                return _EXEC[(plan.kind, plan.form)](plan, env)
+            except UnsupportedProgram:
+                if self.backend == "kernels":
+                    raise
+        from . import codegen
+        if not codegen.has_kernel(fn):
+            # not one of the recognised programs and not a GPU program either
+            recognize(self.program, fn_name)  # raises with the recogniser's diagnosis
+        return codegen.run_compiled(codegen.compile_fn(fn), env, arrays)
 
     def run(self, fn_name: str, inputs: dict):
         fn = self.program.fn(fn_name)
@@ -202,17 +224,16 @@ class Interp:
                 env[pname] = arr
             else:
                 env[pname] = v
-        plan = recognize(self.program, fn_name)
-        ret =_EXEC[(plan.kind, plan.form)](plan, env)
-        return ret, arrays
+        return self._dispatch(fn, fn_name, env, arrays), arrays
 
 
-def run_program(program, entry: str, inputs: dict):
+def run_program(program, entry: str, inputs: dict, backend: str = "auto"):
     """Returns (return value, {param name: flat final array data}) (interp.py:380-387).
 
     List-backed arrays come back as fresh lists; numpy-backed arrays come back
-    as the (mutated) numpy buffer itself."""
-    it = Interp(program)
+    as the (mutated) numpy buffer itself. `backend` selects hand-written kernels
+    and/or generated code (see Interp)."""
+    it = Interp(program, backend)
     ret, arrays = it.run(entry, dict(inputs))
     out = {k: (a.data if isinstance(a.data, np.ndarray) else list(a.data))
            for k, a in arrays.items()}

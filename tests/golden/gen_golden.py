@@ -166,5 +166,59 @@ def main():
     print(len(cases), "cases written")
 
 
+def codegen_cases():
+    """Reference outputs for GPU-form programs beyond the canonical templates,
+    used to pin the code generator (paper_2605_13864_b200/codegen.py)."""
+    rng = np.random.default_rng(77)
+    cases, arrays = [], {}
+
+    def add(case, **arrs):
+        cid = f"g{len(cases):03d}"
+        case["id"] = cid
+        for k, v in arrs.items():
+            arrays[f"{cid}_{k}"] = v
+        cases.append(case)
+        print(cid, case["program"], case.get("note", ""), flush=True)
+
+    def run_t(prog_name, H, W, note):
+        a = rng.uniform(-1, 1, (H, W)).astype(np.float32)
+        _, outs = run_program(load(prog_name), "transpose", {"in": a.reshape(-1).tolist(),
+                                                              "out": [0.0] * (H * W), "W": W, "H": H})
+        add({"kind": "transpose", "program": prog_name, "shape": [H, W], "note": note},
+            inp=a, out=np.array(outs["out"], dtype=np.float32).reshape(W, H))
+
+    run_t("transpose_gpu.optc", 64, 96, "A.4 via codegen")
+    run_t("transpose_gpu_t64.optc", 128, 192, "64x64-tile variant")
+    for prog_name, x, note in [
+        ("reduce_tree_f32.optc", rng.uniform(-1, 1, 4096).astype(np.float32), "A.5 via codegen"),
+        ("reduce_tree_int256.optc", rng.integers(-2**31, 2**31, 4096, dtype=np.int64).astype(np.int32),
+         "int tree, 256 blocks"),
+        ("scale_then_reduce.optc", rng.uniform(-1, 1, 2048).astype(np.float32), "two kernels, binary64 eval"),
+    ]:
+        ret, _ = run_program(load(prog_name), "reduce", {"arr": x.tolist(), "N": int(x.size)})
+        res = {"result_int": str(ret)} if isinstance(ret, int) else \
+            {"result_f32_bits": int(np.float32(ret).view(np.uint32)), "result": ret}
+        add({"kind": "reduce", "program": prog_name, "n": int(x.size), "note": note, **res}, inp=x)
+    errs = []
+    for prog_name, entry, inputs, note in [
+        ("oob_kernel.optc", "shift", {"arr": [0.5] * 128, "N": 128}, "out-of-bounds kernel write"),
+        ("transpose_gpu_t64.optc", "transpose", {"in": [0.0] * (96 * 64), "out": [0.0] * (96 * 64),
+                                                 "W": 96, "H": 64}, "64 not dividing W"),
+        ("reduce_tree_int256.optc", "reduce", {"arr": [1] * 300, "N": 300}, "256 not dividing N"),
+    ]:
+        try:
+            run_program(load(prog_name), entry, inputs)
+            errs.append({"program": prog_name, "entry": entry, "note": note, "error": None})
+        except Exception as e:  # noqa: BLE001
+            errs.append({"program": prog_name, "entry": entry, "note": note, "type": type(e).__name__,
+                         "error": str(e)})
+    np.savez_compressed(os.path.join(HERE, "golden_codegen.npz"), **arrays)
+    with open(os.path.join(HERE, "manifest_codegen.json"), "w") as f:
+        json.dump({"generator": "tests/golden/gen_golden.py (codegen_cases)", "cases": cases,
+                   "errors": errs}, f, indent=1)
+
+
 if __name__ == "__main__":
-    main()
+    if not os.environ.get("GOLDEN_CODEGEN_ONLY"):
+        main()
+    codegen_cases()

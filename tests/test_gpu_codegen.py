@@ -1,0 +1,107 @@
+"""Generated CUDA (codegen.py) vs the reference interpreter's outputs for
+GPU-form programs, including derived variants no hand-written kernel covers
+(tests/golden/manifest_codegen.json, produced by minigpu.interp.run_program)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, program_text
+from oracle import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def b2():
+    import paper_2605_13864_b200 as b2
+    return b2
+
+
+@pytest.fixture(scope="module")
+def gcases():
+    with open(os.path.join(GOLDEN, "manifest_codegen.json")) as f:
+        man = json.load(f)
+    arrs = np.load(os.path.join(GOLDEN, "golden_codegen.npz"))
+    for c in man["cases"]:
+        for k in arrs.files:
+            if k.startswith(c["id"] + "_"):
+                c[k[len(c["id"]) + 1:]] = arrs[k]
+    return man
+
+
+def _prog(b2, name):
+    return b2.parse_program(program_text(name), name)
+
+
+def test_codegen_cases_bit_exact(b2, gcases):
+    assert len(gcases["cases"]) >= 5
+    for c in gcases["cases"]:
+        p = _prog(b2, c["program"])
+        if c["kind"] == "transpose":
+            H, W = c["shape"]
+            ret, outs = b2.run_program(p, "transpose", {"in": c["inp"].reshape(-1).tolist(),
+                                                        "out": [0.0] * (H * W), "W": W, "H": H},
+                                       backend="codegen")
+            assert outs["out"] == c["out"].reshape(-1).tolist(), c["id"]
+        else:
+            x = c["inp"]
+            ret, _ = b2.run_program(p, "reduce", {"arr": x.tolist(), "N": int(x.size)}, backend="codegen")
+            if "result_int" in c:
+                assert isinstance(ret, int) and ret == int(c["result_int"]), c["id"]
+            else:
+                assert np.float32(ret).view(np.uint32) == np.uint32(c["result_f32_bits"]), c["id"]
+
+
+def test_codegen_error_messages_match_reference(b2, gcases):
+    for e in gcases["errors"]:
+        p = _prog(b2, e["program"])
+        fn = p.fn(e["entry"])
+        inputs = {"oob_kernel.optc": {"arr": [0.5] * 128, "N": 128},
+                  "transpose_gpu_t64.optc": {"in": [0.0] * (96 * 64), "out": [0.0] * (96 * 64), "W": 96, "H": 64},
+                  "reduce_tree_int256.optc": {"arr": [1] * 300, "N": 300}}[e["program"]]
+        with pytest.raises(b2.InterpError) as ei:
+            b2.run_program(p, fn.name, inputs, backend="codegen")
+        assert str(ei.value) == e["error"], e["note"]
+
+
+def test_canonical_goldens_through_codegen(b2, golden):
+    for c in golden:
+        if c["program"] not in ("transpose_gpu.optc", "reduce_tree_f32.optc"):
+            continue
+        p = _prog(b2, c["program"])
+        if c["kind"] == "transpose":
+            H, W = c["shape"]
+            _, outs = b2.run_program(p, "transpose", {"in": c["inp"].reshape(-1).tolist(),
+                                                      "out": [0.0] * (H * W), "W": W, "H": H}, backend="codegen")
+            assert outs["out"] == c["out"].reshape(-1).tolist(), c["id"]
+        else:
+            ret, _ = b2.run_program(p, "reduce", {"arr": c["inp"].tolist(), "N": c["n"]}, backend="codegen")
+            assert np.float32(ret).view(np.uint32) == np.uint32(c["result_f32_bits"]), c["id"]
+
+
+def test_codegen_at_scale_numpy_arrays(b2):
+    rng = np.random.default_rng(11)
+    x = rng.uniform(-1, 1, 1 << 20).astype(np.float32)
+    ret, _ = b2.run_program(_prog(b2, "reduce_tree_f32.optc"), "reduce",
+                            {"arr": b2.Array.from_numpy(x), "N": x.size}, backend="codegen")
+    want, _ = oracle.reduce_f32_tree512(x)
+    assert np.float32(ret).view(np.uint32) == np.float32(want).view(np.uint32)
+    a = rng.uniform(-1, 1, (1024, 2048)).astype(np.float32)
+    out = np.zeros(a.size, np.float32)
+    b2.run_program(_prog(b2, "transpose_gpu_t64.optc"), "transpose",
+                   {"in": b2.Array.from_numpy(a.reshape(-1)), "out": b2.Array.from_numpy(out),
+                    "W": 2048, "H": 1024}, backend="codegen")
+    assert np.array_equal(out.reshape(2048, 1024), a.T)
+
+
+def test_auto_backend_routes_variants_to_codegen(b2):
+    # the 64x64 variant is not a template: "auto" compiles it, "kernels" refuses it
+    p = _prog(b2, "transpose_gpu_t64.optc")
+    a = np.arange(64 * 128, dtype=np.float32)
+    _, outs = b2.run_program(p, "transpose", {"in": a.tolist(), "out": [0.0] * a.size, "W": 128, "H": 64})
+    assert outs["out"] == a.reshape(64, 128).T.reshape(-1).tolist()
+    with pytest.raises(b2.UnsupportedProgram):
+        b2.run_program(p, "transpose", {"in": a.tolist(), "out": [0.0] * a.size, "W": 128, "H": 64},
+                       backend="kernels")

@@ -34,6 +34,8 @@ struct Tuning {
     int t_ctas_per_sm = 0;  // 0 = auto (~kInflightBytesPerSM of tiles per SM)
     int r_variant = 0;      // reduce <threads, unroll> instantiation
     int r_ctas_per_sm = 0;  // 0 = auto (kReduceThreadsPerSM threads per SM)
+    int t_tma = 0;          // 1 = TMA-staged transpose for 4-byte cells (transpose_tma.cu)
+    int t_tma_stages = 4;   // input stages in flight per CTA (2, 3, 4, 6)
 };
 extern Tuning g_tune;
 constexpr int kInflightBytesPerSM = 64 * 1024;
@@ -59,6 +61,8 @@ __device__ __forceinline__ void stg_stream(uint4 *p, const uint4 &v) {
 // ---- kernel launchers (defined in transpose.cu / reduce.cu) ---------------
 int launch_transpose(const void *in, void *out, int64_t rows, int64_t cols, int64_t ld_in,
                      int64_t ld_out, int esize, int dev, cudaStream_t st);
+int launch_transpose_tma(const void *in, void *out, int64_t rows, int64_t cols, int64_t ld_in,
+                         int64_t ld_out, int dev, cudaStream_t st);
 
 size_t reduce_ws_bytes(int64_t n, int dtype, int dev);
 int launch_reduce(const void *in, int64_t n, int dtype, void *out, void *ws, size_t ws_bytes,

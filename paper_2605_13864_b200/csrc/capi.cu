@@ -144,6 +144,8 @@ static int *tune_slot(const char *key) {
     if (k == "transpose.ctas_per_sm") return &g_tune.t_ctas_per_sm;
     if (k == "reduce.variant") return &g_tune.r_variant;
     if (k == "reduce.ctas_per_sm") return &g_tune.r_ctas_per_sm;
+    if (k == "transpose.tma") return &g_tune.t_tma;
+    if (k == "transpose.tma_stages") return &g_tune.t_tma_stages;
     return nullptr;
 }
 

@@ -318,6 +318,12 @@ int dispatch(const void *in, void *out, int64_t rows, int64_t cols, int64_t ld_i
     // one row: out[c][0] = in[0][c];  one column: out[0][r] = in[r][0]
     if (rows == 1) return run_copy<T>(in, out, cols, 1, ld_out, dev, st);
     if (cols == 1) return run_copy<T>(in, out, rows, ld_in, 1, dev, st);
+    if constexpr (E == 4) {
+        if (g_tune.t_tma) {
+            const int rc = launch_transpose_tma(in, out, rows, cols, ld_in, ld_out, dev, st);
+            if (rc != B2_ERR_UNSUPPORTED) return rc;  // else: fall through to the LDG path
+        }
+    }
     const bool aligned = E >= 2 && ((uintptr_t)in % 16 == 0) && ((uintptr_t)out % 16 == 0) &&
                          (ld_in * E % 16 == 0) && (ld_out * E % 16 == 0);
     if (!aligned) return run_scalar<T>(in, out, 0, rows, 0, cols, ld_in, ld_out, dev, st);

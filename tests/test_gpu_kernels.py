@@ -155,3 +155,22 @@ def test_launch_counter(b2):
     b2.reduce_sum(torch.ones(100, device="cuda"))
     torch.cuda.synchronize()
     assert b2.launch_count() == n0 + 1
+
+
+@pytest.mark.parametrize("shape", [(64, 64), (1000, 1000), (333, 516), (4096, 4096), (100, 36), (65, 4100)])
+def test_tma_transpose_path(b2, shape):
+    from paper_2605_13864_b200 import _lib
+    _lib.tune("transpose.tma", 1)
+    try:
+        a = torch.randn(shape, device="cuda")
+        out = b2.transpose(a)
+        base = torch.zeros(shape[0], shape[1] + 12, device="cuda")
+        view = base[:, 4:4 + shape[1]]  # 16-B aligned start, pitched
+        view.copy_(a)
+        out2 = torch.full((shape[1], shape[0] + 4), -1.0, device="cuda")
+        b2.transpose(view, out2[:, :shape[0]])
+        torch.cuda.synchronize()
+        assert torch.equal(out, a.t())
+        assert torch.equal(out2[:, :shape[0]], a.t()) and bool((out2[:, shape[0]:] == -1).all())
+    finally:
+        _lib.tune("transpose.tma", 0)

@@ -35,7 +35,7 @@ struct Tuning {
     int r_variant = 0;      // reduce <threads, unroll> instantiation
     int r_ctas_per_sm = 0;  // 0 = auto (kReduceThreadsPerSM threads per SM)
     int t_tma = 0;          // 1 = TMA-staged transpose for 4-byte cells (transpose_tma.cu)
-    int t_tma_stages = 4;   // input stages in flight per CTA (2, 3, 4, 6)
+    int t_tma_stages = 2;   // input stages in flight per CTA (2, 3, 4, 6); 2 x 2 CTAs/SM measured best
 };
 extern Tuning g_tune;
 constexpr int kInflightBytesPerSM = 64 * 1024;

@@ -197,7 +197,9 @@ int run_tma(const void *in, void *out, int64_t rows, int64_t cols, int64_t ld_in
         B2_CUDA(cudaFuncSetAttribute(transpose_tma_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         attr[dev] = true;
     }
-    const int per_sm = g_tune.t_ctas_per_sm > 0 ? g_tune.t_ctas_per_sm : 1;
+    // 2 CTAs x 2 stages per SM (64 KB of tiles in flight) measured best on B200
+    // (profiles/r01_tma.md); deeper rings in one CTA serialise on its barriers.
+    const int per_sm = g_tune.t_ctas_per_sm > 0 ? g_tune.t_ctas_per_sm : 2;
     const int64_t grid = std::min<int64_t>(ntiles, (int64_t)num_sms(dev) * per_sm);
     const int group = (int)std::max<int64_t>(1, std::min<int64_t>(g_tune.t_group, tiles_r));
     transpose_tma_kernel<S><<<(unsigned)grid, 256, smem, st>>>(tin, tout, tiles_r, tiles_c, ntiles, group);

@@ -47,6 +47,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-graph", action="store_true", help="eager launches instead of a CUDA graph")
+    p.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                   help="gloo only to exercise the multi-rank path with several ranks on one GPU")
     p.add_argument("--paper-configs", action="store_true", default=True)
     p.add_argument("--rows", type=int, default=TILE_ROWS)
     p.add_argument("--cols", type=int, default=TILE_COLS)
@@ -222,10 +224,15 @@ def main():
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one process per GPU; the modulo only matters for --dist-backend gloo test runs
+    # that put several ranks on one device to exercise the N > 1 code path
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(args.dist_backend)
 
     import paper_2605_13864_b200 as b2
     from paper_2605_13864_b200 import ops
@@ -252,14 +259,20 @@ def main():
         if ev is not None:
             ev[2].record(st)
         if world > 1:
-            dist.reduce(partial, dst=0)
+            if args.dist_backend == "nccl":
+                dist.reduce(partial, dst=0)  # one NCCL reduce of the 8-byte partial
+            else:
+                dist.all_reduce(partial)  # gloo has no CUDA reduce
 
     # correctness spot checks (cheap, outside the timed region)
     step()
     torch.cuda.synchronize()
     assert torch.equal(out[:64, :64], a[:64, :64].t()) and torch.equal(out[-64:, -64:], a[-64:, -64:].t())
-    if world == 1:
-        assert int(partial.item()) == int(x.to(torch.int64).sum().item())
+    want = x.to(torch.int64).sum().reshape(1)
+    if world > 1:
+        dist.all_reduce(want)
+    if rank == 0:
+        assert int(partial.item()) == int(want.item()), "reduction combine mismatch"
 
     clk = ClockSampler(local)
     clk.start()

@@ -50,9 +50,10 @@ def parse():
     p.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                    help="gloo only to exercise the multi-rank path with several ranks on one GPU")
     p.add_argument("--paper-configs", action="store_true", default=True)
-    p.add_argument("--rows", type=int, default=TILE_ROWS)
-    p.add_argument("--cols", type=int, default=TILE_COLS)
-    p.add_argument("--n", type=int, default=RED_N)
+    # (long names: torchrun's own parser would swallow abbreviations like --n)
+    p.add_argument("--transpose-rows", dest="rows", type=int, default=TILE_ROWS)
+    p.add_argument("--transpose-cols", dest="cols", type=int, default=TILE_COLS)
+    p.add_argument("--reduce-n", dest="n", type=int, default=RED_N)
     return p.parse_args()
 
 

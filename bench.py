@@ -343,14 +343,19 @@ def main():
     peak, peak_src = peaks()
     ach_t = bytes_t / (ms_t / 1e3) / 1e9
     ach_r = bytes_r / (ms_r / 1e3) / 1e9
-    traffic = None
+    # ncu DRAM bytes of the profiled launch (profiles/ncu_summary.json, tools/prof_run.py
+    # at the default sizes); only meaningful when this run's launch has the same size
+    traffic = traffic_r = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
             prof = json.load(f)
-        traffic = prof.get("transpose", {}).get("dram_bytes_per_launch")
-        traffic_r = prof.get("reduce", {}).get("dram_bytes_per_launch")
+        pt, pr = prof.get("transpose", {}), prof.get("reduce", {})
+        if pt.get("algorithmic_bytes", 2 * TILE_ROWS * TILE_COLS * 4) == bytes_t:
+            traffic = pt.get("dram_bytes_per_launch")
+        if pr.get("algorithmic_bytes", RED_N * 4 + 8) == bytes_r:
+            traffic_r = pr.get("dram_bytes_per_launch")
     except Exception:
-        traffic_r = None
+        pass
 
     res = {
         "metric": "effective_GBps_transpose_plus_reduce", "value": value, "unit": "GB/s",
@@ -358,8 +363,11 @@ def main():
         "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "f32+i32", "data": "synthetic (torch.rand / randint on device)",
         "config": {"workload": workload_name(args), "rows": rows, "cols": cols, "n": n,
-                   "l2": "inputs (4 GiB each) larger than L2 (126 MB): no flush needed",
-                   "combine": "NCCL reduce of the int64 partial" if world > 1 else "none (1 GPU)"},
+                   "l2": (f"inputs ({bytes_t // 2 / 2**30:.2f} GiB + {n * 4 / 2**30:.2f} GiB) larger "
+                          "than L2 (126 MB): no flush needed" if min(bytes_t // 2, n * 4) > 2 * L2_BYTES
+                          else "WARNING: inputs not larger than 2x L2"),
+                   "combine": (f"{args.dist_backend} {'reduce' if args.dist_backend == 'nccl' else 'all_reduce'}"
+                               " of the int64 partial" if world > 1 else "none (1 GPU)")},
         "roofline": {"bound": "hbm", "kernel": "transpose_vec_kernel<4,16,16,256>",
                      "achieved": ach_t, "peak": peak, "unit": "GB/s", "frac": ach_t / peak,
                      "traffic": traffic, "algorithmic_bytes": bytes_t, "peak_source": peak_src},

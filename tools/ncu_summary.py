@@ -83,6 +83,8 @@ def main(tag):
         ns = to_ns(r["gpu__time_duration.sum"])
         summary[name] = {"kernel": r["kernel"], "source": f"ncu --set full ({rep})",
                          "dram_bytes_per_launch": rb + wb, "dram_read": rb, "dram_write": wb,
+                         # tools/prof_run.py default sizes: fp32 32768^2 / int32 2^30
+                         "algorithmic_bytes": 2 * 32768 * 32768 * 4 if name == "transpose" else (1 << 30) * 4 + 8,
                          "duration_ns_ncu": ns, "dram_GBps_ncu": (rb + wb) / ns,
                          "metrics": {k: v for k, v in r.items() if k != "kernel"}}
     lp = os.path.join(OUT, "launches.csv")

@@ -165,6 +165,11 @@ __device__ __forceinline__ bool b2_chk(int64_t ix, int64_t d, int *f) {
 }
 template <typename T> struct B2Host { T *p = nullptr; int64_t n = 0; int64_t rank = 0; int64_t dims[8] = {0}; uint8_t *init = nullptr; bool freed = false; bool owned = false; };
 template <typename T> struct B2Dev { T *p = nullptr; int64_t n = 0; int64_t rank = 0; int64_t dims[8] = {0}; bool freed = false; };
+// kernel-only device time of the last launch of each kernel (PAPER.md:1100-1102
+// measures generated kernels this way: host copies excluded)
+static float b2_kernel_ms[64];
+static cudaEvent_t b2_ev0, b2_ev1;
+extern "C" double b2g_kernel_ms(int k) { return (k >= 0 && k < 64) ? b2_kernel_ms[k] : -1.0; }
 static std::vector<void *> *g_dev_allocs;
 static std::vector<void *> *g_host_allocs;
 template <typename T> static B2Dev<T> b2_dev_alloc(int64_t rank, std::initializer_list<int64_t> d) {
@@ -582,8 +587,11 @@ class _Gen:
         out.append(pad + f"  if ({g} > 0 && {t} > 0) {{")
         out.append(pad + f"    if ({smem_bytes} > 48 * 1024) cudaFuncSetAttribute({name}, cudaFuncAttributeMaxDynamicSharedMemorySize, (int){smem_bytes});")
         out.append(pad + "    cudaMemset(b2_err_dev, 0, 5 * sizeof(int));")
+        out.append(pad + "    cudaEventRecord(b2_ev0, 0);")
         out.append(pad + f"    {name}<<<(unsigned){g}, (unsigned){t}, (size_t){smem_bytes}>>>({', '.join(args)});")
+        out.append(pad + "    cudaEventRecord(b2_ev1, 0);")
         out.append(pad + f"    b2_check_kernel(b2_err_dev, \"{name}\");")
+        out.append(pad + f"    {{ float ms = 0; cudaEventElapsedTime(&ms, b2_ev0, b2_ev1); b2_kernel_ms[{self.nk - 1}] = ms; }}")
         out.append(pad + "  }")
         out.append(pad + "}")
 
@@ -612,6 +620,7 @@ class _Gen:
         src.append("    *ret_kind = 0;")
         src.append("    try {")
         src.append("        if (cudaMalloc((void **)&b2_err_dev, 8 * sizeof(int)) != cudaSuccess) b2_throw(\"cudaMalloc failed\");")
+        src.append("        if (!b2_ev0) { cudaEventCreate(&b2_ev0); cudaEventCreate(&b2_ev1); }")
         src.extend(decl)
         src.extend(body)
         src.append("        return 0;")
@@ -845,6 +854,13 @@ class Compiled:
         self.lib = ctypes.CDLL(path)
         self.lib.b2g_main.restype = ctypes.c_int
         self.lib.b2g_main.argtypes = [ctypes.c_void_p] * 8
+        self.lib.b2g_kernel_ms.restype = ctypes.c_double
+        self.lib.b2g_kernel_ms.argtypes = [ctypes.c_int]
+        self.n_kernels = source.count("__global__ void b2g_kernel")
+
+    def kernel_ms(self) -> list:
+        """Device time (CUDA events) of each kernel's last launch, in ms."""
+        return [self.lib.b2g_kernel_ms(k) for k in range(self.n_kernels)]
 
 
 class B2Arr(ctypes.Structure):

@@ -136,13 +136,6 @@ __device__ __forceinline__ void b2_flag(int *f, int code, int64_t a, int64_t b) 
 __host__ __device__ __forceinline__ int64_t b2_div(int64_t a, int64_t b) { return b ? a / b : 0; }
 __host__ __device__ __forceinline__ int64_t b2_mod(int64_t a, int64_t b) { return b ? a - (a / b) * b : 0; }
 __host__ __device__ __forceinline__ int64_t b2_pow2(int64_t k) { return k < 0 ? 0 : ((int64_t)1 << k); }
-// thread-for index math: rel, w >= 0; 32-bit divide whenever both fit (the usual case)
-__device__ __forceinline__ int64_t b2_udiv(int64_t a, int64_t b) {
-    return ((uint64_t)(a | b) >> 32) == 0 ? (int64_t)((uint32_t)a / (uint32_t)b) : a / b;
-}
-__device__ __forceinline__ int64_t b2_umod(int64_t a, int64_t b) {
-    return ((uint64_t)(a | b) >> 32) == 0 ? (int64_t)((uint32_t)a % (uint32_t)b) : a % b;
-}
 static inline int64_t b2_exact_div_h(int64_t a, int64_t b) {
     if (b == 0 || a % b != 0) b2_throw("exact_div(" + std::to_string(a) + ", " + std::to_string(b) + ") is not exact");
     return a / b;
@@ -763,8 +756,8 @@ class _KernelCtx:
                 out.append(pad + f"  if ({n} > 0) {{")
                 out.append(pad + f"  if ({w} % {n} != 0) {{ b2_flag(b2_err, B2E_WIDTH, {n}, {w}); return; }}")
                 out.append(pad + f"  const int64_t {w2} = {w} / {n};")
-                out.append(pad + f"  const int64_t {v} = ({s0}) + b2_udiv({rel}, {w2});")
-                out.append(pad + f"  const int64_t {r2} = b2_umod({rel}, {w2});")
+                out.append(pad + f"  const int64_t {v} = ({s0}) + {rel} / {w2};")
+                out.append(pad + f"  const int64_t {r2} = {rel} % {w2};")
                 self.emit_seq(st.body.stmts, out, ind + 1, w2, r2)
                 out.append(pad + "  } }")
                 return

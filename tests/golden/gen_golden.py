@@ -218,7 +218,37 @@ def codegen_cases():
                    "errors": errs}, f, indent=1)
 
 
+def family_cases():
+    """Reference outputs for members of the parametrised program families
+    (tests/program_families.py); pins the numpy restatement of each family."""
+    sys.path.insert(0, os.path.dirname(HERE))
+    from program_families import np_reduce_family, reduce_family, transpose_family
+    from minigpu.parser import parse_program as ref_parse
+    rng = np.random.default_rng(99)
+    out = []
+    for T, R in [(8, 2), (16, 16), (32, 8), (64, 4)]:
+        H, W = 2 * T, 3 * T
+        a = rng.uniform(-1, 1, (H, W)).astype(np.float32)
+        _, o = run_program(ref_parse(transpose_family(T, R)), "transpose",
+                           {"in": a.reshape(-1).tolist(), "out": [0.0] * (H * W), "W": W, "H": H})
+        ok = np.array_equal(np.array(o["out"], np.float32).reshape(W, H), a.T)
+        out.append({"family": "transpose", "T": T, "R": R, "shape": [H, W], "ref_equals_transpose": bool(ok)})
+        print(out[-1], flush=True)
+    for B, cell in [(64, "float"), (128, "int"), (256, "float"), (1024, "float"), (2048, "int")]:
+        n = 4 * B
+        x = rng.uniform(-1, 1, n).astype(np.float32) if cell == "float" else \
+            rng.integers(-2**31, 2**31, n, dtype=np.int64).astype(np.int32)
+        ret, _ = run_program(ref_parse(reduce_family(B, cell)), "reduce", {"arr": x.tolist(), "N": n})
+        mine = np_reduce_family(x, B)
+        ok = (np.float32(ret).view(np.uint32) == np.float32(mine).view(np.uint32)) if cell == "float" else ret == mine
+        out.append({"family": "reduce", "B": B, "cell": cell, "n": n, "ref_equals_restatement": bool(ok)})
+        print(out[-1], flush=True)
+    with open(os.path.join(HERE, "families_pinned.json"), "w") as f:
+        json.dump({"generator": "tests/golden/gen_golden.py (family_cases)", "members": out}, f, indent=1)
+
+
 if __name__ == "__main__":
     if not os.environ.get("GOLDEN_CODEGEN_ONLY"):
         main()
     codegen_cases()
+    family_cases()

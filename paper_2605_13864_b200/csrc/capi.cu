@@ -62,12 +62,18 @@ struct DevCtx {
 DevCtx g_ctx[64];
 
 int check_dev(int dev) {
-    int n = 0;
-    B2_CUDA(cudaGetDeviceCount(&n));
+    static std::atomic<int> s_count{-1};
+    int n = s_count.load(std::memory_order_relaxed);
+    if (n < 0) {
+        B2_CUDA(cudaGetDeviceCount(&n));
+        s_count.store(n, std::memory_order_relaxed);
+    }
     if (dev < 0 || dev >= n || dev >= 64)
         return fail(B2_ERR_INVALID, "device " + std::to_string(dev) + " out of range (have " +
                                         std::to_string(n) + ")");
-    B2_CUDA(cudaSetDevice(dev));
+    // cudaSetDevice is per host thread; skip it when this thread is already there
+    int cur = -1;
+    if (cudaGetDevice(&cur) != cudaSuccess || cur != dev) B2_CUDA(cudaSetDevice(dev));
     return B2_OK;
 }
 

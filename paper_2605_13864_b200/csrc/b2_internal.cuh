@@ -35,6 +35,7 @@ struct Tuning {
     int r_variant = 0;      // reduce <threads, unroll> instantiation
     int r_ctas_per_sm = 0;  // 0 = auto (kReduceThreadsPerSM threads per SM)
     int t_tma = 0;          // 1 = TMA-staged transpose for 4-byte cells (transpose_tma.cu)
+    int t_any = 1;          // 1 = funnel-shifted 128-bit path for unaligned pitches, 0 = padded scalar tile
     int t_tma_stages = 2;   // input stages in flight per CTA (2, 3, 4, 6); 2 x 2 CTAs/SM measured best
 };
 extern Tuning g_tune;
@@ -63,6 +64,8 @@ int launch_transpose(const void *in, void *out, int64_t rows, int64_t cols, int6
                      int64_t ld_out, int esize, int dev, cudaStream_t st);
 int launch_transpose_tma(const void *in, void *out, int64_t rows, int64_t cols, int64_t ld_in,
                          int64_t ld_out, int dev, cudaStream_t st);
+int launch_transpose_any(const void *in, void *out, int64_t rows, int64_t cols, int64_t ld_in,
+                         int64_t ld_out, int esize, int dev, cudaStream_t st);
 
 size_t reduce_ws_bytes(int64_t n, int dtype, int dev);
 int launch_reduce(const void *in, int64_t n, int dtype, void *out, void *ws, size_t ws_bytes,

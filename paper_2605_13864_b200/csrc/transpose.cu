@@ -326,7 +326,13 @@ int dispatch(const void *in, void *out, int64_t rows, int64_t cols, int64_t ld_i
     }
     const bool aligned = E >= 2 && ((uintptr_t)in % 16 == 0) && ((uintptr_t)out % 16 == 0) &&
                          (ld_in * E % 16 == 0) && (ld_out * E % 16 == 0);
-    if (!aligned) return run_scalar<T>(in, out, 0, rows, 0, cols, ld_in, ld_out, dev, st);
+    if (!aligned) {
+        // odd pitches / unaligned views: funnel-shifted 128-bit path (transpose_any.cu)
+        if constexpr (E >= 2) {
+            if (g_tune.t_any) return launch_transpose_any(in, out, rows, cols, ld_in, ld_out, E, dev, st);
+        }
+        return run_scalar<T>(in, out, 0, rows, 0, cols, ld_in, ld_out, dev, st);
+    }
     const int64_t rv = rows - rows % V, cv = cols - cols % V;
     if constexpr (E >= 2) {
         int rc = run_vec_for<E>(in, out, rv, cv, ld_in, ld_out, dev, st);

@@ -110,22 +110,25 @@ __global__ void __launch_bounds__(NT)
     const int rl = threadIdx.x / NV;    // row within a pass
     uint4 reg[LP];
 
+    const int64_t ldiE = ld_in * E, ldoE = ld_out * E;
     auto load_tile = [&](int64_t tile) {
         const int64_t r0 = (tile / tiles_c) * TS, c0 = (tile % tiles_c) * TS;
-        const int64_t cend = min(c0 + TS, cols);
+        // per-tile base and extents; per row only a 64-bit multiply-add remains
+        const uint8_t *tb = in + r0 * ldiE + c0 * E;
+        const int seg = (int)(min(c0 + TS, cols) - c0) * E;  // valid bytes per row segment
+        const int nrows = (int)min((int64_t)TS, rows - r0);
 #pragma unroll
         for (int p = 0; p < LP; ++p) {
-            const int64_t R = r0 + p * RPP + rl;
+            const int r = p * RPP + rl;
             uint4 v = make_uint4(0, 0, 0, 0), nx = make_uint4(0, 0, 0, 0);
             int m = 0;
-            if (R < rows) {
-                const uintptr_t a0 = reinterpret_cast<uintptr_t>(in) + (uintptr_t)((R * ld_in + c0) * E);
-                const uintptr_t a1 = reinterpret_cast<uintptr_t>(in) + (uintptr_t)((R * ld_in + cend) * E);
-                const uintptr_t f = a0 & ~uintptr_t(15);
+            if (r < nrows) {
+                const uintptr_t a0 = reinterpret_cast<uintptr_t>(tb + r * ldiE);
                 m = (int)(a0 & 15);
-                const uintptr_t va = f + 16 * (uintptr_t)g;
-                if (va < a1) v = ldg_stream(reinterpret_cast<const uint4 *>(va));
-                if (g == NV - 1 && va + 16 < a1) nx = ldg_stream(reinterpret_cast<const uint4 *>(va + 16));
+                const int rel = 16 * g - m;  // this lane's aligned vector, relative to a0
+                const uintptr_t va = a0 - m + 16 * g;
+                if (rel < seg) v = ldg_stream(reinterpret_cast<const uint4 *>(va));
+                if (g == NV - 1 && rel + 16 < seg) nx = ldg_stream(reinterpret_cast<const uint4 *>(va + 16));
             }
             const uint4 up = shfl_down16(v, 1, NV);
             if (g != NV - 1) nx = up;
@@ -160,33 +163,42 @@ __global__ void __launch_bounds__(NT)
         __syncthreads();
         const int64_t next = tile + gridDim.x;
         if (next < ntiles) load_tile(next);
-        // store: aligned 16-B vectors per output row segment, masked at the ends
-        const int64_t rend = min(r0 + TS, rows);
-        for (int idx = threadIdx.x; idx < TS * (NV + 1); idx += NT) {
-            const int o = idx / (NV + 1), gv = idx % (NV + 1);
-            const int64_t OC = c0 + o;
-            if (OC >= cols) continue;
-            const uintptr_t b0 = reinterpret_cast<uintptr_t>(out) + (uintptr_t)((OC * ld_out + r0) * E);
-            const uintptr_t b1 = reinterpret_cast<uintptr_t>(out) + (uintptr_t)((OC * ld_out + rend) * E);
-            const uintptr_t fo = b0 & ~uintptr_t(15);
-            const int mo = (int)(b0 & 15);
-            if (mo == 0 && gv == NV) continue;
-            const uintptr_t va = fo + 16 * (uintptr_t)gv;
-            if (va >= b1) continue;
-            const uint4 zero = make_uint4(0, 0, 0, 0);
-            const uint4 s1 = gv < NV ? tout[o * NV + (gv ^ ((o / V) & 7))] : zero;
-            uint4 w = s1;
-            if (mo) {
-                const uint4 s0 = gv > 0 ? tout[o * NV + ((gv - 1) ^ ((o / V) & 7))] : zero;
-                w = funnel16(s0, s1, 16 - mo);
-            }
-            if (va >= b0 && va + 16 <= b1) {
-                stg_stream(reinterpret_cast<uint4 *>(va), w);
-            } else {
+        // store: aligned 16-B vectors per output row segment, masked at the ends.
+        // NV lanes per output row; the (NV+1)-th vector of a misaligned segment is
+        // taken by lane 0 of the row group as a second item.
+        const uint8_t *ob = out + c0 * ldoE + r0 * E;
+        const int oseg = (int)(min(r0 + TS, rows) - r0) * E;  // valid bytes per out row
+        const int orows = (int)min((int64_t)TS, cols - c0);
+        constexpr int RPI = NT / NV;                          // out rows per block iteration
 #pragma unroll
-                for (int k = 0; k < V; ++k) {
-                    const uintptr_t ca = va + k * E;
-                    if (ca >= b0 && ca < b1) store_cell<E>(reinterpret_cast<uint8_t *>(ca), w, k);
+        for (int it = 0; it < TS / RPI; ++it) {
+            const int o = it * RPI + rl;
+            if (o >= orows) continue;
+            const uintptr_t b0 = reinterpret_cast<uintptr_t>(ob + o * ldoE);
+            const int mo = (int)(b0 & 15);
+            const int sw = (o / V) & 7;
+#pragma unroll
+            for (int pass = 0; pass < 2; ++pass) {
+                const int gv = pass == 0 ? g : NV;
+                if (pass == 1 && (g != 0 || mo == 0)) break;
+                const int rel = 16 * gv - mo;  // vector start relative to b0
+                if (rel >= oseg) continue;
+                const uint4 zero = make_uint4(0, 0, 0, 0);
+                const uint4 s1 = gv < NV ? tout[o * NV + (gv ^ sw)] : zero;
+                uint4 w = s1;
+                if (mo) {
+                    const uint4 s0 = gv > 0 ? tout[o * NV + ((gv - 1) ^ sw)] : zero;
+                    w = funnel16(s0, s1, 16 - mo);
+                }
+                uint8_t *va = reinterpret_cast<uint8_t *>(b0 - mo + 16 * gv);
+                if (rel >= 0 && rel + 16 <= oseg) {
+                    stg_stream(reinterpret_cast<uint4 *>(va), w);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < V; ++k) {
+                        const int c = rel + k * E;
+                        if (c >= 0 && c < oseg) store_cell<E>(va + k * E, w, k);
+                    }
                 }
             }
         }

@@ -35,7 +35,9 @@ struct Tuning {
     int r_variant = 0;      // reduce <threads, unroll> instantiation
     int r_ctas_per_sm = 0;  // 0 = auto (kReduceThreadsPerSM threads per SM)
     int t_tma = 0;          // 1 = TMA-staged transpose for 4-byte cells (transpose_tma.cu)
-    int t_any = 1;          // 1 = funnel-shifted 128-bit path for unaligned pitches, 0 = padded scalar tile
+    int t_any = 0;          // 1 = funnel-shifted 128-bit path for unaligned pitches, 0 = padded scalar tile
+                            //     (measured: the scalar tile is faster, profiles/r01_odd.md)
+    int t_scalar_ctas = 4;  // CTAs per SM of the padded scalar tile kernel
     int t_tma_stages = 2;   // input stages in flight per CTA (2, 3, 4, 6); 2 x 2 CTAs/SM measured best
 };
 extern Tuning g_tune;

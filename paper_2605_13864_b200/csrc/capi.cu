@@ -152,6 +152,7 @@ static int *tune_slot(const char *key) {
     if (k == "reduce.ctas_per_sm") return &g_tune.r_ctas_per_sm;
     if (k == "transpose.tma") return &g_tune.t_tma;
     if (k == "transpose.any") return &g_tune.t_any;
+    if (k == "transpose.scalar_ctas") return &g_tune.t_scalar_ctas;
     if (k == "transpose.tma_stages") return &g_tune.t_tma_stages;
     return nullptr;
 }

@@ -268,7 +268,10 @@ int run_scalar(const void *in, void *out, int64_t r_lo, int64_t r_hi, int64_t c_
     if (r_hi <= r_lo || c_hi <= c_lo) return B2_OK;
     const int64_t tiles_r = (r_hi - r_lo + 63) / 64, tiles_c = (c_hi - c_lo + 63) / 64;
     const int64_t ntiles = tiles_r * tiles_c;
-    const int64_t grid = std::min<int64_t>(ntiles, (int64_t)num_sms(dev) * g_tune.t_scalar_ctas);
+    // same ~64 KB-of-tiles-in-flight rule as the vector path (profiles/r01_odd.md)
+    const int per_sm = g_tune.t_scalar_ctas > 0 ? g_tune.t_scalar_ctas
+                                                : std::max(1, kInflightBytesPerSM / (64 * 64 * (int)sizeof(T)));
+    const int64_t grid = std::min<int64_t>(ntiles, (int64_t)num_sms(dev) * per_sm);
     transpose_scalar_kernel<T><<<(unsigned)grid, 256, 0, st>>>(
         (const T *)in, (T *)out, r_lo, r_hi, c_lo, c_hi, ld_in, ld_out, tiles_c, ntiles);
     count_launch();

@@ -38,6 +38,7 @@ struct Tuning {
     int t_any = 0;          // 1 = funnel-shifted 128-bit path for unaligned pitches, 0 = padded scalar tile
                             //     (measured: the scalar tile is faster, profiles/r01_odd.md)
     int t_scalar_ctas = 0;  // CTAs per SM of the padded scalar tile kernel (0 = auto)
+    int h_chunk_mb = 64;    // host-pipeline chunk (MiB) for the *_host entry points
     int t_tma_stages = 2;   // input stages in flight per CTA (2, 3, 4, 6); 2 x 2 CTAs/SM measured best
 };
 extern Tuning g_tune;

@@ -127,7 +127,8 @@ int ensure_small(DevCtx &c, size_t bytes) {
 
 int esize_of(int dtype) { return (int)b2_dtype_size(dtype); }
 
-constexpr size_t kChunkBytes = size_t(256) << 20;  // host-pipeline stage size
+// host-pipeline stage size (b2_tune_set("host.chunk_mb", ...))
+inline size_t chunk_bytes() { return size_t(g_tune.h_chunk_mb > 0 ? g_tune.h_chunk_mb : 64) << 20; }
 
 }  // namespace
 }  // namespace b2
@@ -154,6 +155,7 @@ static int *tune_slot(const char *key) {
     if (k == "transpose.any") return &g_tune.t_any;
     if (k == "transpose.scalar_ctas") return &g_tune.t_scalar_ctas;
     if (k == "transpose.tma_stages") return &g_tune.t_tma_stages;
+    if (k == "host.chunk_mb") return &g_tune.h_chunk_mb;
     return nullptr;
 }
 
@@ -263,7 +265,7 @@ int b2_reduce_tree512_host(const float *in_host, int64_t n, float *result_host, 
     DevCtx &c = g_ctx[dev];
     std::lock_guard<std::mutex> g(c.mu);
     if (int rc = ctx_init(c, dev)) return rc;
-    int64_t ce = (int64_t)(kChunkBytes / sizeof(float));
+    int64_t ce = (int64_t)(chunk_bytes() / sizeof(float));
     ce -= ce % 512;
     ce = std::min(ce, n);
     if (int rc = ensure_stages(c, (size_t)ce * sizeof(float))) return rc;
@@ -314,7 +316,7 @@ int b2_transpose_host(const void *in_host, void *out_host, int64_t rows, int64_t
     if (int rc = ctx_init(c, dev)) return rc;
     // chunk = a block of input rows -> a column slab of the output
     const int64_t row_bytes = cols * E;
-    int64_t cr = std::max<int64_t>(1, (int64_t)(kChunkBytes / (size_t)row_bytes));
+    int64_t cr = std::max<int64_t>(1, (int64_t)(chunk_bytes() / (size_t)row_bytes));
     if (cr >= 64) cr -= cr % 64;  // whole tiles per chunk
     cr = std::min(cr, rows);
     if (int rc = ensure_stages(c, (size_t)cr * row_bytes)) return rc;
@@ -353,7 +355,7 @@ int b2_reduce_sum_host(const void *in_host, int64_t n, int dtype, void *out_host
     DevCtx &c = g_ctx[dev];
     std::lock_guard<std::mutex> g(c.mu);
     if (int rc = ctx_init(c, dev)) return rc;
-    const int64_t ce = std::min<int64_t>(std::max<int64_t>(n, 1), (int64_t)(kChunkBytes / E));
+    const int64_t ce = std::min<int64_t>(std::max<int64_t>(n, 1), (int64_t)(chunk_bytes() / E));
     if (int rc = ensure_stages(c, (size_t)ce * E)) return rc;
     const int64_t nchunks = n == 0 ? 1 : (n + ce - 1) / ce;
     if (int rc = ensure_small(c, (size_t)nchunks * 8)) return rc;

@@ -157,19 +157,25 @@ def test_launch_counter(b2):
     assert b2.launch_count() == n0 + 1
 
 
+@pytest.mark.parametrize("path", [0, 1])
 @pytest.mark.parametrize("dt", [torch.bfloat16, torch.float32, torch.float64])
 @pytest.mark.parametrize("rows,cols,oin,oout", [(63, 65, 1, 3), (130, 257, 3, 0), (1, 77, 1, 1), (77, 2, 0, 1),
                                                 (129, 129, 5, 7), (2000, 3, 1, 0), (3, 2000, 0, 2),
                                                 (1025, 1023, 7, 5)])
-def test_unaligned_views_funnel_path(b2, dt, rows, cols, oin, oout):
-    # misaligned bases and odd pitches go through transpose_any_kernel (funnel shifts,
-    # masked segment ends); neighbours of the output view must stay untouched
+def test_unaligned_views(b2, path, dt, rows, cols, oin, oout):
+    # misaligned bases and odd pitches: padded scalar tile (path 0, default) and the
+    # funnel-shift kernel (path 1); neighbours of the output view must stay untouched
+    from paper_2605_13864_b200 import _lib
     iv = {torch.bfloat16: torch.int16, torch.float32: torch.int32, torch.float64: torch.int64}[dt]
     src = torch.randn(rows, cols + oin + 3, device="cuda").to(dt)
     view = src[:, oin:oin + cols]
     dst = torch.full((cols, rows + oout + 5), 7.0, device="cuda").to(dt)
     oview = dst[:, oout:oout + rows]
-    b2.transpose(view, oview)
+    _lib.tune("transpose.any", path)
+    try:
+        b2.transpose(view, oview)
+    finally:
+        _lib.tune("transpose.any", 0)
     torch.cuda.synchronize()
     assert torch.equal(oview.view(iv), view.t().contiguous().view(iv))
     rest = torch.cat([dst[:, :oout].reshape(-1), dst[:, oout + rows:].reshape(-1)])

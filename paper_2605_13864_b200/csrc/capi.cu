@@ -4,9 +4,12 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <condition_variable>
 #include <cstring>
+#include <functional>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "b2_internal.cuh"
@@ -57,6 +60,9 @@ struct DevCtx {
     void *d_small = nullptr;  // per-chunk results / tree partials
     size_t small_bytes = 0;
     void *h_small = nullptr;  // pinned mirror of d_small
+    void *hs_in[kStages] = {nullptr, nullptr, nullptr};   // pinned staging (pageable sources)
+    void *hs_out[kStages] = {nullptr, nullptr, nullptr};  // pinned staging (pageable destinations)
+    size_t hs_bytes = 0;
 };
 
 DevCtx g_ctx[64];
@@ -113,6 +119,40 @@ int ensure_stages(DevCtx &c, size_t bytes) {
     return B2_OK;
 }
 
+int ensure_host_stages(DevCtx &c, size_t bytes) {
+    if (c.hs_bytes >= bytes) return B2_OK;
+    B2_CUDA(cudaStreamSynchronize(c.s_h2d));
+    B2_CUDA(cudaStreamSynchronize(c.s_d2h));
+    for (int k = 0; k < kStages; ++k) {
+        if (c.hs_in[k]) cudaFreeHost(c.hs_in[k]);
+        if (c.hs_out[k]) cudaFreeHost(c.hs_out[k]);
+        c.hs_in[k] = c.hs_out[k] = nullptr;
+    }
+    c.hs_bytes = 0;
+    for (int k = 0; k < kStages; ++k) {
+        B2_CUDA(cudaMallocHost(&c.hs_in[k], bytes));
+        B2_CUDA(cudaMallocHost(&c.hs_out[k], bytes));
+    }
+    c.hs_bytes = bytes;
+    return B2_OK;
+}
+
+void par_copy2d(void *dst, size_t dpitch, const void *src, size_t spitch, size_t width, size_t height);
+
+// H2D of `height` host rows (`width` bytes, pitch `spitch`) into contiguous device
+// memory on c.s_h2d, staged through c.hs_in[k] when the source is pageable.
+int h2d_rows(DevCtx &c, int k, bool staged, void *dst, const char *src, size_t spitch, size_t width,
+             size_t height) {
+    if (!staged) {
+        B2_CUDA(cudaMemcpy2DAsync(dst, width, src, spitch, width, height, cudaMemcpyHostToDevice, c.s_h2d));
+        return B2_OK;
+    }
+    B2_CUDA(cudaEventSynchronize(c.ev_in[k]));  // the DMA that last read hs_in[k] is done
+    par_copy2d(c.hs_in[k], width, src, spitch, width, height);
+    B2_CUDA(cudaMemcpyAsync(dst, c.hs_in[k], width * height, cudaMemcpyHostToDevice, c.s_h2d));
+    return B2_OK;
+}
+
 int ensure_small(DevCtx &c, size_t bytes) {
     if (c.small_bytes >= bytes) return B2_OK;
     if (c.d_small) cudaFree(c.d_small);
@@ -126,6 +166,101 @@ int ensure_small(DevCtx &c, size_t bytes) {
 }
 
 int esize_of(int dtype) { return (int)b2_dtype_size(dtype); }
+
+// ------------------------------------------------ staged copies for pageable host memory
+// The DMA engines only stream pinned memory at PCIe speed (55 GB/s measured on the
+// B200 box vs 29 / 18 GB/s H2D / D2H from pageable memory, profiles/r01_e2e_chunks.json).
+// Pageable buffers are therefore staged through pinned chunks by a small pool of host
+// threads, overlapped with the DMA of the neighbouring chunk.
+class CopyPool {
+  public:
+    explicit CopyPool(int n) {
+        for (int i = 0; i < n; ++i) th_.emplace_back([this, i] { loop(i + 1); });
+    }
+    ~CopyPool() {
+        {
+            std::lock_guard<std::mutex> g(m_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto &t : th_) t.join();
+    }
+    int size() const { return (int)th_.size() + 1; }
+    // run f(part) for part in [0, size()); the caller runs part 0
+    void run(const std::function<void(int)> &f) {
+        {
+            std::lock_guard<std::mutex> g(m_);
+            job_ = &f;
+            pending_ = (int)th_.size();
+            ++gen_;
+        }
+        cv_.notify_all();
+        f(0);
+        std::unique_lock<std::mutex> l(m_);
+        done_.wait(l, [this] { return pending_ == 0; });
+        job_ = nullptr;
+    }
+
+  private:
+    void loop(int part) {
+        uint64_t seen = 0;
+        for (;;) {
+            const std::function<void(int)> *job;
+            {
+                std::unique_lock<std::mutex> l(m_);
+                cv_.wait(l, [&] { return stop_ || gen_ != seen; });
+                if (stop_) return;
+                seen = gen_;
+                job = job_;
+            }
+            (*job)(part);
+            {
+                std::lock_guard<std::mutex> g(m_);
+                if (--pending_ == 0) done_.notify_one();
+            }
+        }
+    }
+    std::vector<std::thread> th_;
+    std::mutex m_;
+    std::condition_variable cv_, done_;
+    const std::function<void(int)> *job_ = nullptr;
+    int pending_ = 0;
+    uint64_t gen_ = 0;
+    bool stop_ = false;
+};
+
+CopyPool &copy_pool() {
+    static CopyPool *p = new CopyPool(std::max(1, std::min(8, (int)std::thread::hardware_concurrency() / 2)) - 1);
+    return *p;
+}
+
+// rows of `width` bytes, pitches in bytes, copied by all pool threads
+void par_copy2d(void *dst, size_t dpitch, const void *src, size_t spitch, size_t width, size_t height) {
+    CopyPool &pool = copy_pool();
+    const int parts = pool.size();
+    if (height == 1 || (dpitch == width && spitch == width)) {  // contiguous: split bytes
+        const size_t total = width * height, step = (total + parts - 1) / parts;
+        pool.run([&](int p) {
+            const size_t b = std::min(total, p * step), e = std::min(total, b + step);
+            if (e > b) memcpy((char *)dst + b, (const char *)src + b, e - b);
+        });
+        return;
+    }
+    const size_t step = (height + parts - 1) / parts;
+    pool.run([&](int p) {
+        const size_t b = std::min(height, p * step), e = std::min(height, b + step);
+        for (size_t r = b; r < e; ++r) memcpy((char *)dst + r * dpitch, (const char *)src + r * spitch, width);
+    });
+}
+
+bool is_pinned(const void *p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
 
 // host-pipeline stage size (b2_tune_set("host.chunk_mb", ...))
 inline size_t chunk_bytes() { return size_t(g_tune.h_chunk_mb > 0 ? g_tune.h_chunk_mb : 64) << 20; }
@@ -272,12 +407,15 @@ int b2_reduce_tree512_host(const float *in_host, int64_t n, float *result_host, 
     const int64_t nb = n / 512;
     if (int rc = ensure_small(c, (size_t)nb * sizeof(float))) return rc;
     const int64_t nchunks = (n + ce - 1) / ce;
+    const bool stage_in = !is_pinned(in_host);
+    if (stage_in && ensure_host_stages(c, (size_t)ce * sizeof(float))) return B2_ERR_NOMEM;
     for (int64_t i = 0; i < nchunks; ++i) {
         const int k = (int)(i % kStages);
         const int64_t e0 = i * ce, ne = std::min(ce, n - e0);
         if (i >= kStages) B2_CUDA(cudaStreamWaitEvent(c.s_h2d, c.ev_comp[k], 0));
-        B2_CUDA(cudaMemcpyAsync(c.d_in[k], in_host + e0, ne * sizeof(float), cudaMemcpyHostToDevice,
-                                c.s_h2d));
+        if (int rc = h2d_rows(c, k, stage_in, c.d_in[k], (const char *)(in_host + e0), ne * sizeof(float),
+                              ne * sizeof(float), 1))
+            return rc;
         B2_CUDA(cudaEventRecord(c.ev_in[k], c.s_h2d));
         B2_CUDA(cudaStreamWaitEvent(c.s_comp, c.ev_in[k], 0));
         if (int rc = launch_tree512((const float *)c.d_in[k], ne, (float *)c.d_small + e0 / 512, dev,
@@ -320,15 +458,26 @@ int b2_transpose_host(const void *in_host, void *out_host, int64_t rows, int64_t
     if (cr >= 64) cr -= cr % 64;  // whole tiles per chunk
     cr = std::min(cr, rows);
     if (int rc = ensure_stages(c, (size_t)cr * row_bytes)) return rc;
+    const bool stage_in = !is_pinned(in_host), stage_out = !is_pinned(out_host);
+    if ((stage_in || stage_out) && ensure_host_stages(c, (size_t)cr * row_bytes)) return B2_ERR_NOMEM;
     const char *hin = (const char *)in_host;
     char *hout = (char *)out_host;
     const int64_t nchunks = (rows + cr - 1) / cr;
+    // pageable destination: the D2H lands in hs_out[k]; the host scatters it into the
+    // output column slab one chunk later, overlapped with the next chunk's DMA
+    auto scatter = [&](int64_t j) -> int {
+        const int kk = (int)(j % kStages);
+        const int64_t r0 = j * cr, nr = std::min(cr, rows - r0);
+        B2_CUDA(cudaEventSynchronize(c.ev_out[kk]));
+        par_copy2d(hout + r0 * E, ld_out * E, c.hs_out[kk], nr * E, nr * E, cols);
+        return B2_OK;
+    };
     for (int64_t i = 0; i < nchunks; ++i) {
         const int k = (int)(i % kStages);
         const int64_t r0 = i * cr, nr = std::min(cr, rows - r0);
         if (i >= kStages) B2_CUDA(cudaStreamWaitEvent(c.s_h2d, c.ev_comp[k], 0));  // d_in[k] free
-        B2_CUDA(cudaMemcpy2DAsync(c.d_in[k], row_bytes, hin + r0 * ld_in * E, ld_in * E, row_bytes,
-                                  nr, cudaMemcpyHostToDevice, c.s_h2d));
+        if (int rc = h2d_rows(c, k, stage_in, c.d_in[k], hin + r0 * ld_in * E, ld_in * E, row_bytes, nr))
+            return rc;
         B2_CUDA(cudaEventRecord(c.ev_in[k], c.s_h2d));
         B2_CUDA(cudaStreamWaitEvent(c.s_comp, c.ev_in[k], 0));
         if (i >= kStages) B2_CUDA(cudaStreamWaitEvent(c.s_comp, c.ev_out[k], 0));  // d_out[k] free
@@ -336,10 +485,17 @@ int b2_transpose_host(const void *in_host, void *out_host, int64_t rows, int64_t
             return rc;
         B2_CUDA(cudaEventRecord(c.ev_comp[k], c.s_comp));
         B2_CUDA(cudaStreamWaitEvent(c.s_d2h, c.ev_comp[k], 0));
-        B2_CUDA(cudaMemcpy2DAsync(hout + r0 * E, ld_out * E, c.d_out[k], nr * E, nr * E, cols,
-                                  cudaMemcpyDeviceToHost, c.s_d2h));
+        if (stage_out)
+            B2_CUDA(cudaMemcpyAsync(c.hs_out[k], c.d_out[k], (size_t)nr * E * cols, cudaMemcpyDeviceToHost, c.s_d2h));
+        else
+            B2_CUDA(cudaMemcpy2DAsync(hout + r0 * E, ld_out * E, c.d_out[k], nr * E, nr * E, cols,
+                                      cudaMemcpyDeviceToHost, c.s_d2h));
         B2_CUDA(cudaEventRecord(c.ev_out[k], c.s_d2h));
+        if (stage_out && i > 0)
+            if (int rc = scatter(i - 1)) return rc;
     }
+    if (stage_out)
+        if (int rc = scatter(nchunks - 1)) return rc;
     B2_CUDA(cudaStreamSynchronize(c.s_d2h));
     B2_CUDA(cudaStreamSynchronize(c.s_comp));
     return B2_OK;
@@ -359,13 +515,15 @@ int b2_reduce_sum_host(const void *in_host, int64_t n, int dtype, void *out_host
     if (int rc = ensure_stages(c, (size_t)ce * E)) return rc;
     const int64_t nchunks = n == 0 ? 1 : (n + ce - 1) / ce;
     if (int rc = ensure_small(c, (size_t)nchunks * 8)) return rc;
+    const bool stage_in = n > 0 && !is_pinned(in_host);
+    if (stage_in && ensure_host_stages(c, (size_t)ce * E)) return B2_ERR_NOMEM;
     const char *hin = (const char *)in_host;
     for (int64_t i = 0; i < nchunks; ++i) {
         const int k = (int)(i % kStages);
         const int64_t e0 = i * ce, ne = std::min(ce, n - e0);
         if (i >= kStages) B2_CUDA(cudaStreamWaitEvent(c.s_h2d, c.ev_comp[k], 0));
         if (ne > 0)
-            B2_CUDA(cudaMemcpyAsync(c.d_in[k], hin + e0 * E, ne * E, cudaMemcpyHostToDevice, c.s_h2d));
+            if (int rc = h2d_rows(c, k, stage_in, c.d_in[k], hin + e0 * E, ne * E, ne * E, 1)) return rc;
         B2_CUDA(cudaEventRecord(c.ev_in[k], c.s_h2d));
         B2_CUDA(cudaStreamWaitEvent(c.s_comp, c.ev_in[k], 0));
         if (int rc = launch_reduce(c.d_in[k], std::max<int64_t>(ne, 0), dtype,

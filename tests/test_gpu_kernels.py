@@ -150,6 +150,32 @@ def test_host_paths(b2):
     assert abs(b2.reduce_sum(xf) - exact) <= oracle.f32_tolerance(xf.size, exact, absum)
 
 
+@pytest.mark.parametrize("pinned", [False, True])
+def test_host_paths_staging(b2, pinned):
+    # pageable buffers go through the pinned staging ring + host copy pool; pinned
+    # ones straight to the DMA engines; pitched sub-views of both directions
+    from paper_2605_13864_b200 import _lib
+    _lib.tune("host.chunk_mb", 1)  # many chunks: exercise ring reuse
+    try:
+        rng = np.random.default_rng(4)
+        big_in = rng.standard_normal((700, 530)).astype(np.float32)
+        big_out = np.full((520, 720), -3.0, dtype=np.float32)
+        if pinned:
+            t_in = torch.from_numpy(big_in).pin_memory()
+            t_out = torch.from_numpy(big_out).pin_memory()
+            big_in, big_out = t_in.numpy(), t_out.numpy()
+        b2.transpose(big_in[:690, 4:524], big_out[:, 8:698])
+        assert np.array_equal(big_out[:, 8:698], big_in[:690, 4:524].T)
+        assert (big_out[:, :8] == -3).all() and (big_out[:, 698:] == -3).all()
+        x = rng.uniform(-1, 1, 3 * 262144 + 512).astype(np.float32)
+        want, _ = oracle.reduce_f32_tree512(x)
+        assert np.float32(b2.reduce_tree512(x)).view(np.uint32) == np.float32(want).view(np.uint32)
+        xi = rng.integers(-2**31, 2**31, 2_000_003, dtype=np.int64).astype(np.int32)
+        assert b2.reduce_sum(xi) == oracle.reduce_i32(xi)
+    finally:
+        _lib.tune("host.chunk_mb", 64)
+
+
 def test_launch_counter(b2):
     n0 = b2.launch_count()
     b2.reduce_sum(torch.ones(100, device="cuda"))

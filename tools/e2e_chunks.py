@@ -54,5 +54,25 @@ for mb in [16, 32, 64, 128, 256, 512]:
     res.append({"what": "e2e", "chunk_mb": mb, "transpose_ms": tt * 1e3, "reduce_ms": tr * 1e3,
                 "e2e_GBps": step / (tt + tr) / 1e9})
     print(json.dumps(res[-1]), flush=True)
+# pageable host buffers (staged through the pinned ring + host copy pool)
+_lib.tune("host.chunk_mb", 64)
+pin_in, pin_out = np.empty((rows, cols), np.float32), np.empty((cols, rows), np.float32)
+pin_in[:] = 1.0
+px = np.ones(n, np.int32)
+t_in = {"in": b2.Array.from_numpy(pin_in), "out": b2.Array.from_numpy(pin_out), "W": cols, "H": rows}
+r_in = {"arr": b2.Array.from_numpy(px, "int"), "N": n}
+b2.run_program(tp, "transpose", t_in)
+b2.run_program(rp, "reduce", r_in)
+t0 = time.perf_counter()
+for _ in range(3):
+    b2.run_program(tp, "transpose", t_in)
+t1 = time.perf_counter()
+for _ in range(3):
+    b2.run_program(rp, "reduce", r_in)
+t2 = time.perf_counter()
+tt, tr = (t1 - t0) / 3, (t2 - t1) / 3
+res.append({"what": "e2e_pageable", "chunk_mb": 64, "transpose_ms": tt * 1e3, "reduce_ms": tr * 1e3,
+            "e2e_GBps": (2 * rows * cols * 4 + n * 4 + 8) / (tt + tr) / 1e9})
+print(json.dumps(res[-1]), flush=True)
 os.makedirs("gpurun_out", exist_ok=True)
 json.dump(res, open("gpurun_out/e2e_chunks.json", "w"), indent=1)

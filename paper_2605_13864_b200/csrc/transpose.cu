@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(NT)
     static_assert(TRV >= 8 && (TRV & (TRV - 1)) == 0, "swizzle needs >= 8 vector columns");
     constexpr int ST = TC * TRV / NT;  // 16-B stores per thread per tile
 
-    __shared__ uint4 S[TC * TRV];
+    extern __shared__ uint4 S[];  // TC * TRV vectors (dynamic: large tiles exceed 48 KB)
 
     uint4 reg[MT][V];
 
@@ -239,11 +239,15 @@ int run_vec(const void *in, void *out, int64_t rows_v, int64_t cols_v, int64_t l
     const int64_t tiles_r = (rows_v + TR - 1) / TR, tiles_c = (cols_v + TC - 1) / TC;
     const int64_t ntiles = tiles_r * tiles_c;
     if (ntiles == 0) return B2_OK;
+    constexpr int kSmem = TC * TRV * 16;
     static int occ[64] = {0};
     if (occ[dev] == 0) {
+        if (kSmem > 48 * 1024)
+            B2_CUDA(cudaFuncSetAttribute(transpose_vec_kernel<E, TRV, TCV, NT>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
         int o = 0;
         B2_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &o, transpose_vec_kernel<E, TRV, TCV, NT>, NT, 0));
+            &o, transpose_vec_kernel<E, TRV, TCV, NT>, NT, kSmem));
         occ[dev] = o > 0 ? o : 1;
     }
     // Default residency: ~64 KB of tile data in flight per SM. Measured on B200
@@ -254,7 +258,7 @@ int run_vec(const void *in, void *out, int64_t rows_v, int64_t cols_v, int64_t l
     const int per_sm = std::min(g_tune.t_ctas_per_sm > 0 ? g_tune.t_ctas_per_sm : auto_sm, occ[dev]);
     const int64_t grid = std::min<int64_t>(ntiles, (int64_t)num_sms(dev) * per_sm);
     const int group = (int)std::max<int64_t>(1, std::min<int64_t>(g_tune.t_group, tiles_r));
-    transpose_vec_kernel<E, TRV, TCV, NT><<<(unsigned)grid, NT, 0, st>>>(
+    transpose_vec_kernel<E, TRV, TCV, NT><<<(unsigned)grid, NT, kSmem, st>>>(
         (const uint8_t *)in, (uint8_t *)out, rows_v, cols_v, ld_in * E, ld_out * E, tiles_r,
         tiles_c, ntiles, group);
     count_launch();
@@ -290,6 +294,7 @@ int run_scalar_all(const void *in, void *out, int64_t rows, int64_t cols, int64_
 
 // Tile shapes per element size; g_tune.t_variant picks one (0 = default).
 //   4-byte: 0: 64x64   1: 128x64 (rows x cols)   2: 64x128   3: 256x32   4: 128x32
+//           5: 128x128 (512 thr)  6: 128x128 (256 thr)  7: 256x128 (512 thr, 128 KB smem)
 //   2-byte: 0: 128x128 1: 64x128                 2: 128x64
 //   8-byte: 0: 64x32   1: 32x32                  2: 64x64
 template <int E>
@@ -301,6 +306,9 @@ int run_vec_for(const void *in, void *out, int64_t rv, int64_t cv, int64_t ld_in
         if (v == 2) return run_vec<4, 16, 32, 256>(in, out, rv, cv, ld_in, ld_out, dev, st);
         if (v == 3) return run_vec<4, 64, 8, 256>(in, out, rv, cv, ld_in, ld_out, dev, st);
         if (v == 4) return run_vec<4, 32, 8, 256>(in, out, rv, cv, ld_in, ld_out, dev, st);
+        if (v == 5) return run_vec<4, 32, 32, 512>(in, out, rv, cv, ld_in, ld_out, dev, st);
+        if (v == 6) return run_vec<4, 32, 32, 256>(in, out, rv, cv, ld_in, ld_out, dev, st);
+        if (v == 7) return run_vec<4, 64, 32, 512>(in, out, rv, cv, ld_in, ld_out, dev, st);
         return run_vec<4, 16, 16, 256>(in, out, rv, cv, ld_in, ld_out, dev, st);
     } else if constexpr (E == 2) {
         if (v == 1) return run_vec<2, 8, 16, 128>(in, out, rv, cv, ld_in, ld_out, dev, st);

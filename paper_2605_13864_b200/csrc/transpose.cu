@@ -309,14 +309,19 @@ int run_vec_for(const void *in, void *out, int64_t rv, int64_t cv, int64_t ld_in
         if (v == 5) return run_vec<4, 32, 32, 512>(in, out, rv, cv, ld_in, ld_out, dev, st);
         if (v == 6) return run_vec<4, 32, 32, 256>(in, out, rv, cv, ld_in, ld_out, dev, st);
         if (v == 7) return run_vec<4, 64, 32, 512>(in, out, rv, cv, ld_in, ld_out, dev, st);
+        if (v == 8) return run_vec<4, 64, 16, 512>(in, out, rv, cv, ld_in, ld_out, dev, st);
+        if (v == 9) return run_vec<4, 32, 64, 512>(in, out, rv, cv, ld_in, ld_out, dev, st);
+        if (v == 10) return run_vec<4, 64, 32, 1024>(in, out, rv, cv, ld_in, ld_out, dev, st);
         return run_vec<4, 16, 16, 256>(in, out, rv, cv, ld_in, ld_out, dev, st);
     } else if constexpr (E == 2) {
         if (v == 1) return run_vec<2, 8, 16, 128>(in, out, rv, cv, ld_in, ld_out, dev, st);
         if (v == 2) return run_vec<2, 16, 8, 128>(in, out, rv, cv, ld_in, ld_out, dev, st);
+        if (v == 7) return run_vec<2, 32, 32, 512>(in, out, rv, cv, ld_in, ld_out, dev, st);
         return run_vec<2, 16, 16, 256>(in, out, rv, cv, ld_in, ld_out, dev, st);
     } else {
         if (v == 1) return run_vec<8, 16, 16, 256>(in, out, rv, cv, ld_in, ld_out, dev, st);
         if (v == 2) return run_vec<8, 32, 32, 256>(in, out, rv, cv, ld_in, ld_out, dev, st);
+        if (v == 7) return run_vec<8, 128, 32, 512>(in, out, rv, cv, ld_in, ld_out, dev, st);
         return run_vec<8, 32, 16, 256>(in, out, rv, cv, ld_in, ld_out, dev, st);
     }
 }

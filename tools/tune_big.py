@@ -27,19 +27,29 @@ def timeit(fn, reps=10):
     return statistics.median(ts)
 
 
-a = torch.empty((32768, 32768), device="cuda").uniform_()
-o = torch.empty_like(a)
-nb = 2 * a.numel() * 4
-for var, cpss in [(0, [0, 3, 4]), (5, [1, 2, 3]), (6, [1, 2, 3, 4]), (7, [1])]:
-    for cps in cpss:
-        for grp in [1, 4]:
-            _lib.tune("transpose.variant", var)
-            _lib.tune("transpose.ctas_per_sm", cps)
-            _lib.tune("transpose.group", grp)
-            o.zero_()
-            ms = timeit(lambda: b2.transpose(a, o))
-            ok = bool(torch.equal(o, a.t()))
-            res.append({"variant": var, "cps": cps, "group": grp, "ms": ms, "GBps": nb / ms / 1e6, "ok": ok})
-            print(json.dumps(res[-1]), flush=True)
+SWEEP = {
+    "float32": ((32768, 32768), [(0, [0]), (7, [1]), (8, [1, 2]), (9, [1]), (10, [1])]),
+    "bfloat16": ((32768, 65536), [(0, [0]), (7, [1])]),
+    "float64": ((16384, 32768), [(0, [0]), (7, [1])]),
+}
+for dtn, ((R, C), plan) in SWEEP.items():
+    dt = getattr(torch, dtn)
+    a = torch.empty((R, C), device="cuda", dtype=dt).uniform_()
+    o = torch.empty((C, R), device="cuda", dtype=dt)
+    nb = 2 * a.numel() * a.element_size()
+    for var, cpss in plan:
+        for cps in cpss:
+            for grp in [1, 2, 4]:
+                _lib.tune("transpose.variant", var)
+                _lib.tune("transpose.ctas_per_sm", cps)
+                _lib.tune("transpose.group", grp)
+                o.zero_()
+                ms = timeit(lambda: b2.transpose(a, o))
+                ok = bool(torch.equal(o, a.t()))
+                res.append({"dtype": dtn, "variant": var, "cps": cps, "group": grp, "ms": ms,
+                            "GBps": nb / ms / 1e6, "ok": ok})
+                print(json.dumps(res[-1]), flush=True)
+    del a, o
+    torch.cuda.empty_cache()
 os.makedirs("gpurun_out", exist_ok=True)
 json.dump(res, open("gpurun_out/tune_big.json", "w"), indent=1)

@@ -368,7 +368,10 @@ def main():
                           else "WARNING: inputs not larger than 2x L2"),
                    "combine": (f"{args.dist_backend} {'reduce' if args.dist_backend == 'nccl' else 'all_reduce'}"
                                " of the int64 partial" if world > 1 else "none (1 GPU)")},
-        "roofline": {"bound": "hbm", "kernel": "transpose_vec_kernel<4,16,16,256>",
+        "roofline": {"bound": "hbm",
+                     "kernel": ("transpose_vec_kernel<4,64,32,512> (256x128 fp32 tile, 1 CTA/SM)"
+                                if (rows // 256) * (cols // 128) >= 8 * 148 else
+                                "transpose_vec_kernel<4,16,16,256> (64x64 fp32 tile)"),
                      "achieved": ach_t, "peak": peak, "unit": "GB/s", "frac": ach_t / peak,
                      "traffic": traffic, "algorithmic_bytes": bytes_t, "peak_source": peak_src},
         "kernels": {

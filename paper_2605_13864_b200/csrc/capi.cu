@@ -283,6 +283,7 @@ static int *tune_slot(const char *key) {
     const std::string k(key);
     if (k == "transpose.variant") return &g_tune.t_variant;
     if (k == "transpose.group") return &g_tune.t_group;
+    if (k == "transpose.big") return &g_tune.t_big;
     if (k == "transpose.ctas_per_sm") return &g_tune.t_ctas_per_sm;
     if (k == "reduce.variant") return &g_tune.r_variant;
     if (k == "reduce.ctas_per_sm") return &g_tune.r_ctas_per_sm;

@@ -257,7 +257,9 @@ int run_vec(const void *in, void *out, int64_t rows_v, int64_t cols_v, int64_t l
     const int auto_sm = std::max(1, kInflightBytesPerSM / kTileBytes);
     const int per_sm = std::min(g_tune.t_ctas_per_sm > 0 ? g_tune.t_ctas_per_sm : auto_sm, occ[dev]);
     const int64_t grid = std::min<int64_t>(ntiles, (int64_t)num_sms(dev) * per_sm);
-    const int group = (int)std::max<int64_t>(1, std::min<int64_t>(g_tune.t_group, tiles_r));
+    // band height: 4 tile-rows for small tiles, 1 for the 128-KB tiles (tune_big sweep)
+    const int grp = g_tune.t_group > 0 ? g_tune.t_group : (kTileBytes >= 64 * 1024 ? 1 : 4);
+    const int group = (int)std::max<int64_t>(1, std::min<int64_t>(grp, tiles_r));
     transpose_vec_kernel<E, TRV, TCV, NT><<<(unsigned)grid, NT, kSmem, st>>>(
         (const uint8_t *)in, (uint8_t *)out, rows_v, cols_v, ld_in * E, ld_out * E, tiles_r,
         tiles_c, ntiles, group);
@@ -301,6 +303,19 @@ template <int E>
 int run_vec_for(const void *in, void *out, int64_t rv, int64_t cv, int64_t ld_in,
                 int64_t ld_out, int dev, cudaStream_t st) {
     const int v = g_tune.t_variant;
+    // Large matrices: one 128-KB tile per SM (256 x 512 B) — half as many concurrent
+    // DRAM row streams, each twice as long, measured +2.5 % for fp32 / fp64
+    // (profiles/r01_tune_big.md). Needs enough tiles to keep every SM busy.
+    const int64_t big_min_tiles = 8 * (int64_t)num_sms(dev);
+    if (v == 0 && g_tune.t_big) {
+        if constexpr (E == 4) {
+            if ((rv / 256) * (cv / 128) >= big_min_tiles)
+                return run_vec<4, 64, 32, 512>(in, out, rv, cv, ld_in, ld_out, dev, st);
+        } else if constexpr (E == 8) {
+            if ((rv / 256) * (cv / 64) >= big_min_tiles)
+                return run_vec<8, 128, 32, 512>(in, out, rv, cv, ld_in, ld_out, dev, st);
+        }
+    }
     if constexpr (E == 4) {
         if (v == 1) return run_vec<4, 32, 16, 256>(in, out, rv, cv, ld_in, ld_out, dev, st);
         if (v == 2) return run_vec<4, 16, 32, 256>(in, out, rv, cv, ld_in, ld_out, dev, st);

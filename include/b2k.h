@@ -127,6 +127,13 @@ B2_API int b2_reduce_tree512(const float *in, int64_t n, float *result_host, int
  * on the device, D2H of the partials, sequential binary32 host sum. Bit-exact. */
 B2_API int b2_reduce_tree512_host(const float *in_host, int64_t n, float *result_host, int dev);
 
+/* Synchronous bulk copies for generated host code (codegen.py), replacing the
+ * interpreter's element-wise memcpy_host_to_device / memcpy_device_to_host
+ * (interp.py:353-365): pinned host buffers go straight to the DMA engines,
+ * pageable ones are staged through the pinned ring by the host copy pool. */
+B2_API int b2_copy_h2d(void *dst_dev, const void *src_host, size_t bytes, int dev);
+B2_API int b2_copy_d2h(void *dst_host, const void *src_dev, size_t bytes, int dev);
+
 /* Block until all work this library queued on `stream` of `dev` is done. */
 B2_API int b2_sync(int dev, void *stream);
 

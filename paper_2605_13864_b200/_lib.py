@@ -37,6 +37,8 @@ SIGNATURES = {
     "b2_reduce_tree512": (_int, [_vp, _i64, _vp, _int, _vp]),
     "b2_reduce_tree512_host": (_int, [_vp, _i64, _vp, _int]),
     "b2_sync": (_int, [_int, _vp]),
+    "b2_copy_h2d": (_int, [_vp, _vp, _sz, _int]),
+    "b2_copy_d2h": (_int, [_vp, _vp, _sz, _int]),
 }
 
 

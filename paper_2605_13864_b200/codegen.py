@@ -210,22 +210,31 @@ template <typename T> static void b2_hwrite(B2Host<T> &a, int64_t nidx, const in
     a.p[o] = v;
     if (a.init) a.init[o] = 1;
 }
+// Host runtime services from libb200k.so (include/b2k.h): staged / pinned bulk
+// copies (b2_copy_h2d / b2_copy_d2h) and the device this call runs on.
+struct B2Ops {
+    int (*h2d)(void *, const void *, size_t, int);
+    int (*d2h)(void *, const void *, size_t, int);
+    const char *(*last_error)(void);
+    int64_t dev;
+};
+static const B2Ops *g_ops;
 template <typename T, typename S> static void b2_h2d(B2Dev<T> &d, B2Host<S> &s, int64_t n) {
     static_assert(sizeof(T) == sizeof(S), "memcpy between different cell types");
     if (d.freed || s.freed) b2_throw("use after free");
     if (n <= 0) return;
     if (n > s.n || n > d.n) b2_throw("list index out of range");
     if (s.init) for (int64_t i = 0; i < n; ++i) if (!s.init[i]) b2_throw("memcpy of uninitialized data");
-    cudaError_t e = cudaMemcpy(d.p, s.p, (size_t)n * sizeof(T), cudaMemcpyHostToDevice);
-    if (e != cudaSuccess) b2_throw(std::string("memcpy_host_to_device: ") + cudaGetErrorString(e));
+    if (g_ops->h2d(d.p, s.p, (size_t)n * sizeof(T), (int)g_ops->dev))
+        b2_throw(std::string("memcpy_host_to_device: ") + g_ops->last_error());
 }
 template <typename T, typename S> static void b2_d2h(B2Host<T> &d, B2Dev<S> &s, int64_t n) {
     static_assert(sizeof(T) == sizeof(S), "memcpy between different cell types");
     if (d.freed || s.freed) b2_throw("use after free");
     if (n <= 0) return;
     if (n > s.n || n > d.n) b2_throw("list index out of range");
-    cudaError_t e = cudaMemcpy(d.p, s.p, (size_t)n * sizeof(T), cudaMemcpyDeviceToHost);
-    if (e != cudaSuccess) b2_throw(std::string("memcpy_device_to_host: ") + cudaGetErrorString(e));
+    if (g_ops->d2h(d.p, s.p, (size_t)n * sizeof(T), (int)g_ops->dev))
+        b2_throw(std::string("memcpy_device_to_host: ") + g_ops->last_error());
     if (d.init) memset(d.init, 1, (size_t)n);
 }
 static void b2_check_kernel(int *flags_dev, const char *name) {
@@ -610,7 +619,9 @@ class _Gen:
         src = [PRELUDE]
         src.extend(self.kernels)
         src.append('extern "C" int b2g_main(B2Arr *arrs, const int64_t *ints, const double *flts, '
-                   'int64_t *ret_i, double *ret_f, int *ret_kind, char *err, int errlen) {')
+                   'int64_t *ret_i, double *ret_f, int *ret_kind, char *err, int errlen, const B2Ops *ops) {')
+        src.append("    g_ops = ops;")
+        src.append("    if (cudaSetDevice((int)ops->dev) != cudaSuccess) { snprintf(err, errlen, \"bad device\"); return 1; }")
         src.append("    std::vector<void *> dev_allocs, host_allocs;")
         src.append("    g_dev_allocs = &dev_allocs; g_host_allocs = &host_allocs;")
         src.append("    int *b2_err_dev = nullptr;")
@@ -853,7 +864,7 @@ class Compiled:
         self.source = source
         self.lib = ctypes.CDLL(path)
         self.lib.b2g_main.restype = ctypes.c_int
-        self.lib.b2g_main.argtypes = [ctypes.c_void_p] * 8
+        self.lib.b2g_main.argtypes = [ctypes.c_void_p] * 9
         self.lib.b2g_kernel_ms.restype = ctypes.c_double
         self.lib.b2g_kernel_ms.argtypes = [ctypes.c_int]
         self.n_kernels = source.count("__global__ void b2g_kernel")
@@ -861,6 +872,19 @@ class Compiled:
     def kernel_ms(self) -> list:
         """Device time (CUDA events) of each kernel's last launch, in ms."""
         return [self.lib.b2g_kernel_ms(k) for k in range(self.n_kernels)]
+
+
+class B2Ops(ctypes.Structure):
+    """Host runtime services handed to generated code (libb200k.so copy engine)."""
+    _fields_ = [("h2d", ctypes.c_void_p), ("d2h", ctypes.c_void_p), ("last_error", ctypes.c_void_p),
+                ("dev", ctypes.c_int64)]
+
+
+def _ops(dev: int) -> B2Ops:
+    from ._lib import lib
+    L = lib()
+    addr = lambda f: ctypes.cast(f, ctypes.c_void_p).value  # noqa: E731
+    return B2Ops(addr(L.b2_copy_h2d), addr(L.b2_copy_d2h), addr(L.b2_last_error), dev)
 
 
 class B2Arr(ctypes.Structure):
@@ -930,8 +954,10 @@ def run_compiled(c: Compiled, env: dict, arrays: dict):
     rf = ctypes.c_double(0.0)
     rk = ctypes.c_int(0)
     err = ctypes.create_string_buffer(1024)
+    from .ops import _host_device
+    ops = _ops(_host_device())
     rc = c.lib.b2g_main(ctypes.addressof(arrs), ctypes.addressof(ints), ctypes.addressof(flts),
-                        ctypes.byref(ri), ctypes.byref(rf), ctypes.byref(rk), err, 1024)
+                        ctypes.byref(ri), ctypes.byref(rf), ctypes.byref(rk), err, 1024, ctypes.byref(ops))
     for a, buf, init, wb in writeback:
         wb(buf, init)
     if rc != 0:

@@ -439,6 +439,62 @@ int b2_sync(int dev, void *stream) {
     return B2_OK;
 }
 
+// ------------------------------------------------------------ bulk copies
+int b2_copy_h2d(void *dst_dev, const void *src_host, size_t bytes, int dev) {
+    if (!bytes) return B2_OK;
+    if (!dst_dev || !src_host) return fail(B2_ERR_INVALID, "copy: NULL buffer");
+    if (int rc = check_dev(dev)) return rc;
+    DevCtx &c = g_ctx[dev];
+    std::lock_guard<std::mutex> g(c.mu);
+    if (int rc = ctx_init(c, dev)) return rc;
+    const bool staged = !is_pinned(src_host);
+    const size_t cb = chunk_bytes();
+    if (staged && ensure_host_stages(c, std::min(bytes, cb))) return B2_ERR_NOMEM;
+    const size_t nchunks = staged ? (bytes + cb - 1) / cb : 1;
+    for (size_t i = 0; i < nchunks; ++i) {
+        const int k = (int)(i % kStages);
+        const size_t off = i * cb, n = staged ? std::min(cb, bytes - off) : bytes;
+        if (int rc = h2d_rows(c, k, staged, (char *)dst_dev + off, (const char *)src_host + off, n, n, 1))
+            return rc;
+        B2_CUDA(cudaEventRecord(c.ev_in[k], c.s_h2d));
+    }
+    B2_CUDA(cudaStreamSynchronize(c.s_h2d));
+    return B2_OK;
+}
+
+int b2_copy_d2h(void *dst_host, const void *src_dev, size_t bytes, int dev) {
+    if (!bytes) return B2_OK;
+    if (!dst_host || !src_dev) return fail(B2_ERR_INVALID, "copy: NULL buffer");
+    if (int rc = check_dev(dev)) return rc;
+    DevCtx &c = g_ctx[dev];
+    std::lock_guard<std::mutex> g(c.mu);
+    if (int rc = ctx_init(c, dev)) return rc;
+    if (is_pinned(dst_host)) {
+        B2_CUDA(cudaMemcpyAsync(dst_host, src_dev, bytes, cudaMemcpyDeviceToHost, c.s_d2h));
+        B2_CUDA(cudaStreamSynchronize(c.s_d2h));
+        return B2_OK;
+    }
+    const size_t cb = chunk_bytes();
+    if (ensure_host_stages(c, std::min(bytes, cb))) return B2_ERR_NOMEM;
+    const size_t nchunks = (bytes + cb - 1) / cb;
+    auto drain = [&](size_t j) -> int {  // host copy of chunk j out of its pinned stage
+        const int kk = (int)(j % kStages);
+        const size_t off = j * cb, n = std::min(cb, bytes - off);
+        B2_CUDA(cudaEventSynchronize(c.ev_out[kk]));
+        par_copy2d((char *)dst_host + off, n, c.hs_out[kk], n, n, 1);
+        return B2_OK;
+    };
+    for (size_t i = 0; i < nchunks; ++i) {
+        const int k = (int)(i % kStages);
+        const size_t off = i * cb, n = std::min(cb, bytes - off);
+        B2_CUDA(cudaMemcpyAsync(c.hs_out[k], (const char *)src_dev + off, n, cudaMemcpyDeviceToHost, c.s_d2h));
+        B2_CUDA(cudaEventRecord(c.ev_out[k], c.s_d2h));
+        if (i > 0)
+            if (int rc = drain(i - 1)) return rc;
+    }
+    return drain(nchunks - 1);
+}
+
 // ------------------------------------------------------------ host pipelines
 int b2_transpose_host(const void *in_host, void *out_host, int64_t rows, int64_t cols,
                       int64_t ld_in, int64_t ld_out, int dtype, int dev) {

@@ -77,6 +77,25 @@ def main():
         ms = statistics.median(ts)
         res.append({"program": label, "kernel": "hand-written", "ms": ms, "GBps": nbytes / ms / 1e6})
         print(json.dumps(res[-1]), flush=True)
+    # end to end through run_program (host Arrays, generated host code, copy engine)
+    import time
+    N2 = 8192
+    big = rng.uniform(-1, 1, (N2, N2)).astype(np.float32)
+    for label, pin in [("pageable", False), ("pinned", True)]:
+        src = torch.from_numpy(big.reshape(-1)).pin_memory().numpy() if pin else big.reshape(-1).copy()
+        dst = torch.zeros(N2 * N2, dtype=torch.float32).pin_memory().numpy() if pin else np.zeros(N2 * N2, np.float32)
+        p = prog("transpose_gpu.optc")
+        inputs = {"in": b2.Array.from_numpy(src), "out": b2.Array.from_numpy(dst), "W": N2, "H": N2}
+        b2.run_program(p, "transpose", inputs, backend="codegen")
+        t0 = time.perf_counter()
+        for _ in range(3):
+            b2.run_program(p, "transpose", inputs, backend="codegen")
+        dt = (time.perf_counter() - t0) / 3
+        assert np.array_equal(dst.reshape(N2, N2), big.T)
+        res.append({"program": "transpose_gpu.optc e2e " + label, "kernel": "generated + host copies",
+                    "ms": dt * 1e3, "GBps": 2 * N2 * N2 * 4 / dt / 1e9,
+                    "note": "run_program wall time: H2D + kernel + D2H through b2_copy_h2d/d2h"})
+        print(json.dumps(res[-1]), flush=True)
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     with open(os.path.join(ROOT, "gpurun_out", "bench_codegen.json"), "w") as f:
         json.dump(res, f, indent=1)

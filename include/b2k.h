@@ -133,6 +133,10 @@ B2_API int b2_reduce_tree512_host(const float *in_host, int64_t n, float *result
  * pageable ones are staged through the pinned ring by the host copy pool. */
 B2_API int b2_copy_h2d(void *dst_dev, const void *src_host, size_t bytes, int dev);
 B2_API int b2_copy_d2h(void *dst_host, const void *src_dev, size_t bytes, int dev);
+/* Caching device allocator for generated code's gmem_malloc / gmem_free
+ * (intrinsics.py:107-161 gmem contracts): 2 MiB-rounded blocks reused across calls. */
+B2_API int b2_device_alloc(size_t bytes, int dev, void **out);
+B2_API int b2_device_free(void *ptr, int dev);
 
 /* Block until all work this library queued on `stream` of `dev` is done. */
 B2_API int b2_sync(int dev, void *stream);

@@ -170,6 +170,17 @@ template <typename T> struct B2Dev { T *p = nullptr; int64_t n = 0; int64_t rank
 static float b2_kernel_ms[64];
 static cudaEvent_t b2_ev0, b2_ev1;
 extern "C" double b2g_kernel_ms(int k) { return (k >= 0 && k < 64) ? b2_kernel_ms[k] : -1.0; }
+// Host runtime services from libb200k.so (include/b2k.h): staged / pinned bulk
+// copies, the caching device allocator, and the device this call runs on.
+struct B2Ops {
+    int (*h2d)(void *, const void *, size_t, int);
+    int (*d2h)(void *, const void *, size_t, int);
+    const char *(*last_error)(void);
+    int (*alloc)(size_t, int, void **);
+    int (*dfree)(void *, int);
+    int64_t dev;
+};
+static const B2Ops *g_ops;
 static std::vector<void *> *g_dev_allocs;
 static std::vector<void *> *g_host_allocs;
 template <typename T> static B2Dev<T> b2_dev_alloc(int64_t rank, std::initializer_list<int64_t> d) {
@@ -177,8 +188,8 @@ template <typename T> static B2Dev<T> b2_dev_alloc(int64_t rank, std::initialize
     for (int64_t x : d) { a.dims[i++] = x; a.n *= x; }
     if (a.n < 0) a.n = 0;
     if (a.n > 0) {
-        cudaError_t e = cudaMalloc((void **)&a.p, (size_t)a.n * sizeof(T));
-        if (e != cudaSuccess) b2_throw(std::string("gmem_malloc: ") + cudaGetErrorString(e));
+        if (g_ops->alloc((size_t)a.n * sizeof(T), (int)g_ops->dev, (void **)&a.p))
+            b2_throw(std::string("gmem_malloc: ") + g_ops->last_error());
         g_dev_allocs->push_back(a.p);
     }
     return a;
@@ -210,15 +221,6 @@ template <typename T> static void b2_hwrite(B2Host<T> &a, int64_t nidx, const in
     a.p[o] = v;
     if (a.init) a.init[o] = 1;
 }
-// Host runtime services from libb200k.so (include/b2k.h): staged / pinned bulk
-// copies (b2_copy_h2d / b2_copy_d2h) and the device this call runs on.
-struct B2Ops {
-    int (*h2d)(void *, const void *, size_t, int);
-    int (*d2h)(void *, const void *, size_t, int);
-    const char *(*last_error)(void);
-    int64_t dev;
-};
-static const B2Ops *g_ops;
 template <typename T, typename S> static void b2_h2d(B2Dev<T> &d, B2Host<S> &s, int64_t n) {
     static_assert(sizeof(T) == sizeof(S), "memcpy between different cell types");
     if (d.freed || s.freed) b2_throw("use after free");
@@ -626,11 +628,13 @@ class _Gen:
         src.append("    g_dev_allocs = &dev_allocs; g_host_allocs = &host_allocs;")
         src.append("    int *b2_err_dev = nullptr;")
         src.append("    struct Cleanup { std::vector<void *> &d, &h; int **e; ~Cleanup() {")
-        src.append("        for (void *p : d) cudaFree(p); for (void *p : h) free(p); if (*e) cudaFree(*e); } }")
+        src.append("        cudaDeviceSynchronize();")
+        src.append("        for (void *p : d) g_ops->dfree(p, (int)g_ops->dev); for (void *p : h) free(p);")
+        src.append("        if (*e) g_ops->dfree(*e, (int)g_ops->dev); } }")
         src.append("        cleanup{dev_allocs, host_allocs, &b2_err_dev};")
         src.append("    *ret_kind = 0;")
         src.append("    try {")
-        src.append("        if (cudaMalloc((void **)&b2_err_dev, 8 * sizeof(int)) != cudaSuccess) b2_throw(\"cudaMalloc failed\");")
+        src.append("        if (g_ops->alloc(8 * sizeof(int), (int)g_ops->dev, (void **)&b2_err_dev)) b2_throw(g_ops->last_error());")
         src.append("        if (!b2_ev0) { cudaEventCreate(&b2_ev0); cudaEventCreate(&b2_ev1); }")
         src.extend(decl)
         src.extend(body)
@@ -877,14 +881,15 @@ class Compiled:
 class B2Ops(ctypes.Structure):
     """Host runtime services handed to generated code (libb200k.so copy engine)."""
     _fields_ = [("h2d", ctypes.c_void_p), ("d2h", ctypes.c_void_p), ("last_error", ctypes.c_void_p),
-                ("dev", ctypes.c_int64)]
+                ("alloc", ctypes.c_void_p), ("dfree", ctypes.c_void_p), ("dev", ctypes.c_int64)]
 
 
 def _ops(dev: int) -> B2Ops:
     from ._lib import lib
     L = lib()
     addr = lambda f: ctypes.cast(f, ctypes.c_void_p).value  # noqa: E731
-    return B2Ops(addr(L.b2_copy_h2d), addr(L.b2_copy_d2h), addr(L.b2_last_error), dev)
+    return B2Ops(addr(L.b2_copy_h2d), addr(L.b2_copy_d2h), addr(L.b2_last_error),
+                 addr(L.b2_device_alloc), addr(L.b2_device_free), dev)
 
 
 class B2Arr(ctypes.Structure):

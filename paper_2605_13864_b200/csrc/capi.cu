@@ -7,7 +7,9 @@
 #include <condition_variable>
 #include <cstring>
 #include <functional>
+#include <map>
 #include <mutex>
+#include <unordered_map>
 #include <string>
 #include <thread>
 #include <vector>
@@ -436,6 +438,73 @@ int b2_reduce_tree512_host(const float *in_host, int64_t n, float *result_host, 
 int b2_sync(int dev, void *stream) {
     if (int rc = check_dev(dev)) return rc;
     B2_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+    return B2_OK;
+}
+
+// ------------------------------------------------------------ caching device allocator
+// Generated programs gmem_malloc / gmem_free their arrays on every call; cudaMalloc
+// and cudaFree of multi-hundred-MB blocks cost milliseconds and synchronise the
+// device. Blocks are rounded to 2 MiB, kept per device in size-keyed free lists and
+// handed back on the next request of the same rounded size (cache capped at 16 GiB).
+namespace {
+struct AllocCache {
+    std::mutex mu;
+    std::multimap<size_t, void *> free_blocks;
+    std::unordered_map<void *, size_t> live;
+    size_t cached = 0;
+};
+AllocCache g_alloc[64];
+constexpr size_t kAllocGrain = size_t(2) << 20, kAllocCap = size_t(16) << 30;
+}  // namespace
+
+int b2_device_alloc(size_t bytes, int dev, void **out) {
+    if (!out) return fail(B2_ERR_INVALID, "alloc: NULL out");
+    *out = nullptr;
+    if (!bytes) return B2_OK;
+    if (int rc = check_dev(dev)) return rc;
+    const size_t sz = (bytes + kAllocGrain - 1) / kAllocGrain * kAllocGrain;
+    AllocCache &a = g_alloc[dev];
+    {
+        std::lock_guard<std::mutex> g(a.mu);
+        auto it = a.free_blocks.find(sz);
+        if (it != a.free_blocks.end()) {
+            *out = it->second;
+            a.free_blocks.erase(it);
+            a.cached -= sz;
+            a.live[*out] = sz;
+            return B2_OK;
+        }
+    }
+    cudaError_t e = cudaMalloc(out, sz);
+    if (e != cudaSuccess) {  // release the cache and retry once
+        std::lock_guard<std::mutex> g(a.mu);
+        for (auto &kv : a.free_blocks) cudaFree(kv.second);
+        a.free_blocks.clear();
+        a.cached = 0;
+        cudaGetLastError();
+        e = cudaMalloc(out, sz);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+    }
+    std::lock_guard<std::mutex> g(a.mu);
+    a.live[*out] = sz;
+    return B2_OK;
+}
+
+int b2_device_free(void *p, int dev) {
+    if (!p) return B2_OK;
+    if (dev < 0 || dev >= 64) return fail(B2_ERR_INVALID, "free: bad device");
+    AllocCache &a = g_alloc[dev];
+    std::lock_guard<std::mutex> g(a.mu);
+    auto it = a.live.find(p);
+    if (it == a.live.end()) return fail(B2_ERR_INVALID, "free: pointer not from b2_device_alloc");
+    const size_t sz = it->second;
+    a.live.erase(it);
+    if (a.cached + sz > kAllocCap) {
+        B2_CUDA(cudaFree(p));
+        return B2_OK;
+    }
+    a.free_blocks.emplace(sz, p);
+    a.cached += sz;
     return B2_OK;
 }
 

@@ -593,7 +593,7 @@ class _Gen:
         out.extend(pad + ln for ln in host_lines)
         g, t = self.fresh("bpg"), self.fresh("tpb")
         out.append(pad + f"{{ const int64_t {g} = {bpg}, {t} = {tpb};")
-        out.append(pad + f"  if ({g} < 0 || {g} > 2147483647LL || {t} < 0 || {t} > 1024) "
+        out.append(pad + f"  if ({g} < 0 || {g} > 2147483647LL || {t} < 0 || {t} > 1024 || {g} * {t} >= (1LL << 32)) "
                    f"b2_throw(\"kernel_launch(\" + std::to_string({g}) + \", \" + std::to_string({t}) + \") exceeds the B200 launch limits\");")
         out.append(pad + f"  if ({g} > 0 && {t} > 0) {{")
         out.append(pad + f"    if ({smem_bytes} > 48 * 1024) cudaFuncSetAttribute({name}, cudaFuncAttributeMaxDynamicSharedMemorySize, (int){smem_bytes});")
@@ -710,8 +710,8 @@ class _KernelCtx:
             pro.append(f"    {s.elem} {s.cname}[B2_TREG_MAX]; if (({n}) > B2_TREG_MAX) {{ b2_flag(b2_err, B2E_OOB, {n}, B2_TREG_MAX); return; }}")
         out = [f"__global__ void {self.name}({', '.join(params)}) {{",
                "    extern __shared__ __align__(16) unsigned char b2_smem[];",
-               "    const int64_t b2_w0 = (int64_t)gridDim.x * blockDim.x;",
-               "    const int64_t b2_rel0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;"]
+               "    const uint32_t b2_w0 = gridDim.x * blockDim.x;",
+               "    const uint32_t b2_rel0 = blockIdx.x * blockDim.x + threadIdx.x;"]
         if treg:
             out.insert(0, "#define B2_TREG_MAX 64")
         out.extend(pro)
@@ -767,12 +767,17 @@ class _KernelCtx:
             out.extend(pad + p for p in pre)
             if st.mode in ("thread", "magic_thread"):
                 n, w2, r2 = g.fresh("n"), g.fresh("w"), g.fresh("rel")
+                # widths / positions are uint32 (launch guard: grid < 2^32 threads);
+                # power-of-two widths (the usual tile shapes) split with shift / mask
+                sh = g.fresh("sh")
                 out.append(pad + f"{{ const int64_t {n} = ({s1}) - ({s0});")
                 out.append(pad + f"  if ({n} > 0) {{")
-                out.append(pad + f"  if ({w} % {n} != 0) {{ b2_flag(b2_err, B2E_WIDTH, {n}, {w}); return; }}")
-                out.append(pad + f"  const int64_t {w2} = {w} / {n};")
-                out.append(pad + f"  const int64_t {v} = ({s0}) + {rel} / {w2};")
-                out.append(pad + f"  const int64_t {r2} = {rel} % {w2};")
+                out.append(pad + f"  if ({n} > (int64_t){w} || {w} % (uint32_t){n} != 0) "
+                                 f"{{ b2_flag(b2_err, B2E_WIDTH, {n}, {w}); return; }}")
+                out.append(pad + f"  const uint32_t {w2} = {w} / (uint32_t){n};")
+                out.append(pad + f"  const int {sh} = ({w2} & ({w2} - 1u)) == 0u ? __ffs({w2}) - 1 : -1;")
+                out.append(pad + f"  const int64_t {v} = ({s0}) + (int64_t)({sh} >= 0 ? {rel} >> {sh} : {rel} / {w2});")
+                out.append(pad + f"  const uint32_t {r2} = {sh} >= 0 ? ({rel} & ({w2} - 1u)) : {rel} % {w2};")
                 self.emit_seq(st.body.stmts, out, ind + 1, w2, r2)
                 out.append(pad + "  } }")
                 return

@@ -373,11 +373,14 @@ class _Gen:
         if len(codes) != s.rank:
             raise UnsupportedProgram(f"rank mismatch on {s.name!r}: {len(codes)} indices into {s.rank}-d array")
         ok, off = [], "((int64_t)0)"
+        padded = s.kind == "smem_arr" and s.rank >= 2
         for k, cd in enumerate(codes):
             v = self.fresh("ix")
             lines.append(f"const int64_t {v} = {cd};")
             ok.append(f"b2_chk({v}, {dims}[{k}], b2_err)")
-            off = f"({off} * {dims}[{k}] + {v})"
+            # shared arrays: the last dimension is stored with a padded pitch
+            stride = f"{s.cname}_pitch" if (padded and k == s.rank - 1) else f"{dims}[{k}]"
+            off = f"({off} * {stride} + {v})"
         return "(" + " && ".join(ok or ["true"]) + ")", off, lines
 
     def access_read(self, base, idxs, dev):
@@ -581,8 +584,18 @@ class _Gen:
             dv = f"{s.cname}_hdims"
             host_lines.append(f"const int64_t {dv}[8] = {{{', '.join(dims) or '0'}}};")
             if kind == "smem_arr":
+                # The interpreter's shared arrays are plain row-major; on the device the
+                # last dimension of a rank >= 2 array gets one cell of padding when it is
+                # a multiple of 32 cells, so column accesses (the transpose's tile[x][y])
+                # hit 32 different banks (the +1 of transposeNoBankConflicts,
+                # PAPER.md:1104). Layout only: indices and bounds are unchanged.
+                r = len(dims)
+                last = f"{dv}[{r - 1}]" if r else "1"
+                pad = f"(({last}) % 32 == 0 ? 1 : 0)" if r >= 2 else "0"
+                host_lines.append(f"const int64_t {s.cname}_pitch = {last} + {pad};")
                 host_lines.append(f"const int64_t {s.cname}_soff = {smem_bytes};")
-                host_lines.append(f"{smem_bytes} += ((" + " * ".join(f"{dv}[{k}]" for k in range(len(dims)) or ["1"]) +
+                host_lines.append(f"{smem_bytes} += ((" + " * ".join([f"{dv}[{k}]" for k in range(r - 1)] +
+                                                                     [f"{s.cname}_pitch"]) +
                                   f") * (int64_t)sizeof({s.elem}) + 15) / 16 * 16;")
         # kernel body
         dl = []
@@ -678,6 +691,7 @@ class _KernelCtx:
                 args.append(f"{s.cname}_hdims[{k}]")
             if s.kind == "smem_arr":
                 args.append(f"{s.cname}_soff")
+                args.append(f"{s.cname}_pitch")
         for s in self.scalars.values():
             args.append(s.cname)
         args.append("b2_err_dev")
@@ -698,6 +712,7 @@ class _KernelCtx:
             pro.append(f"    const int64_t {s.cname}_dims[4] = {{{s.cname}_d0, {s.cname}_d1, {s.cname}_d2, {s.cname}_d3}};")
             if s.kind == "smem_arr":
                 params.append(f"int64_t {s.cname}_soff")
+                params.append(f"int64_t {s.cname}_pitch")
                 pro.append(f"    {s.elem} *{s.cname} = ({s.elem} *)(b2_smem + {s.cname}_soff);")
             else:
                 treg.append(s)

@@ -591,8 +591,8 @@ class _Gen:
                 # PAPER.md:1104). Layout only: indices and bounds are unchanged.
                 r = len(dims)
                 last = f"{dv}[{r - 1}]" if r else "1"
-                pad = f"(({last}) % 32 == 0 ? 1 : 0)" if r >= 2 else "0"
-                host_lines.append(f"const int64_t {s.cname}_pitch = {last} + {pad};")
+                extra = f"(({last}) % 32 == 0 ? 1 : 0)" if r >= 2 else "0"
+                host_lines.append(f"const int64_t {s.cname}_pitch = {last} + {extra};")
                 host_lines.append(f"const int64_t {s.cname}_soff = {smem_bytes};")
                 host_lines.append(f"{smem_bytes} += ((" + " * ".join([f"{dv}[{k}]" for k in range(r - 1)] +
                                                                      [f"{s.cname}_pitch"]) +

@@ -48,6 +48,15 @@ def _is_torch_cuda(x) -> bool:
     return torch is not None and isinstance(x, torch.Tensor) and x.is_cuda
 
 
+def _as_device(x):
+    """CUDA arrays from other libraries (`__cuda_array_interface__`, e.g. CuPy,
+    Numba) become zero-copy torch views; everything else passes through."""
+    if x is not None and torch is not None and not isinstance(x, torch.Tensor) \
+            and hasattr(x, "__cuda_array_interface__"):
+        return torch.as_tensor(x, device="cuda")
+    return x
+
+
 def b2_dtype(x) -> int:
     if torch is not None and isinstance(x, torch.Tensor):
         d = _torch_dtypes().get(x.dtype)
@@ -72,6 +81,7 @@ def transpose(inp, out=None, *, stream=None):
     Device tensors: returns `out` (allocated if None), asynchronous on the stream.
     Host numpy arrays: returns `out` after the host pipeline completes.
     """
+    inp, out = _as_device(inp), _as_device(out)
     if _is_torch_cuda(inp):
         if inp.dim() != 2 or (inp.numel() and inp.stride(1) != 1):
             raise ValueError("transpose: input must be 2-D with unit column stride")
@@ -116,6 +126,7 @@ def reduce_sum(arr, *, out=None, ws=None, stream=None):
     Device: returns a 1-element CUDA tensor (float32 / int64 / float64), async.
     Host: returns a Python float / int.
     """
+    arr, out = _as_device(arr), _as_device(out)
     d = b2_dtype(arr)
     if d not in _ACC:
         raise TypeError("reduce: dtype must be float32, int32 or float64")

@@ -176,6 +176,28 @@ def test_host_paths_staging(b2, pinned):
         _lib.tune("host.chunk_mb", 64)
 
 
+class _CAI:
+    """Minimal foreign CUDA array (as CuPy / Numba expose it)."""
+
+    def __init__(self, t):
+        self._t = t
+        self.__cuda_array_interface__ = {
+            "shape": tuple(t.shape), "typestr": {torch.float32: "<f4", torch.int32: "<i4"}[t.dtype],
+            "data": (t.data_ptr(), False), "version": 3,
+            "strides": tuple(s * t.element_size() for s in t.stride())}
+
+
+def test_cuda_array_interface_inputs(b2):
+    a = torch.randn(300, 200, device="cuda")
+    out = torch.empty(200, 300, device="cuda")
+    b2.transpose(_CAI(a), _CAI(out))
+    x = torch.randint(-2**31, 2**31, (10001,), device="cuda", dtype=torch.int64).to(torch.int32)
+    s = b2.reduce_sum(_CAI(x))
+    torch.cuda.synchronize()
+    assert torch.equal(out, a.t())
+    assert int(s.item()) == int(x.to(torch.int64).sum().item())
+
+
 def test_launch_counter(b2):
     n0 = b2.launch_count()
     b2.reduce_sum(torch.ones(100, device="cuda"))

@@ -109,6 +109,22 @@ B2_API size_t b2_reduce_ws_bytes(int64_t n, int dtype);
 B2_API int b2_reduce_sum(const void *in, int64_t n, int dtype, void *out, void *ws, size_t ws_bytes,
                   int dev, void *stream);
 
+/* Multi-GPU reduction with the cross-GPU combine fused into the kernel (SURVEY 8e
+ * "fused variant"; replaces a separate NCCL reduce of the 8-byte partial). Rank 0
+ * creates a mailbox in its memory and exports a 64-byte CUDA IPC handle; every
+ * other rank opens it (peer-mapped over NVLink). In b2_reduce_sum_fused the last
+ * CTA of rank g stores its partial into the mailbox and publishes it (system-scope
+ * release); rank 0's last CTA waits for all ranks (acquire, bounded: 20 s, then
+ * b2_mailbox_status reports 1) and writes the rank-ordered sum to its *out.
+ * epoch = 1, 2, 3, ... must advance identically on every rank. */
+B2_API int b2_mailbox_create(int dev, void **mailbox, void *ipc_handle64);
+B2_API int b2_mailbox_open(const void *ipc_handle64, int dev, void **mailbox);
+B2_API int b2_mailbox_close(void *mailbox, int dev, int owner);
+B2_API int b2_mailbox_status(void *mailbox, int dev, uint64_t *status);
+B2_API int b2_reduce_sum_fused(const void *in, int64_t n, int dtype, void *out, void *ws,
+                               size_t ws_bytes, void *mailbox, int rank, int nranks,
+                               uint64_t epoch, int dev, void *stream);
+
 /* Host-buffer form of b2_reduce_sum; *out_host receives float/int64/double. */
 B2_API int b2_reduce_sum_host(const void *in_host, int64_t n, int dtype, void *out_host, int dev);
 

@@ -33,6 +33,12 @@ SIGNATURES = {
     "b2_reduce_ws_bytes": (_sz, [_i64, _int]),
     "b2_reduce_sum": (_int, [_vp, _i64, _int, _vp, _vp, _sz, _int, _vp]),
     "b2_reduce_sum_host": (_int, [_vp, _i64, _int, _vp, _int]),
+    "b2_mailbox_create": (_int, [_int, ctypes.POINTER(_vp), _vp]),
+    "b2_mailbox_open": (_int, [_vp, _int, ctypes.POINTER(_vp)]),
+    "b2_mailbox_close": (_int, [_vp, _int, _int]),
+    "b2_mailbox_status": (_int, [_vp, _int, ctypes.POINTER(ctypes.c_uint64)]),
+    "b2_reduce_sum_fused": (_int, [_vp, _i64, _int, _vp, _vp, _sz, _vp, _int, _int, ctypes.c_uint64,
+                                   _int, _vp]),
     "b2_reduce_tree512_partials": (_int, [_vp, _i64, _vp, _int, _vp]),
     "b2_reduce_tree512": (_int, [_vp, _i64, _vp, _int, _vp]),
     "b2_reduce_tree512_host": (_int, [_vp, _i64, _vp, _int]),

@@ -72,8 +72,16 @@ int launch_transpose_any(const void *in, void *out, int64_t rows, int64_t cols, 
                          int64_t ld_out, int esize, int dev, cudaStream_t st);
 
 size_t reduce_ws_bytes(int64_t n, int dtype, int dev);
+// Cross-GPU combine fused into the reduction's last CTA (reduce.cu): mailbox is a
+// mailbox_bytes() region in rank 0's memory, mapped into every rank (CUDA IPC).
+struct FusedCombine {
+    void *mailbox = nullptr;  // nullptr: plain single-GPU reduction
+    int rank = 0, nranks = 1;
+    unsigned long long epoch = 0;  // 1, 2, 3, ... identical on every rank
+};
+size_t mailbox_bytes();
 int launch_reduce(const void *in, int64_t n, int dtype, void *out, void *ws, size_t ws_bytes,
-                  int dev, cudaStream_t st);
+                  int dev, cudaStream_t st, const FusedCombine &fz = FusedCombine());
 int launch_tree512(const float *in, int64_t n, float *partials, int dev, cudaStream_t st);
 
 }  // namespace b2

@@ -441,6 +441,64 @@ int b2_sync(int dev, void *stream) {
     return B2_OK;
 }
 
+// ------------------------------------------------------------ fused cross-GPU combine
+int b2_mailbox_create(int dev, void **mailbox, void *ipc_handle) {
+    if (!mailbox || !ipc_handle) return fail(B2_ERR_INVALID, "mailbox: NULL argument");
+    if (int rc = check_dev(dev)) return rc;
+    B2_CUDA(cudaMalloc(mailbox, mailbox_bytes()));
+    B2_CUDA(cudaMemset(*mailbox, 0, mailbox_bytes()));
+    B2_CUDA(cudaDeviceSynchronize());
+    cudaIpcMemHandle_t h;
+    B2_CUDA(cudaIpcGetMemHandle(&h, *mailbox));
+    memcpy(ipc_handle, &h, sizeof(h));
+    return B2_OK;
+}
+
+int b2_mailbox_open(const void *ipc_handle, int dev, void **mailbox) {
+    if (!mailbox || !ipc_handle) return fail(B2_ERR_INVALID, "mailbox: NULL argument");
+    if (int rc = check_dev(dev)) return rc;
+    cudaIpcMemHandle_t h;
+    memcpy(&h, ipc_handle, sizeof(h));
+    B2_CUDA(cudaIpcOpenMemHandle(mailbox, h, cudaIpcMemLazyEnablePeerAccess));
+    return B2_OK;
+}
+
+int b2_mailbox_close(void *mailbox, int dev, int owner) {
+    if (!mailbox) return B2_OK;
+    if (int rc = check_dev(dev)) return rc;
+    if (owner) B2_CUDA(cudaFree(mailbox));
+    else B2_CUDA(cudaIpcCloseMemHandle(mailbox));
+    return B2_OK;
+}
+
+int b2_mailbox_status(void *mailbox, int dev, uint64_t *status) {
+    if (!mailbox || !status) return fail(B2_ERR_INVALID, "mailbox: NULL argument");
+    if (int rc = check_dev(dev)) return rc;
+    // layout (reduce.cu): slots 4 x 64 x 8 | written 64 x 8 | consumed 8 | status 8
+    B2_CUDA(cudaMemcpy(status, (char *)mailbox + 4 * 64 * 8 + 64 * 8 + 8, 8, cudaMemcpyDeviceToHost));
+    return B2_OK;
+}
+
+int b2_reduce_sum_fused(const void *in, int64_t n, int dtype, void *out, void *ws, size_t ws_bytes,
+                        void *mailbox, int rank, int nranks, uint64_t epoch, int dev, void *stream) {
+    if (n < 0) return fail(B2_ERR_INVALID, "reduce: negative length");
+    if ((!in && n) || !out || !mailbox) return fail(B2_ERR_INVALID, "reduce: NULL buffer");
+    if (int rc = check_dev(dev)) return rc;
+    if (!ws) {
+        DevCtx &c = g_ctx[dev];
+        std::lock_guard<std::mutex> g(c.mu);
+        if (int rc = ctx_init(c, dev)) return rc;
+        ws = c.ws;
+        ws_bytes = c.ws_bytes;
+    }
+    FusedCombine fz;
+    fz.mailbox = mailbox;
+    fz.rank = rank;
+    fz.nranks = nranks;
+    fz.epoch = epoch;
+    return launch_reduce(in, n, dtype, out, ws, ws_bytes, dev, (cudaStream_t)stream, fz);
+}
+
 // ------------------------------------------------------------ caching device allocator
 // Generated programs gmem_malloc / gmem_free their arrays on every call; cudaMalloc
 // and cudaFree of multi-hundred-MB blocks cost milliseconds and synchronise the

@@ -79,11 +79,88 @@ __device__ __forceinline__ A block_tree(A a, A *sm) {
     return sm[0];
 }
 
+// ---- fused cross-GPU combine (mailbox in rank 0's memory, mapped into every rank)
+// Layout (bytes): slots[kEpochs][64] x 8 | written[64] u64 | consumed u64 | status u64.
+// Rank g's last CTA stores its partial into slots[e % kEpochs][g] over NVLink,
+// fences at system scope and publishes written[g] = e (release). Rank 0's last CTA
+// waits for written[g] >= e for every g (acquire), sums the slots in rank order
+// (deterministic for fp32) and publishes consumed = e. A writer may only reuse a
+// slot row after the root consumed the epoch that last used it (window kEpochs).
+// Every wait is bounded (kSpinNs): on timeout the status word is set and the
+// kernel exits instead of hanging the device.
+constexpr int kEpochs = 4;
+constexpr int kMaxRanks = 64;
+constexpr unsigned long long kSpinNs = 20ull * 1000 * 1000 * 1000;
+
+using Fused = FusedCombine;
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// wait until *p >= want; false on timeout (status word set)
+__device__ __forceinline__ bool wait_ge(const unsigned long long *p, unsigned long long want,
+                                        unsigned long long *status) {
+    const unsigned long long t0 = gtimer();
+    while (ld_acquire_sys(p) < want) {
+        if (gtimer() - t0 > kSpinNs) {
+            atomicExch(status, 1ull);
+            return false;
+        }
+        __nanosleep(200);
+    }
+    return true;
+}
+
+template <typename A>
+__device__ void fused_combine(const Fused &fz, A total, A *out) {
+    unsigned char *mb = static_cast<unsigned char *>(fz.mailbox);
+    A *slots = reinterpret_cast<A *>(mb);  // 8-byte slots: A is float, long long or double
+    unsigned long long *written = reinterpret_cast<unsigned long long *>(mb + kEpochs * kMaxRanks * 8);
+    unsigned long long *consumed = written + kMaxRanks;
+    unsigned long long *status = consumed + 1;
+    const int row = (int)(fz.epoch % kEpochs) * kMaxRanks * (8 / (int)sizeof(A));
+    const int stride = 8 / (int)sizeof(A);
+    if (fz.rank != 0 && fz.epoch > kEpochs - 1)  // slot row free again?
+        if (!wait_ge(consumed, fz.epoch - (kEpochs - 1), status)) {
+            *out = total;
+            return;
+        }
+    *reinterpret_cast<volatile A *>(slots + row + fz.rank * stride) = total;
+    __threadfence_system();
+    st_release_sys(written + fz.rank, fz.epoch);
+    if (fz.rank != 0) {
+        *out = total;
+        return;
+    }
+    A s = A(0);
+    for (int g = 0; g < fz.nranks; ++g) {
+        if (!wait_ge(written + g, fz.epoch, status)) {
+            *out = total;
+            return;
+        }
+        s += *reinterpret_cast<volatile A *>(slots + row + g * stride);
+    }
+    *out = s;
+    __threadfence_system();
+    st_release_sys(consumed, fz.epoch);
+}
+
 template <typename T, int NT, int U>
 __global__ void __launch_bounds__(NT)
     reduce_kernel(const T *__restrict__ in, int64_t head, int64_t nvec, int64_t n,
                   typename AccOf<T>::type *__restrict__ out,
-                  typename AccOf<T>::type *__restrict__ partials, unsigned *__restrict__ ticket) {
+                  typename AccOf<T>::type *__restrict__ partials, unsigned *__restrict__ ticket,
+                  Fused fz) {
     using A = typename AccOf<T>::type;
     constexpr int V = 16 / sizeof(T);
     __shared__ A sm[NT / 32];
@@ -125,8 +202,9 @@ __global__ void __launch_bounds__(NT)
     __syncthreads();  // sm reuse
     A total = block_tree<A, NT>(a, sm);
     if (threadIdx.x == 0) {
-        *out = total;
         *ticket = 0u;  // re-arm for the next call on this workspace
+        if (fz.mailbox) fused_combine<A>(fz, total, out);
+        else *out = total;
     }
 }
 
@@ -166,7 +244,7 @@ int max_grid(int dev) { return num_sms(dev) * (2048 / kMinNT); }
 
 template <typename T, int NT, int U>
 int run_reduce_v(const T *in, int64_t head, int64_t nvec, int64_t n, void *out, void *ws,
-                 int dev, cudaStream_t st) {
+                 int dev, cudaStream_t st, const Fused &fz) {
     using A = typename AccOf<T>::type;
     static int occ[64] = {0};
     if (occ[dev] == 0) {
@@ -183,7 +261,7 @@ int run_reduce_v(const T *in, int64_t head, int64_t nvec, int64_t n, void *out, 
     const int grid = (int)std::min(cap, need);
     unsigned *ticket = (unsigned *)ws;
     A *partials = (A *)((char *)ws + 64);
-    reduce_kernel<T, NT, U><<<grid, NT, 0, st>>>(in, head, nvec, n, (A *)out, partials, ticket);
+    reduce_kernel<T, NT, U><<<grid, NT, 0, st>>>(in, head, nvec, n, (A *)out, partials, ticket, fz);
     count_launch();
     B2_CUDA(cudaGetLastError());
     return B2_OK;
@@ -192,7 +270,7 @@ int run_reduce_v(const T *in, int64_t head, int64_t nvec, int64_t n, void *out, 
 // <threads, loads in flight per thread> variants; g_tune.r_variant picks one.
 template <typename T>
 int run_reduce(const void *in_, int64_t n, void *out, void *ws, size_t ws_bytes, int dev,
-               cudaStream_t st) {
+               cudaStream_t st, const Fused &fz) {
     using A = typename AccOf<T>::type;
     constexpr int V = 16 / sizeof(T);
     const T *in = (const T *)in_;
@@ -203,11 +281,11 @@ int run_reduce(const void *in_, int64_t n, void *out, void *ws, size_t ws_bytes,
     const size_t need = (size_t)max_grid(dev) * sizeof(A) + 64;
     if (ws_bytes < need) return fail(B2_ERR_INVALID, "reduce: workspace too small");
     switch (g_tune.r_variant) {
-    case 1: return run_reduce_v<T, 512, 8>(in, head, nvec, n, out, ws, dev, st);
-    case 2: return run_reduce_v<T, 256, 8>(in, head, nvec, n, out, ws, dev, st);
-    case 3: return run_reduce_v<T, 1024, 4>(in, head, nvec, n, out, ws, dev, st);
-    case 4: return run_reduce_v<T, 256, 16>(in, head, nvec, n, out, ws, dev, st);
-    default: return run_reduce_v<T, 512, 4>(in, head, nvec, n, out, ws, dev, st);
+    case 1: return run_reduce_v<T, 512, 8>(in, head, nvec, n, out, ws, dev, st, fz);
+    case 2: return run_reduce_v<T, 256, 8>(in, head, nvec, n, out, ws, dev, st, fz);
+    case 3: return run_reduce_v<T, 1024, 4>(in, head, nvec, n, out, ws, dev, st, fz);
+    case 4: return run_reduce_v<T, 256, 16>(in, head, nvec, n, out, ws, dev, st, fz);
+    default: return run_reduce_v<T, 512, 4>(in, head, nvec, n, out, ws, dev, st, fz);
     }
 }
 
@@ -218,12 +296,17 @@ size_t reduce_ws_bytes(int64_t, int dtype, int dev) {
     return (size_t)max_grid(dev) * a + 64;
 }
 
+size_t mailbox_bytes() { return 4096; }
+
 int launch_reduce(const void *in, int64_t n, int dtype, void *out, void *ws, size_t ws_bytes,
-                  int dev, cudaStream_t st) {
+                  int dev, cudaStream_t st, const FusedCombine &fz) {
+    if (fz.mailbox && (fz.nranks < 1 || fz.nranks > kMaxRanks || fz.rank < 0 || fz.rank >= fz.nranks ||
+                       fz.epoch == 0))
+        return fail(B2_ERR_INVALID, "fused combine: bad rank / nranks / epoch");
     switch (dtype) {
-    case B2_F32: return run_reduce<float>(in, n, out, ws, ws_bytes, dev, st);
-    case B2_I32: return run_reduce<int32_t>(in, n, out, ws, ws_bytes, dev, st);
-    case B2_F64: return run_reduce<double>(in, n, out, ws, ws_bytes, dev, st);
+    case B2_F32: return run_reduce<float>(in, n, out, ws, ws_bytes, dev, st, fz);
+    case B2_I32: return run_reduce<int32_t>(in, n, out, ws, ws_bytes, dev, st, fz);
+    case B2_F64: return run_reduce<double>(in, n, out, ws, ws_bytes, dev, st, fz);
     default: return fail(B2_ERR_UNSUPPORTED, "reduce: dtype must be B2_F32, B2_I32 or B2_F64");
     }
 }

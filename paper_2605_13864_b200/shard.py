@@ -93,6 +93,61 @@ def sharded_reduce_sum(local_x, *, group=None, root: int | None = None, reduce_f
     return float(acc)
 
 
+class FusedReduce:
+    """Sharded sum with the cross-GPU combine fused into the reduction kernel
+    (include/b2k.h b2_reduce_sum_fused): no separate NCCL launch per step.
+
+    Rank 0 owns a small mailbox in its HBM; its CUDA IPC handle is broadcast once
+    over the process group (any backend) and opened by every other rank (a peer
+    mapping over NVLink). Each call advances a shared epoch. The result on rank 0
+    is the global sum (rank-ordered, deterministic for fp32); other ranks get
+    their local partial.
+    """
+
+    def __init__(self, group=None, device=None):
+        import ctypes
+
+        from ._lib import check, lib
+        self._lib, self._check, self._ct = lib(), check, ctypes
+        self.group = group
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.dev = torch.cuda.current_device() if device is None else int(device)
+        self.mailbox = ctypes.c_void_p()
+        handle = ctypes.create_string_buffer(64)
+        if self.rank == 0:
+            check(self._lib.b2_mailbox_create(self.dev, ctypes.byref(self.mailbox), handle))
+        obj = [handle.raw if self.rank == 0 else None]
+        if self.world > 1:
+            dist.broadcast_object_list(obj, src=0, group=group)
+        if self.rank != 0:
+            check(self._lib.b2_mailbox_open(obj[0], self.dev, ctypes.byref(self.mailbox)))
+        self.epoch = 0
+
+    def __call__(self, x, out=None, stream=None):
+        from . import ops
+        d = ops.b2_dtype(x)
+        npacc, tacc = ops._ACC[d]
+        if out is None:
+            out = torch.empty(1, dtype=getattr(torch, tacc), device=x.device)
+        self.epoch += 1
+        self._check(self._lib.b2_reduce_sum_fused(
+            x.data_ptr(), x.numel(), d, out.data_ptr(), None, 0, self.mailbox, self.rank, self.world,
+            self.epoch, self.dev, ops._stream_ptr(x, stream)))
+        return out
+
+    def status(self) -> int:
+        """0 = healthy; 1 = a bounded wait timed out (a rank never published)."""
+        s = self._ct.c_uint64(0)
+        self._check(self._lib.b2_mailbox_status(self.mailbox, self.dev, self._ct.byref(s)))
+        return int(s.value)
+
+    def close(self):
+        if self.mailbox:
+            self._lib.b2_mailbox_close(self.mailbox, self.dev, 1 if self.rank == 0 else 0)
+            self.mailbox = self._ct.c_void_p()
+
+
 def gather_transpose(local_out, rows: list, *, root: int = 0, group=None):
     """Assemble the full W x H output on `root` from the ranks' W x H_g slabs."""
     rank = dist.get_rank(group)

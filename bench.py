@@ -47,6 +47,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-graph", action="store_true", help="eager launches instead of a CUDA graph")
+    p.add_argument("--combine", default="fused", choices=["fused", "nccl"],
+                   help="N > 1: cross-GPU combine of the reduction partials")
     p.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                    help="gloo only to exercise the multi-rank path with several ranks on one GPU")
     p.add_argument("--paper-configs", action="store_true", default=True)
@@ -250,28 +252,52 @@ def main():
 
     st = torch.cuda.current_stream(dev)
 
+    # N > 1 combine of the per-GPU partials: fused into the reduction kernel (the
+    # partial goes straight into rank 0's mailbox over NVLink) or one NCCL reduce
+    combine = args.combine if world > 1 else "none"
+    fused = None
+    combine_note = None
+    if combine == "fused":
+        try:
+            from paper_2605_13864_b200 import shard
+            fused = shard.FusedReduce()
+        except Exception as e:  # e.g. no CUDA IPC / peer access between these GPUs
+            combine, combine_note = "nccl", f"fused combine unavailable ({e}); NCCL reduce used"
+
     def step(ev=None):
         if ev is not None:
             ev[0].record(st)
         b2.transpose(a, out)
         if ev is not None:
             ev[1].record(st)
-        b2.reduce_sum(x, out=partial)
+        if fused is not None:
+            fused(x, out=partial)
+        else:
+            b2.reduce_sum(x, out=partial)
         if ev is not None:
             ev[2].record(st)
-        if world > 1:
+        if world > 1 and fused is None:
             if args.dist_backend == "nccl":
                 dist.reduce(partial, dst=0)  # one NCCL reduce of the 8-byte partial
             else:
                 dist.all_reduce(partial)  # gloo has no CUDA reduce
 
     # correctness spot checks (cheap, outside the timed region)
-    step()
-    torch.cuda.synchronize()
-    assert torch.equal(out[:64, :64], a[:64, :64].t()) and torch.equal(out[-64:, -64:], a[-64:, -64:].t())
     want = x.to(torch.int64).sum().reshape(1)
     if world > 1:
         dist.all_reduce(want)
+    step()
+    torch.cuda.synchronize()
+    assert torch.equal(out[:64, :64], a[:64, :64].t()) and torch.equal(out[-64:, -64:], a[-64:, -64:].t())
+    if fused is not None:
+        bad = torch.tensor([0 if (rank != 0 or (int(partial.item()) == int(want.item())
+                                                and fused.status() == 0)) else 1], device=dev)
+        dist.all_reduce(bad)
+        if int(bad.item()):
+            fused, combine = None, "nccl"
+            combine_note = "fused combine failed its check; NCCL reduce used"
+            step()
+            torch.cuda.synchronize()
     if rank == 0:
         assert int(partial.item()) == int(want.item()), "reduction combine mismatch"
 
@@ -366,8 +392,11 @@ def main():
                    "l2": (f"inputs ({bytes_t // 2 / 2**30:.2f} GiB + {n * 4 / 2**30:.2f} GiB) larger "
                           "than L2 (126 MB): no flush needed" if min(bytes_t // 2, n * 4) > 2 * L2_BYTES
                           else "WARNING: inputs not larger than 2x L2"),
-                   "combine": (f"{args.dist_backend} {'reduce' if args.dist_backend == 'nccl' else 'all_reduce'}"
-                               " of the int64 partial" if world > 1 else "none (1 GPU)")},
+                   "combine": ("fused into the reduction kernel (partial -> rank 0 mailbox over "
+                               "NVLink, release/acquire epochs)" if combine == "fused" else
+                               f"{args.dist_backend} {'reduce' if args.dist_backend == 'nccl' else 'all_reduce'}"
+                               " of the int64 partial" if world > 1 else "none (1 GPU)"),
+                   "combine_note": combine_note},
         "roofline": {"bound": "hbm",
                      "kernel": ("transpose_vec_kernel<4,64,32,512> (256x128 fp32 tile, 1 CTA/SM)"
                                 if (rows // 256) * (cols // 128) >= 8 * 148 else

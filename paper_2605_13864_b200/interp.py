@@ -141,16 +141,25 @@ def _to_f32(v: np.ndarray) -> np.ndarray:
 
 
 def _ints(part) -> np.ndarray:
+    """Exact integer cells: int32 when every value fits, else int64, else uint64
+    (64-bit bit patterns such as fp64 bits). Values the reference would keep as
+    non-integers (floats in an int cell) or beyond 64 bits are refused rather than
+    silently converted."""
+    if not all(isinstance(x, (int, np.integer)) for x in part):
+        raise InterpError("int cell holds a non-integer value (not representable on the device)")
     try:
         v = np.array(part, dtype=np.int64)
         return v.astype(np.int32) if v.size == 0 or (
             v.min() >= -2**31 and v.max() < 2**31) else v
     except OverflowError:
-        v = np.array(part, dtype=np.uint64)  # 64-bit patterns (fp64 bits) up to 2^64-1
-        return v
+        pass
+    try:
+        return np.array(part, dtype=np.uint64)
+    except OverflowError:
+        raise InterpError("int cell value outside the 64-bit range") from None
 
 
-def _store(arr, flat_positions_rows, values2d: np.ndarray, row_pitch: int):
+def _store(arr, values2d: np.ndarray, row_pitch: int):
     """Write a (rows x cols) block into arr.data, row r at offset r*row_pitch."""
     data = arr.data
     rows, cols = values2d.shape
@@ -210,6 +219,9 @@ class Interp:
             if ptype.endswith("*"):
                 if _is_array(v):
                     arr = v
+                    if isinstance(v.data, np.ndarray) and not v.data.flags.c_contiguous:
+                        raise InterpError(f"{pname!r}: numpy-backed Array data must be C-contiguous "
+                                          "(results are written in place)")
                 elif isinstance(v, np.ndarray):
                     flat = np.ascontiguousarray(v).reshape(-1)
                     if ptype.startswith("float") and flat.dtype != np.float32:
@@ -285,7 +297,7 @@ def _exec_transpose_naive(plan: Plan, env):
         ops.transpose(a, out2d)
     else:
         out = ops.transpose(a)
-        _store(dst, None, out, Co)
+        _store(dst, out, Co)
     return None
 
 
@@ -321,7 +333,7 @@ def _exec_transpose_gpu(plan: Plan, env):
     if (len(dst.data) if not isinstance(dst.data, np.ndarray) else dst.data.size) < n:
         raise IndexError("list assignment index out of range")
     out = ops.transpose(np.ascontiguousarray(a).reshape(H, W))
-    _store(dst, None, out.reshape(1, n), n)
+    _store(dst, out.reshape(1, n), n)
     return None
 
 

@@ -146,11 +146,16 @@ B2_API int b2_reduce_tree512_host(const float *in_host, int64_t n, float *result
 /* Synchronous bulk copies for generated host code (codegen.py), replacing the
  * interpreter's element-wise memcpy_host_to_device / memcpy_device_to_host
  * (interp.py:353-365): pinned host buffers go straight to the DMA engines,
- * pageable ones are staged through the pinned ring by the host copy pool. */
+ * pageable ones are staged through the pinned ring by the host copy pool.
+ * Like cudaMemcpy they are ordered after the work already queued on the device's
+ * legacy default stream (stream NULL), and return when the copy is complete. */
 B2_API int b2_copy_h2d(void *dst_dev, const void *src_host, size_t bytes, int dev);
 B2_API int b2_copy_d2h(void *dst_host, const void *src_dev, size_t bytes, int dev);
 /* Caching device allocator for generated code's gmem_malloc / gmem_free
- * (intrinsics.py:107-161 gmem contracts): 2 MiB-rounded blocks reused across calls. */
+ * (intrinsics.py:107-161 gmem contracts): 2 MiB-rounded blocks reused across calls.
+ * b2_device_free first waits for the legacy default stream (like cudaFree), so a
+ * block is never handed out again while queued work still uses it; work the
+ * caller queued on its own non-blocking streams must be synchronised first. */
 B2_API int b2_device_alloc(size_t bytes, int dev, void **out);
 B2_API int b2_device_free(void *ptr, int dev);
 

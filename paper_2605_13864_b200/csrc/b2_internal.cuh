@@ -31,7 +31,7 @@ int num_sms(int dev);
 struct Tuning {
     int t_variant = 0;      // transpose tile shape (see run_vec_for)
     int t_group = 0;        // tile-rows per band in the tile walk order (0 = auto)
-    int t_big = 1;          // 1 = 128-KB tiles (1 CTA/SM) for large fp32/fp64 matrices
+    int t_big = 1;          // 1 = 128-KB tiles (1 CTA/SM) for large fp32/fp64 matrices, 2 = always
     int t_ctas_per_sm = 0;  // 0 = auto (~kInflightBytesPerSM of tiles per SM)
     int r_variant = 0;      // reduce <threads, unroll> instantiation
     int r_ctas_per_sm = 0;  // 0 = auto (kReduceThreadsPerSM threads per SM)

@@ -54,6 +54,7 @@ struct DevCtx {
     bool ready = false;
     cudaStream_t s_h2d = nullptr, s_comp = nullptr, s_d2h = nullptr;
     cudaEvent_t ev_in[kStages], ev_comp[kStages], ev_out[kStages];
+    cudaEvent_t ev_legacy = nullptr;  // orders bulk copies after the legacy default stream
     void *d_in[kStages] = {nullptr, nullptr, nullptr};
     void *d_out[kStages] = {nullptr, nullptr, nullptr};
     size_t stage_bytes = 0;
@@ -95,6 +96,7 @@ int ctx_init(DevCtx &c, int dev) {
         B2_CUDA(cudaEventCreateWithFlags(&c.ev_comp[k], cudaEventDisableTiming));
         B2_CUDA(cudaEventCreateWithFlags(&c.ev_out[k], cudaEventDisableTiming));
     }
+    B2_CUDA(cudaEventCreateWithFlags(&c.ev_legacy, cudaEventDisableTiming));
     c.ws_bytes = reduce_ws_bytes(0, B2_F64, dev);
     B2_CUDA(cudaMalloc(&c.ws, c.ws_bytes));
     B2_CUDA(cudaMemset(c.ws, 0, c.ws_bytes));
@@ -557,6 +559,9 @@ int b2_device_free(void *p, int dev) {
     if (it == a.live.end()) return fail(B2_ERR_INVALID, "free: pointer not from b2_device_alloc");
     const size_t sz = it->second;
     a.live.erase(it);
+    // like cudaFree: work already queued on the legacy stream may still use the block
+    if (int rc = check_dev(dev)) return rc;
+    B2_CUDA(cudaStreamSynchronize(cudaStreamLegacy));
     if (a.cached + sz > kAllocCap) {
         B2_CUDA(cudaFree(p));
         return B2_OK;
@@ -574,6 +579,10 @@ int b2_copy_h2d(void *dst_dev, const void *src_host, size_t bytes, int dev) {
     DevCtx &c = g_ctx[dev];
     std::lock_guard<std::mutex> g(c.mu);
     if (int rc = ctx_init(c, dev)) return rc;
+    // like cudaMemcpy: ordered after the work already queued on the legacy default
+    // stream (our copy streams are non-blocking, so this is explicit)
+    B2_CUDA(cudaEventRecord(c.ev_legacy, cudaStreamLegacy));
+    B2_CUDA(cudaStreamWaitEvent(c.s_h2d, c.ev_legacy, 0));
     const bool staged = !is_pinned(src_host);
     const size_t cb = chunk_bytes();
     if (staged && ensure_host_stages(c, std::min(bytes, cb))) return B2_ERR_NOMEM;
@@ -596,6 +605,8 @@ int b2_copy_d2h(void *dst_host, const void *src_dev, size_t bytes, int dev) {
     DevCtx &c = g_ctx[dev];
     std::lock_guard<std::mutex> g(c.mu);
     if (int rc = ctx_init(c, dev)) return rc;
+    B2_CUDA(cudaEventRecord(c.ev_legacy, cudaStreamLegacy));  // see b2_copy_h2d
+    B2_CUDA(cudaStreamWaitEvent(c.s_d2h, c.ev_legacy, 0));
     if (is_pinned(dst_host)) {
         B2_CUDA(cudaMemcpyAsync(dst_host, src_dev, bytes, cudaMemcpyDeviceToHost, c.s_d2h));
         B2_CUDA(cudaStreamSynchronize(c.s_d2h));

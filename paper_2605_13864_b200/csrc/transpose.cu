@@ -306,13 +306,14 @@ int run_vec_for(const void *in, void *out, int64_t rv, int64_t cv, int64_t ld_in
     // Large matrices: one 128-KB tile per SM (256 x 512 B) — half as many concurrent
     // DRAM row streams, each twice as long, measured +2.5 % for fp32 / fp64
     // (profiles/r01_tune_big.md). Needs enough tiles to keep every SM busy.
-    const int64_t big_min_tiles = 8 * (int64_t)num_sms(dev);
+    // t_big == 2 forces them whatever the size (sanitizer / test coverage).
+    const int64_t big_min_tiles = g_tune.t_big == 2 ? 1 : 8 * (int64_t)num_sms(dev);
     if (v == 0 && g_tune.t_big) {
         if constexpr (E == 4) {
-            if ((rv / 256) * (cv / 128) >= big_min_tiles)
+            if (rv >= 256 && cv >= 128 && (rv / 256) * (cv / 128) >= big_min_tiles)
                 return run_vec<4, 64, 32, 512>(in, out, rv, cv, ld_in, ld_out, dev, st);
         } else if constexpr (E == 8) {
-            if ((rv / 256) * (cv / 64) >= big_min_tiles)
+            if (rv >= 256 && cv >= 64 && (rv / 256) * (cv / 64) >= big_min_tiles)
                 return run_vec<8, 128, 32, 512>(in, out, rv, cv, ld_in, ld_out, dev, st);
         }
     }

@@ -159,6 +159,36 @@ B2_API int b2_copy_d2h(void *dst_host, const void *src_dev, size_t bytes, int de
 B2_API int b2_device_alloc(size_t bytes, int dev, void **out);
 B2_API int b2_device_free(void *ptr, int dev);
 
+/* ---- single-process multi-GPU ------------------------------
+ * One host thread drives every GPU of the box. Shard g runs on the device that
+ * owns its pointer, so the same call covers 1..8 GPUs (or several shards on one
+ * GPU). Both calls order after each device's legacy default stream and return
+ * when the work is complete.
+ * b2_init: create the per-device contexts of devices 0..ndev-1 (ndev <= 0: all)
+ *   and enable peer access between every pair that supports it. Optional: the
+ *   multi calls initialise what they touch lazily.
+ * b2_peer_access: 1 if kernels on `from` can load/store memory of `to`
+ *   (enabling it if possible), else 0. */
+B2_API int b2_init(int ndev);
+B2_API int b2_peer_access(int from, int to);
+/* Row-block sharded transpose: shard g is the rows[g] x cols block in[g] (pitch
+ * ld_in[g]); its transpose goes to out[g] (cols x rows[g], pitch ld_out[g]), which
+ * may live on another GPU (e.g. a column slab of one full W x H matrix: the
+ * kernel's stores then cross NVLink). No exchange step.
+ * Replaces the A.1 / A.4 nest over a partition of the y loop (interp.py:282-300). */
+B2_API int b2_transpose_multi(const void *const *in, void *const *out, const int64_t *rows,
+                              int64_t cols, const int64_t *ld_in, const int64_t *ld_out, int dtype,
+                              int nshards);
+/* Sharded sum: shard g (n[g] elements, device pointer) is reduced on its device;
+ * the partials are combined in shard order inside the kernels over NVLink (each
+ * shard's last CTA stores into the root's mailbox, root = shard 0's device; the
+ * root's last CTA sums them) — or, without peer access, on the host in the same
+ * order (identical bits). *host_out receives float / int64 / double as in
+ * b2_reduce_sum. Replaces: `for i < N { sum += arr[i]; }` (A.2 / A.3) over
+ * contiguous shards + one combine step. */
+B2_API int b2_reduce_sum_multi(const void *const *shards, const int64_t *n, int nshards, int dtype,
+                               void *host_out);
+
 /* Block until all work this library queued on `stream` of `dev` is done. */
 B2_API int b2_sync(int dev, void *stream);
 

@@ -8,15 +8,19 @@ Public surface:
   * `parse_program`, `ParseError`                           — the program
     grammar (minigpu/parser.py:893) for building those Programs;
   * `transpose`, `reduce_sum`, `reduce_tree512`              — typed zero-copy
-    entries on CUDA tensors or host arrays.
+    entries on CUDA tensors or host arrays;
+  * `transpose_multi`, `reduce_sum_multi`                    — the same over
+    shards on several GPUs from one process (fused NVLink combine).
 """
 from ._lib import B2Error, launch_count  # noqa: F401
 from .interp import Array, Interp, InterpError, UnsupportedProgram, f32, run_program  # noqa: F401
 from .lang import ParseError, Program, parse_program  # noqa: F401
-from .ops import reduce_sum, reduce_tree512, reduce_tree512_partials, transpose  # noqa: F401
+from .ops import (init_devices, reduce_sum, reduce_sum_multi, reduce_tree512,  # noqa: F401
+                  reduce_tree512_partials, transpose, transpose_multi)
 from .recognize import recognize  # noqa: F401
 from . import programs  # noqa: F401
 
 __all__ = ["run_program", "Interp", "Array", "InterpError", "UnsupportedProgram", "f32",
            "parse_program", "ParseError", "Program", "recognize", "transpose", "reduce_sum",
-           "reduce_tree512", "reduce_tree512_partials", "B2Error", "launch_count"]
+           "reduce_tree512", "reduce_tree512_partials", "transpose_multi", "reduce_sum_multi",
+           "init_devices", "B2Error", "launch_count"]

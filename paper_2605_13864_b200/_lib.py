@@ -43,6 +43,11 @@ SIGNATURES = {
     "b2_reduce_tree512": (_int, [_vp, _i64, _vp, _int, _vp]),
     "b2_reduce_tree512_host": (_int, [_vp, _i64, _vp, _int]),
     "b2_sync": (_int, [_int, _vp]),
+    "b2_init": (_int, [_int]),
+    "b2_peer_access": (_int, [_int, _int]),
+    "b2_transpose_multi": (_int, [ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_i64), _i64,
+                                  ctypes.POINTER(_i64), ctypes.POINTER(_i64), _int, _int]),
+    "b2_reduce_sum_multi": (_int, [ctypes.POINTER(_vp), ctypes.POINTER(_i64), _int, _int, _vp]),
     "b2_copy_h2d": (_int, [_vp, _vp, _sz, _int]),
     "b2_copy_d2h": (_int, [_vp, _vp, _sz, _int]),
     "b2_device_alloc": (_int, [_sz, _int, ctypes.POINTER(_vp)]),

@@ -66,6 +66,12 @@ struct DevCtx {
     void *hs_in[kStages] = {nullptr, nullptr, nullptr};   // pinned staging (pageable sources)
     void *hs_out[kStages] = {nullptr, nullptr, nullptr};  // pinned staging (pageable destinations)
     size_t hs_bytes = 0;
+    // single-process multi-GPU entries (b2_*_multi): per-shard result slots, and the
+    // fused-combine mailbox when this device is the root
+    void *d_slots = nullptr;  // kMaxShards x 8 B
+    void *h_slots = nullptr;  // pinned mirror
+    void *mailbox = nullptr;
+    unsigned long long mb_epoch = 0;
 };
 
 DevCtx g_ctx[64];
@@ -742,6 +748,237 @@ int b2_reduce_sum_host(const void *in_host, int64_t n, int dtype, void *out_host
         double s = 0.0;
         for (int64_t i = 0; i < nchunks; ++i) s += *(const double *)(h + i * 8);
         *(double *)out_host = s;
+    }
+    return B2_OK;
+}
+
+
+// ------------------------------------------------ single-process multi-GPU entries
+// One host thread drives every GPU of the box. Shard g lives on the
+// device that owns its pointer (cudaPointerGetAttributes), so the same call runs on
+// 1..8 GPUs, or with several shards on one GPU. Transpose: no exchange, each device
+// transposes its row block into its column slab (possibly a peer pointer into one
+// full matrix: the stores then cross NVLink inside the kernel). Reduction: every
+// shard's single-pass kernel combines into the root's mailbox over NVLink (fused
+// P2P combine, root = shard 0's device), rank-ordered and deterministic; without
+// peer access the per-shard partials go to the host and are summed in the same
+// order (identical bits).
+static bool g_peer[64][64];
+static std::mutex g_multi_mu;
+constexpr int kMaxShards = 64;
+
+static int ptr_device(const void *p, int *dev) {
+    cudaPointerAttributes a;
+    cudaError_t e = cudaPointerGetAttributes(&a, p);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return cuda_fail(e, "cudaPointerGetAttributes");
+    }
+    if (a.type != cudaMemoryTypeDevice && a.type != cudaMemoryTypeManaged)
+        return fail(B2_ERR_INVALID, "multi: shard pointers must be device memory");
+    *dev = a.device;
+    return B2_OK;
+}
+
+static int enable_peer(int from, int to) {
+    if (from == to) return 1;
+    if (g_peer[from][to]) return 1;
+    int can = 0;
+    if (cudaDeviceCanAccessPeer(&can, from, to) != cudaSuccess || !can) {
+        cudaGetLastError();
+        return 0;
+    }
+    if (check_dev(from)) return 0;
+    cudaError_t e = cudaDeviceEnablePeerAccess(to, 0);
+    if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) {
+        cudaGetLastError();
+        return 0;
+    }
+    cudaGetLastError();
+    g_peer[from][to] = true;
+    return 1;
+}
+
+static int multi_ctx(int dev) {
+    if (int rc = check_dev(dev)) return rc;
+    DevCtx &c = g_ctx[dev];
+    if (int rc = ctx_init(c, dev)) return rc;
+    if (!c.d_slots) {
+        B2_CUDA(cudaMalloc(&c.d_slots, kMaxShards * 8));
+        B2_CUDA(cudaMallocHost(&c.h_slots, kMaxShards * 8));
+    }
+    return B2_OK;
+}
+
+// lock the contexts of every device involved, in device order (no lock-order cycles)
+struct MultiLock {
+    std::vector<std::unique_lock<std::mutex>> locks;
+    explicit MultiLock(const std::vector<int> &devs) {
+        std::vector<int> d(devs);
+        std::sort(d.begin(), d.end());
+        d.erase(std::unique(d.begin(), d.end()), d.end());
+        for (int x : d) locks.emplace_back(g_ctx[x].mu);
+    }
+};
+
+int b2_init(int ndev) {
+    int have = 0;
+    if (int rc = b2_device_count(&have)) return rc;
+    if (ndev <= 0 || ndev > have) ndev = have;
+    std::lock_guard<std::mutex> g(g_multi_mu);
+    for (int d = 0; d < ndev; ++d) {
+        std::lock_guard<std::mutex> l(g_ctx[d].mu);
+        if (int rc = multi_ctx(d)) return rc;
+    }
+    for (int a = 0; a < ndev; ++a)
+        for (int b = 0; b < ndev; ++b) enable_peer(a, b);
+    return B2_OK;
+}
+
+int b2_peer_access(int from, int to) {
+    if (from < 0 || to < 0 || from >= 64 || to >= 64) return 0;
+    std::lock_guard<std::mutex> g(g_multi_mu);
+    return enable_peer(from, to);
+}
+
+int b2_transpose_multi(const void *const *in, void *const *out, const int64_t *rows, int64_t cols,
+                       const int64_t *ld_in, const int64_t *ld_out, int dtype, int nshards) {
+    const int E = esize_of(dtype);
+    if (!E) return fail(B2_ERR_UNSUPPORTED, "transpose: unknown dtype " + std::to_string(dtype));
+    if (nshards <= 0 || nshards > kMaxShards || !in || !out || !rows || !ld_in || !ld_out)
+        return fail(B2_ERR_INVALID, "transpose_multi: bad shard arrays");
+    if (cols < 0) return fail(B2_ERR_INVALID, "transpose: negative extent");
+    std::vector<int> devs(nshards, 0);
+    for (int g = 0; g < nshards; ++g) {
+        if (rows[g] < 0) return fail(B2_ERR_INVALID, "transpose: negative extent");
+        if (rows[g] == 0 || cols == 0) continue;
+        if (!in[g] || !out[g]) return fail(B2_ERR_INVALID, "transpose: NULL buffer");
+        if (ld_in[g] < cols || ld_out[g] < rows[g])
+            return fail(B2_ERR_INVALID, "transpose: pitch smaller than row length");
+        if (int rc = ptr_device(in[g], &devs[g])) return rc;
+    }
+    std::lock_guard<std::mutex> gm(g_multi_mu);
+    MultiLock lk(devs);
+    for (int g = 0; g < nshards; ++g) {
+        if (rows[g] == 0 || cols == 0) continue;
+        if (int rc = multi_ctx(devs[g])) return rc;
+        int od = devs[g];
+        if (int rc = ptr_device(out[g], &od)) return rc;
+        if (od != devs[g] && !enable_peer(devs[g], od))
+            return fail(B2_ERR_UNSUPPORTED, "transpose_multi: no peer access from device " +
+                                                std::to_string(devs[g]) + " to " + std::to_string(od));
+    }
+    // every device's stream first waits for the legacy stream (inputs produced there)
+    for (int g = 0; g < nshards; ++g) {
+        if (rows[g] == 0 || cols == 0) continue;
+        DevCtx &c = g_ctx[devs[g]];
+        if (int rc = check_dev(devs[g])) return rc;
+        B2_CUDA(cudaEventRecord(c.ev_legacy, cudaStreamLegacy));
+        B2_CUDA(cudaStreamWaitEvent(c.s_comp, c.ev_legacy, 0));
+        if (int rc = launch_transpose(in[g], out[g], rows[g], cols, ld_in[g], ld_out[g], E, devs[g], c.s_comp))
+            return rc;
+    }
+    for (int g = 0; g < nshards; ++g) {
+        if (rows[g] == 0 || cols == 0) continue;
+        if (int rc = check_dev(devs[g])) return rc;
+        B2_CUDA(cudaStreamSynchronize(g_ctx[devs[g]].s_comp));
+    }
+    return B2_OK;
+}
+
+int b2_reduce_sum_multi(const void *const *shards, const int64_t *n, int nshards, int dtype,
+                        void *host_out) {
+    if (dtype != B2_F32 && dtype != B2_I32 && dtype != B2_F64)
+        return fail(B2_ERR_UNSUPPORTED, "reduce: dtype must be B2_F32, B2_I32 or B2_F64");
+    if (nshards <= 0 || nshards > kMaxShards || !shards || !n || !host_out)
+        return fail(B2_ERR_INVALID, "reduce_multi: bad shard arrays");
+    std::vector<int> devs(nshards, -1);
+    int root = -1;
+    for (int g = 0; g < nshards; ++g) {
+        if (n[g] < 0) return fail(B2_ERR_INVALID, "reduce: negative length");
+        if (n[g] > 0) {
+            if (!shards[g]) return fail(B2_ERR_INVALID, "reduce: NULL buffer");
+            if (int rc = ptr_device(shards[g], &devs[g])) return rc;
+        }
+    }
+    // empty shards run on the root's device (their partial is 0)
+    for (int g = 0; g < nshards && root < 0; ++g) root = devs[g];
+    if (root < 0) {
+        if (int rc = check_dev(0)) return rc;
+        root = 0;
+    }
+    for (int g = 0; g < nshards; ++g)
+        if (devs[g] < 0) devs[g] = root;
+    std::lock_guard<std::mutex> gm(g_multi_mu);
+    MultiLock lk(devs);
+    bool fused = true;
+    for (int g = 0; g < nshards; ++g) {
+        if (int rc = multi_ctx(devs[g])) return rc;
+        fused = fused && enable_peer(devs[g], root);
+    }
+    DevCtx &rc_ = g_ctx[root];
+    if (fused && !rc_.mailbox) {
+        if (int rc = check_dev(root)) return rc;
+        B2_CUDA(cudaMalloc(&rc_.mailbox, mailbox_bytes()));
+        B2_CUDA(cudaMemset(rc_.mailbox, 0, mailbox_bytes()));
+        B2_CUDA(cudaDeviceSynchronize());
+    }
+    const unsigned long long epoch = fused ? ++rc_.mb_epoch : 0;
+    // non-root shards first: shards sharing the root's device then precede the
+    // root's kernel on the same stream, so its wait can never block them
+    auto launch = [&](int g) -> int {
+        DevCtx &c = g_ctx[devs[g]];
+        if (int rc = check_dev(devs[g])) return rc;
+        B2_CUDA(cudaEventRecord(c.ev_legacy, cudaStreamLegacy));
+        B2_CUDA(cudaStreamWaitEvent(c.s_comp, c.ev_legacy, 0));
+        FusedCombine fz;
+        if (fused) {
+            fz.mailbox = rc_.mailbox;
+            fz.rank = g;
+            fz.nranks = nshards;
+            fz.epoch = epoch;
+        }
+        return launch_reduce(shards[g], n[g], dtype, (char *)c.d_slots + 8 * g, c.ws, c.ws_bytes,
+                             devs[g], c.s_comp, fz);
+    };
+    for (int g = 1; g < nshards; ++g)
+        if (int rc = launch(g)) return rc;
+    if (int rc = launch(0)) return rc;
+    // collect: the root's slot 0 holds the combined value (fused), else every slot
+    std::vector<char> part(8 * nshards, 0);
+    for (int g = 0; g < nshards; ++g) {
+        if (fused && g > 0) continue;
+        DevCtx &c = g_ctx[devs[g]];
+        if (int rc = check_dev(devs[g])) return rc;
+        B2_CUDA(cudaMemcpyAsync((char *)c.h_slots + 8 * g, (char *)c.d_slots + 8 * g, 8,
+                                cudaMemcpyDeviceToHost, c.s_comp));
+    }
+    for (int g = 0; g < nshards; ++g) {
+        if (int rc = check_dev(devs[g])) return rc;
+        B2_CUDA(cudaStreamSynchronize(g_ctx[devs[g]].s_comp));
+        memcpy(&part[8 * g], (char *)g_ctx[devs[g]].h_slots + 8 * g, 8);
+    }
+    if (fused) {
+        uint64_t st = 0;
+        if (int rc = check_dev(root)) return rc;
+        B2_CUDA(cudaMemcpy(&st, (char *)rc_.mailbox + 4 * 64 * 8 + 64 * 8 + 8, 8, cudaMemcpyDeviceToHost));
+        if (st) return fail(B2_ERR_CUDA, "reduce_multi: fused combine timed out");
+        memcpy(host_out, &part[0], dtype == B2_F32 ? 4 : 8);
+        return B2_OK;
+    }
+    // host combine, shard order (the fused kernel's order: identical result)
+    if (dtype == B2_I32) {
+        long long s = 0;
+        for (int g = 0; g < nshards; ++g) s += *(const long long *)&part[8 * g];
+        *(long long *)host_out = s;
+    } else if (dtype == B2_F32) {
+        volatile float s = 0.0f;
+        for (int g = 0; g < nshards; ++g) s = s + *(const float *)&part[8 * g];
+        *(float *)host_out = s;
+    } else {
+        double s = 0.0;
+        for (int g = 0; g < nshards; ++g) s += *(const double *)&part[8 * g];
+        *(double *)host_out = s;
     }
     return B2_OK;
 }

@@ -173,6 +173,77 @@ def reduce_ws_bytes(n: int, dtype: int) -> int:
     return int(lib().b2_reduce_ws_bytes(n, dtype))
 
 
+# ----------------------------------------------------------------------------- multi-GPU (one process)
+
+def _ptr_array(ptrs):
+    return (ctypes.c_void_p * len(ptrs))(*ptrs)
+
+
+def _i64_array(vals):
+    return (ctypes.c_int64 * len(vals))(*vals)
+
+
+def transpose_multi(shards, outs=None):
+    """Row-block sharded transpose driven from one process (b2_transpose_multi).
+
+    `shards[g]` is a rows_g x cols CUDA tensor (any device); `outs[g]` receives
+    its cols x rows_g transpose — by default a new tensor on the shard's device
+    (the output stays sharded); pass column-slab views of one full
+    matrix (e.g. `full[:, r0:r1]`, possibly on another GPU) to assemble it with
+    the kernels' own peer stores. Synchronous; returns `outs`."""
+    shards = [_as_device(t) for t in shards]
+    if not shards:
+        raise ValueError("transpose_multi: no shards")
+    cols = shards[0].shape[1] if shards[0].dim() == 2 else -1
+    dt = b2_dtype(shards[0])
+    for t in shards:
+        if not _is_torch_cuda(t) or t.dim() != 2 or t.shape[1] != cols or b2_dtype(t) != dt:
+            raise ValueError("transpose_multi: shards must be 2-D CUDA tensors with equal cols and dtype")
+        if t.numel() and t.stride(1) != 1:
+            raise ValueError("transpose_multi: shards must have unit column stride")
+    if outs is None:
+        outs = [torch.empty((cols, t.shape[0]), dtype=t.dtype, device=t.device) for t in shards]
+    outs = [_as_device(o) for o in outs]
+    if len(outs) != len(shards):
+        raise ValueError("transpose_multi: one output per shard")
+    for t, o in zip(shards, outs):
+        if not _is_torch_cuda(o) or tuple(o.shape) != (cols, t.shape[0]) or o.dtype != t.dtype \
+                or (o.numel() and o.stride(1) != 1):
+            raise ValueError("transpose_multi: outs[g] must be a (cols, rows_g) CUDA tensor, unit column stride")
+    check(lib().b2_transpose_multi(
+        _ptr_array([t.data_ptr() or None for t in shards]), _ptr_array([o.data_ptr() or None for o in outs]),
+        _i64_array([t.shape[0] for t in shards]), cols,
+        _i64_array([max(t.stride(0), cols) for t in shards]),
+        _i64_array([max(o.stride(0), t.shape[0]) for t, o in zip(shards, outs)]), dt, len(shards)))
+    return outs
+
+
+def reduce_sum_multi(shards):
+    """Sum over contiguous 1-D CUDA shards (any devices) with the cross-GPU
+    combine fused into the kernels (b2_reduce_sum_multi). Synchronous; returns a
+    Python float (fp32 / fp64) or int (int32 inputs, exact int64 sum)."""
+    shards = [_as_device(t) for t in shards]
+    if not shards:
+        raise ValueError("reduce_sum_multi: no shards")
+    d = b2_dtype(shards[0])
+    if d not in _ACC:
+        raise TypeError("reduce: dtype must be float32, int32 or float64")
+    for t in shards:
+        if not _is_torch_cuda(t) or t.dim() != 1 or b2_dtype(t) != d or (t.numel() and t.stride(0) != 1):
+            raise ValueError("reduce_sum_multi: shards must be contiguous 1-D CUDA tensors of one dtype")
+    res = np.zeros(1, dtype=_ACC[d][0])
+    check(lib().b2_reduce_sum_multi(_ptr_array([t.data_ptr() or None for t in shards]),
+                                    _i64_array([t.numel() for t in shards]), len(shards), d,
+                                    res.ctypes.data))
+    return res[0].item()
+
+
+def init_devices(ndev: int = 0) -> None:
+    """Create the library's per-device contexts and enable peer access between
+    every pair of devices 0..ndev-1 (all devices when ndev <= 0)."""
+    check(lib().b2_init(int(ndev)))
+
+
 # ----------------------------------------------------------------------------- device choice
 
 _HOST_DEVICE = None

@@ -66,3 +66,22 @@ def test_missing_library_fails_loudly(monkeypatch, tmp_path):
     monkeypatch.setattr(_lib, "_lib", None)
     with pytest.raises(ImportError, match="no CPU fallback"):
         _lib.lib()
+
+
+def test_multi_argument_validation():
+    """b2_transpose_multi / b2_reduce_sum_multi reject bad shard arrays before
+    touching a device."""
+    L = _lib.lib()
+    vp2 = (ctypes.c_void_p * 2)(None, None)
+    i2 = (ctypes.c_int64 * 2)(4, 4)
+    out = ctypes.c_double()
+    assert L.b2_transpose_multi(vp2, vp2, i2, 4, i2, i2, _lib.F32, 0) == _lib.B2_ERR_INVALID
+    assert L.b2_transpose_multi(vp2, vp2, i2, 4, i2, i2, 99, 2) == _lib.B2_ERR_UNSUPPORTED
+    assert L.b2_transpose_multi(vp2, vp2, i2, 4, i2, i2, _lib.F32, 2) == _lib.B2_ERR_INVALID  # NULL shard
+    neg = (ctypes.c_int64 * 2)(4, -1)
+    assert L.b2_transpose_multi(vp2, vp2, neg, 4, i2, i2, _lib.F32, 2) == _lib.B2_ERR_INVALID
+    assert L.b2_reduce_sum_multi(vp2, i2, 0, _lib.F32, ctypes.addressof(out)) == _lib.B2_ERR_INVALID
+    assert L.b2_reduce_sum_multi(vp2, i2, 2, _lib.U8, ctypes.addressof(out)) == _lib.B2_ERR_UNSUPPORTED
+    assert L.b2_reduce_sum_multi(vp2, neg, 2, _lib.I32, ctypes.addressof(out)) == _lib.B2_ERR_INVALID
+    assert L.b2_reduce_sum_multi(vp2, i2, 2, _lib.I32, None) == _lib.B2_ERR_INVALID
+    assert L.b2_peer_access(-1, 0) == 0

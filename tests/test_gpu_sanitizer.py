@@ -22,8 +22,8 @@ SAN = "/usr/local/cuda/bin/compute-sanitizer"
 
 CASES = [
     ("memcheck", "transpose"), ("memcheck", "transpose_big"), ("memcheck", "reduce"),
-    ("memcheck", "fused"), ("memcheck", "codegen"),
-    ("racecheck", "transpose"), ("racecheck", "reduce"), ("racecheck", "fused"),
+    ("memcheck", "fused"), ("memcheck", "multi"), ("memcheck", "codegen"),
+    ("racecheck", "transpose"), ("racecheck", "reduce"), ("racecheck", "fused"), ("racecheck", "multi"),
     ("racecheck", "codegen"),
     ("synccheck", "transpose"), ("synccheck", "reduce"), ("synccheck", "codegen"),
     ("initcheck", "transpose"), ("initcheck", "reduce"),

@@ -9,7 +9,7 @@ addressing. Every case also checks its result bit-exact (transposes, integer
 sums, A.5 tree order) or within the north-star tolerance (fp32 sums), so a
 sanitizer run is also a parity run.
 
-    python tools/sanitize_driver.py [transpose|reduce|fused|codegen|all]
+    python tools/sanitize_driver.py [transpose|transpose_big|reduce|fused|multi|codegen|all]
 
 Used by tests/test_gpu_sanitizer.py; needs a GPU, no torch CUDA context.
 """
@@ -234,7 +234,35 @@ def run_transpose_big(rng):
     one_transpose(256 * 37, 64 * 32 + 24, np.float64, rng)
 
 
-GROUPS = {"transpose": run_transpose, "transpose_big": run_transpose_big, "reduce": run_reduce, "fused": run_fused, "codegen": run_codegen}
+def run_multi(rng):
+    """Single-process multi-shard entries (all shards on device 0 here)."""
+    k = 3
+    a = rand((300, 200), np.float32, rng)
+    cuts = [0, 128, 256, 300]
+    ins = [h2d(np.ascontiguousarray(a[cuts[g]:cuts[g + 1]])) for g in range(k)]
+    outs = [dalloc(200 * (cuts[g + 1] - cuts[g]) * 4) for g in range(k)]
+    rows = [cuts[g + 1] - cuts[g] for g in range(k)]
+    vp = ctypes.c_void_p * k
+    i64 = ctypes.c_int64 * k
+    check(L.b2_transpose_multi(vp(*ins), vp(*outs), i64(*rows), 200, i64(*[200] * k), i64(*rows), _lib.F32, k))
+    for g in range(k):
+        got = d2h(outs[g], np.empty((200, rows[g]), np.float32))
+        assert np.array_equal(got, a[cuts[g]:cuts[g + 1]].T), g
+        dfree(ins[g])
+        dfree(outs[g])
+    x = rng.integers(-2**31, 2**31, 1_000_003, dtype=np.int64).astype(np.int32)
+    cuts = [0, 1, 500_000, 1_000_003]
+    ps = [h2d(np.ascontiguousarray(x[cuts[g]:cuts[g + 1]])) for g in range(k)]
+    r = np.zeros(1, np.int64)
+    for _ in range(5):
+        check(L.b2_reduce_sum_multi(vp(*ps), i64(*[cuts[g + 1] - cuts[g] for g in range(k)]), k, _lib.I32,
+                                    r.ctypes.data))
+        assert int(r[0]) == int(x.astype(np.int64).sum())
+    for p in ps:
+        dfree(p)
+
+
+GROUPS = {"transpose": run_transpose, "multi": run_multi, "transpose_big": run_transpose_big, "reduce": run_reduce, "fused": run_fused, "codegen": run_codegen}
 
 if __name__ == "__main__":
     which = sys.argv[1:] or ["all"]

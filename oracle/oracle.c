@@ -30,6 +30,7 @@
  *                 sequentially in binary32 (interp.py
  *                 :282-300 thread-for executed in ascending order).
  */
+#include <math.h>
 #include <stdint.h>
 #include <string.h>
 #include <omp.h>
@@ -118,6 +119,29 @@ OR_EXPORT void or_sum_f64(const float *x, int64_t n, double *sum, double *abssum
     }
     *sum = s + c;
     *abssum = a;
+}
+
+/* interp.py:262-270 for a float cell: `sum += v` is f32(old + v) with old and v
+ * Python floats (binary64), i.e. a binary64 add rounded to binary32. Segmented
+ * form for the vectorised interpreter (oracle/vinterp.py): segment g folds
+ * v[ends[g-1] .. ends[g]) into acc[g] in order. Returns 1 if a finite sum
+ * rounded to infinity (struct.pack("f") raises OverflowError there on older
+ * CPythons and returns +-inf on 3.12+, :43-44; the caller applies the rule). */
+OR_EXPORT int or_seg_f32_fold(const double *v, const int64_t *ends, int64_t nseg, double *acc) {
+    int64_t b = 0;
+    int ovf = 0;
+    for (int64_t g = 0; g < nseg; ++g) {
+        volatile double s = acc[g];
+        for (int64_t i = b; i < ends[g]; ++i) {
+            const double t = s + v[i];
+            const float r = (float)t;
+            if (isinf(r) && !isinf(t)) ovf = 1;
+            s = (double)r;
+        }
+        acc[g] = s;
+        b = ends[g];
+    }
+    return ovf;
 }
 
 /* Fast synthetic data (splitmix64) so the CPU legs do not spend minutes in numpy. */

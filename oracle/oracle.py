@@ -52,6 +52,8 @@ def lib():
         L.or_reduce_f32_tree512.restype = ctypes.c_int
         L.or_sum_f64.argtypes = [vp, i64, vp, vp]
         L.or_fill_u32.argtypes = [vp, i64, ctypes.c_uint64, ctypes.c_int]
+        L.or_seg_f32_fold.argtypes = [vp, vp, i64, vp]
+        L.or_seg_f32_fold.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -111,6 +113,15 @@ def sum_f64(x: np.ndarray) -> tuple[float, float]:
     a = np.zeros(1, dtype=np.float64)
     lib().or_sum_f64(_ptr(x), x.size, _ptr(s), _ptr(a))
     return float(s[0]), float(a[0])
+
+
+def seg_f32_fold(v: np.ndarray, ends: np.ndarray, acc: np.ndarray) -> bool:
+    """In place: acc[g] = f32(... f32(acc[g] + v[b]) ... + v[e-1]) per segment
+    [ends[g-1], ends[g]); v, acc float64; returns True on binary32 overflow."""
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    ends = np.ascontiguousarray(ends, dtype=np.int64)
+    assert acc.dtype == np.float64 and acc.flags.c_contiguous and acc.size == ends.size
+    return bool(lib().or_seg_f32_fold(_ptr(v), _ptr(ends), ends.size, _ptr(acc)))
 
 
 def fill_u32(x: np.ndarray, seed: int, nthreads: int = 0) -> None:

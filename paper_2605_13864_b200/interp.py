@@ -131,11 +131,24 @@ def _cells(arr, n: int, want: str) -> np.ndarray:
     return _ints(part)
 
 
+def _struct_f_overflow_raises() -> bool:
+    """struct.pack("f", x) for |x| beyond binary32 raises OverflowError on older
+    CPythons and rounds to +-inf on 3.12+; f32() (interp.py:43-44) inherits
+    whichever this interpreter does, so the drop-in follows the same rule."""
+    try:
+        struct.pack("f", 1e300)
+        return False
+    except OverflowError:
+        return True
+
+
+_F32_OVERFLOW_RAISES = _struct_f_overflow_raises()
+
+
 def _to_f32(v: np.ndarray) -> np.ndarray:
     with np.errstate(over="ignore"):
         r = v.astype(np.float32)
-    bad = np.isinf(r) & np.isfinite(v)
-    if bad.any():  # struct.pack("f") refuses these (interp.py:44)
+    if _F32_OVERFLOW_RAISES and (np.isinf(r) & np.isfinite(v)).any():
         raise OverflowError("float too large to pack with f format")
     return r
 

@@ -175,6 +175,37 @@ def cpu_leg(rows, cols, n, reps=1):
             "transpose_s": tt, "reduce_s": tr, "checksum": s}
 
 
+def interp_leg(rows, cols, n):
+    """The reference's interpreter semantics on host cores: the A.1 transpose and
+    A.3 int reduce PROGRAMS executed by oracle/vinterp.py (vectorised restatement
+    of minigpu.interp, one core, numpy) on a bounded sample — what running the
+    reference's own program path costs once it is not a per-element Python walk."""
+    import paper_2605_13864_b200 as b2
+    from oracle import oracle, vinterp
+    a = np.empty((rows, cols), dtype=np.float32)
+    oracle.fill_u32(a.view(np.uint32).reshape(-1), 3)
+    a[~np.isfinite(a)] = 0.0  # finite cells, like the GPU leg's inputs
+    out = np.zeros(rows * cols, np.float32)
+    x = np.empty(n, dtype=np.int32)
+    oracle.fill_u32(x.view(np.uint32), 4)
+    tp = b2.parse_program(b2.programs.TRANSPOSE_NAIVE)
+    rp = b2.parse_program(b2.programs.REDUCE_NAIVE_INT)
+    t0 = time.perf_counter()
+    vinterp.run_program(tp, "transpose", {"in": b2.Array([rows, cols], a.reshape(-1), "float"),
+                                          "out": b2.Array([cols, rows], out, "float"), "W": cols, "H": rows},
+                        as_numpy=True)
+    t1 = time.perf_counter()
+    s, _ = vinterp.run_program(rp, "reduce", {"arr": b2.Array([n], x, "int"), "N": n}, as_numpy=True)
+    t2 = time.perf_counter()
+    assert s == oracle.reduce_i32(x)
+    assert np.array_equal(out.reshape(cols, rows)[:5, :7], a[:7, :5].T)
+    bytes_ = 2 * rows * cols * 4 + n * 4 + 8
+    return {"value": bytes_ / (t2 - t0) / 1e9, "unit": "GB/s", "cores": 1, "kind": "port",
+            "transpose_s": t1 - t0, "reduce_s": t2 - t1,
+            "sample": (f"programs A.1 (fp32 {rows}x{cols}) + A.3 (int32 n={n}) run by oracle/vinterp.py, "
+                       "the vectorised restatement of minigpu.interp (single core)")}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -210,8 +241,11 @@ def run_reference(args):
                          "sample": sample},
         "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "note": ("reference = minigpu.interp (pure Python, ~1 MB/s single core; cannot run 12 GiB "
-                 "workloads), timed through its C restatement oracle/oracle.c"),
+                 "workloads), timed through its C restatement oracle/oracle.c; interp_semantics = "
+                 "the same programs through the vectorised interpreter restatement"),
     }
+    if not args.no_cpu:
+        line["interp_semantics"] = interp_leg(min(rows, 2048), cols, min(n, 1 << 26))
     print(json.dumps(line), flush=True)
     return 0
 

@@ -18,9 +18,10 @@ from .lang import ParseError, Program, parse_program  # noqa: F401
 from .ops import (init_devices, reduce_sum, reduce_sum_multi, reduce_tree512,  # noqa: F401
                   reduce_tree512_partials, transpose, transpose_multi)
 from .recognize import recognize  # noqa: F401
+from .gate import GateError, check_kernels  # noqa: F401
 from . import programs  # noqa: F401
 
 __all__ = ["run_program", "Interp", "Array", "InterpError", "UnsupportedProgram", "f32",
            "parse_program", "ParseError", "Program", "recognize", "transpose", "reduce_sum",
            "reduce_tree512", "reduce_tree512_partials", "transpose_multi", "reduce_sum_multi",
-           "init_devices", "B2Error", "launch_count"]
+           "init_devices", "GateError", "check_kernels", "B2Error", "launch_count"]

@@ -196,14 +196,18 @@ class Interp:
 
     BACKENDS = ("auto", "kernels", "codegen")
 
-    def __init__(self, program, backend: str = "auto"):
+    def __init__(self, program, backend: str = "auto", check=None):
         """backend: "kernels" = only the hand-written kernels (recognised
         programs); "codegen" = compile any GPU-form program (codegen.py);
-        "auto" = kernels when the program is recognised, else codegen."""
+        "auto" = kernels when the program is recognised, else codegen.
+        check: pre-dispatch gate (gate.py): None (the reference's behaviour),
+        "kernels" (device-side checker rules for this launch) or a callable
+        such as minigpu.checker.check_program."""
         if backend not in self.BACKENDS:
             raise ValueError(f"backend must be one of {self.BACKENDS}")
         self.program = program
         self.backend = backend
+        self.check = check
         self.launch: list = []
         self.ctx_width: list = []
 
@@ -249,16 +253,19 @@ class Interp:
                 env[pname] = arr
             else:
                 env[pname] = v
+        if self.check is not None:
+            from .gate import run_check
+            run_check(self.check, self.program, fn_name, env)
         return self._dispatch(fn, fn_name, env, arrays), arrays
 
 
-def run_program(program, entry: str, inputs: dict, backend: str = "auto"):
+def run_program(program, entry: str, inputs: dict, backend: str = "auto", check=None):
     """Returns (return value, {param name: flat final array data}) (interp.py:380-387).
 
     List-backed arrays come back as fresh lists; numpy-backed arrays come back
     as the (mutated) numpy buffer itself. `backend` selects hand-written kernels
-    and/or generated code (see Interp)."""
-    it = Interp(program, backend)
+    and/or generated code, `check` an optional pre-dispatch gate (see Interp)."""
+    it = Interp(program, backend, check)
     ret, arrays = it.run(entry, dict(inputs))
     out = {k: (a.data if isinstance(a.data, np.ndarray) else list(a.data))
            for k, a in arrays.items()}

@@ -96,8 +96,9 @@ __global__ void __launch_bounds__(NT)
     uint4 reg[MT][V];
 
     // Tile order: bands of `group` tile-rows, walked column by column inside a
-    // band, so CTAs running at the same time write neighbouring column blocks of
-    // the same output rows (and still read long runs of the same input rows).
+    // band; with group = tiles_r (the default) the walk is column-major, so CTAs
+    // running at the same time work down one column block and write neighbouring
+    // segments of the same output rows.
     auto origin = [&](int64_t tile, int64_t &r0, int64_t &c0) {
         const int64_t per_band = (int64_t)group * tiles_c;
         const int64_t band = tile / per_band, w = tile - band * per_band;
@@ -171,8 +172,11 @@ __global__ void __launch_bounds__(256)
     constexpr int PAD = sizeof(T) == 2 ? 2 : 1;
     __shared__ T tile[TS][TS + PAD];
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+    const int64_t tiles_r = ntiles / tiles_c;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const int64_t r0 = r_lo + (t / tiles_c) * TS, c0 = c_lo + (t % tiles_c) * TS;
+        // column-major tile walk, as in the vector path: concurrent tiles share
+        // output rows, so the (short) output segments merge into long write runs
+        const int64_t r0 = r_lo + (t % tiles_r) * TS, c0 = c_lo + (t / tiles_r) * TS;
         T v[TS / 8][2];
 #pragma unroll
         for (int j = 0; j < TS / 8; ++j) {
@@ -257,8 +261,12 @@ int run_vec(const void *in, void *out, int64_t rows_v, int64_t cols_v, int64_t l
     const int auto_sm = std::max(1, kInflightBytesPerSM / kTileBytes);
     const int per_sm = std::min(g_tune.t_ctas_per_sm > 0 ? g_tune.t_ctas_per_sm : auto_sm, occ[dev]);
     const int64_t grid = std::min<int64_t>(ntiles, (int64_t)num_sms(dev) * per_sm);
-    // band height: 4 tile-rows for small tiles, 1 for the 128-KB tiles (tune_big sweep)
-    const int grp = g_tune.t_group > 0 ? g_tune.t_group : (kTileBytes >= 64 * 1024 ? 1 : 4);
+    // Tile walk: column-major by default (band height = all tile-rows), so the ~#SM
+    // tiles in flight sit in one column block and their output rows are written as
+    // long contiguous runs; DRAM efficiency is set by the write side. Measured on
+    // B200 (profiles/r01h_colwalk.md): fp32 32768^2 6.37-6.43 TB/s vs 6.01-6.18 with
+    // row-major bands, fp64 +5 %, bf16 +3 %.
+    const int grp = g_tune.t_group > 0 ? g_tune.t_group : (int)std::min<int64_t>(tiles_r, 1 << 30);
     const int group = (int)std::max<int64_t>(1, std::min<int64_t>(grp, tiles_r));
     transpose_vec_kernel<E, TRV, TCV, NT><<<(unsigned)grid, NT, kSmem, st>>>(
         (const uint8_t *)in, (uint8_t *)out, rows_v, cols_v, ld_in * E, ld_out * E, tiles_r,

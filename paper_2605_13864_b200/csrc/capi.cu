@@ -653,43 +653,66 @@ int b2_transpose_host(const void *in_host, void *out_host, int64_t rows, int64_t
     DevCtx &c = g_ctx[dev];
     std::lock_guard<std::mutex> g(c.mu);
     if (int rc = ctx_init(c, dev)) return rc;
-    // chunk = a block of input rows -> a column slab of the output
-    const int64_t row_bytes = cols * E;
-    int64_t cr = std::max<int64_t>(1, (int64_t)(chunk_bytes() / (size_t)row_bytes));
-    if (cr >= 64) cr -= cr % 64;  // whole tiles per chunk
+    // Chunk = a cr x cc block of the input -> a cc x cr block of the output, both
+    // moved as 2-D DMA copies. Rows of either copy shorter than ~4 KB drop the copy
+    // engines from 57 to 48 GB/s (profiles/r01i_pcie.md), so cr is at least 4 KB of
+    // cells (output rows) and cc takes the rest of the chunk budget (input rows);
+    // whole 64-row tiles per chunk where possible.
+    const size_t budget = chunk_bytes();
+    const int64_t min_run = std::max<int64_t>(64, 4096 / E);
+    int64_t cr, cc;
+    if ((size_t)cols * E * (size_t)min_run <= budget) {  // full-width row blocks
+        cc = cols;
+        cr = std::max<int64_t>(min_run, (int64_t)(budget / ((size_t)cols * E)));
+    } else {
+        cr = min_run;
+        cc = std::max<int64_t>(64, (int64_t)(budget / ((size_t)cr * E)));
+    }
+    if (cr >= 64) cr -= cr % 64;
+    if (cc >= 64 && cc < cols) cc -= cc % 64;
     cr = std::min(cr, rows);
-    if (int rc = ensure_stages(c, (size_t)cr * row_bytes)) return rc;
+    cc = std::min(cc, cols);
+    if (int rc = ensure_stages(c, (size_t)cr * cc * E)) return rc;
     const bool stage_in = !is_pinned(in_host), stage_out = !is_pinned(out_host);
-    if ((stage_in || stage_out) && ensure_host_stages(c, (size_t)cr * row_bytes)) return B2_ERR_NOMEM;
+    if ((stage_in || stage_out) && ensure_host_stages(c, (size_t)cr * cc * E)) return B2_ERR_NOMEM;
     const char *hin = (const char *)in_host;
     char *hout = (char *)out_host;
-    const int64_t nchunks = (rows + cr - 1) / cr;
+    const int64_t nbr = (rows + cr - 1) / cr, nbc = (cols + cc - 1) / cc;
+    const int64_t nchunks = nbr * nbc;
+    auto block = [&](int64_t i, int64_t &r0, int64_t &nr, int64_t &c0, int64_t &nc) {
+        r0 = (i / nbc) * cr;
+        c0 = (i % nbc) * cc;
+        nr = std::min(cr, rows - r0);
+        nc = std::min(cc, cols - c0);
+    };
     // pageable destination: the D2H lands in hs_out[k]; the host scatters it into the
-    // output column slab one chunk later, overlapped with the next chunk's DMA
+    // output block one chunk later, overlapped with the next chunk's DMA
     auto scatter = [&](int64_t j) -> int {
         const int kk = (int)(j % kStages);
-        const int64_t r0 = j * cr, nr = std::min(cr, rows - r0);
+        int64_t r0, nr, c0, nc;
+        block(j, r0, nr, c0, nc);
         B2_CUDA(cudaEventSynchronize(c.ev_out[kk]));
-        par_copy2d(hout + r0 * E, ld_out * E, c.hs_out[kk], nr * E, nr * E, cols);
+        par_copy2d(hout + (c0 * ld_out + r0) * E, ld_out * E, c.hs_out[kk], nr * E, nr * E, nc);
         return B2_OK;
     };
     for (int64_t i = 0; i < nchunks; ++i) {
         const int k = (int)(i % kStages);
-        const int64_t r0 = i * cr, nr = std::min(cr, rows - r0);
+        int64_t r0, nr, c0, nc;
+        block(i, r0, nr, c0, nc);
         if (i >= kStages) B2_CUDA(cudaStreamWaitEvent(c.s_h2d, c.ev_comp[k], 0));  // d_in[k] free
-        if (int rc = h2d_rows(c, k, stage_in, c.d_in[k], hin + r0 * ld_in * E, ld_in * E, row_bytes, nr))
+        if (int rc = h2d_rows(c, k, stage_in, c.d_in[k], hin + (r0 * ld_in + c0) * E, ld_in * E, nc * E, nr))
             return rc;
         B2_CUDA(cudaEventRecord(c.ev_in[k], c.s_h2d));
         B2_CUDA(cudaStreamWaitEvent(c.s_comp, c.ev_in[k], 0));
         if (i >= kStages) B2_CUDA(cudaStreamWaitEvent(c.s_comp, c.ev_out[k], 0));  // d_out[k] free
-        if (int rc = launch_transpose(c.d_in[k], c.d_out[k], nr, cols, cols, nr, E, dev, c.s_comp))
+        if (int rc = launch_transpose(c.d_in[k], c.d_out[k], nr, nc, nc, nr, E, dev, c.s_comp))
             return rc;
         B2_CUDA(cudaEventRecord(c.ev_comp[k], c.s_comp));
         B2_CUDA(cudaStreamWaitEvent(c.s_d2h, c.ev_comp[k], 0));
         if (stage_out)
-            B2_CUDA(cudaMemcpyAsync(c.hs_out[k], c.d_out[k], (size_t)nr * E * cols, cudaMemcpyDeviceToHost, c.s_d2h));
+            B2_CUDA(cudaMemcpyAsync(c.hs_out[k], c.d_out[k], (size_t)nr * E * nc, cudaMemcpyDeviceToHost, c.s_d2h));
         else
-            B2_CUDA(cudaMemcpy2DAsync(hout + r0 * E, ld_out * E, c.d_out[k], nr * E, nr * E, cols,
+            B2_CUDA(cudaMemcpy2DAsync(hout + (c0 * ld_out + r0) * E, ld_out * E, c.d_out[k], nr * E, nr * E, nc,
                                       cudaMemcpyDeviceToHost, c.s_d2h));
         B2_CUDA(cudaEventRecord(c.ev_out[k], c.s_d2h));
         if (stage_out && i > 0)

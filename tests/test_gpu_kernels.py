@@ -176,6 +176,30 @@ def test_host_paths_staging(b2, pinned):
         _lib.tune("host.chunk_mb", 64)
 
 
+@pytest.mark.parametrize("dt", [np.float32, np.float64, np.uint16])
+@pytest.mark.parametrize("pinned", [False, True])
+@pytest.mark.parametrize("chunk_mb", [1, 3])
+def test_host_transpose_2d_chunks(b2, dt, pinned, chunk_mb):
+    """b2_transpose_host moves cr x cc blocks (>= 4 KB rows on both DMA sides):
+    ragged last blocks, pitched sub-views, pinned and staged buffers."""
+    from paper_2605_13864_b200 import _lib
+    _lib.tune("host.chunk_mb", chunk_mb)
+    try:
+        rng = np.random.default_rng(7)
+        big_in = rng.integers(0, 2**16, (1300, 3100)).astype(dt)
+        big_out = np.zeros((3090, 1310), dtype=dt)
+        if pinned:
+            big_in = torch.from_numpy(big_in).pin_memory().numpy()
+            big_out = torch.from_numpy(big_out).pin_memory().numpy()
+        src = big_in[3:1298, 5:3085]
+        dst = big_out[:3080, 7:1302]
+        b2.transpose(src, dst)
+        assert np.array_equal(dst, src.T)
+        assert (big_out[:, :7] == 0).all() and (big_out[:, 1302:] == 0).all() and (big_out[3080:] == 0).all()
+    finally:
+        _lib.tune("host.chunk_mb", 64)
+
+
 class _CAI:
     """Minimal foreign CUDA array (as CuPy / Numba expose it)."""
 

@@ -1,7 +1,8 @@
 """BASELINE config C5 size sweep on one B200: reductions 2^10 .. 2^32 (fp32,
 int32) and odd / non-square transposes (bf16, fp32, fp64), each checked
 against the CPU oracle, timed with CUDA events (median of REPS after warm-up,
-L2 flushed by a 252 MB write before every launch when the working set is
+L2 flushed by a 252 MB read pass (clean lines, no write-back inside the timed
+kernel) before every launch when the working set is
 smaller than 4x L2). Also times the in-step interference experiment
 (transpose and reduce alternating vs. isolated vs. CUDA-graph captured).
 
@@ -23,7 +24,7 @@ from oracle import oracle  # noqa: E402  (checker only)
 L2 = 126 * 1024 * 1024
 REPS = 15
 dev = torch.device("cuda", 0)
-flush = torch.empty(2 * L2 // 4, dtype=torch.float32, device=dev)
+flush = torch.ones(2 * L2 // 4, dtype=torch.float32, device=dev)
 results = []
 
 
@@ -34,7 +35,7 @@ def timeit(fn, nbytes, reps=REPS):
     ts = []
     for i in range(reps):
         if do_flush:
-            flush.fill_(float(i))
+            flush.sum()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         fn()

@@ -389,10 +389,11 @@ def main():
     ms_t = statistics.mean(e[0].elapsed_time(e[1]) for e in evs)
     ms_r = statistics.mean(e[1].elapsed_time(e[2]) for e in evs)
     ms_max = ms
+    ms_k = (ms_t + ms_r) * args.steps  # transpose + reduce kernels (a separate NCCL combine excluded)
     if world > 1:
-        tt = torch.tensor([ms], device=dev, dtype=torch.float64)
+        tt = torch.tensor([ms, ms_k], device=dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms_max = float(tt.item())
+        ms_max, ms_k = float(tt[0].item()), float(tt[1].item())
 
     bytes_t = 2 * rows * cols * 4
     bytes_r = n * 4 + 8
@@ -400,6 +401,9 @@ def main():
     tot_n = n * world if args.scaling == "weak" else args.n
     total_bytes = 2 * tot_rows * cols * 4 + tot_n * 4 + 8 * world
     value = total_bytes * args.steps / (ms_max / 1e3) / 1e9
+    # aggregate GB/s also without the combine step (with the fused combine
+    # it runs inside the reduction kernel and cannot be separated)
+    value_k = total_bytes * args.steps / (ms_k / 1e3) / 1e9
     peak, peak_src = peaks()
     ach_t = bytes_t / (ms_t / 1e3) / 1e9
     ach_r = bytes_r / (ms_r / 1e3) / 1e9
@@ -444,6 +448,7 @@ def main():
                        "traffic": traffic_r},
         },
         "gpu_launches": launches,
+        "value_kernels_only": value_k,
         "launch_mode": ("CUDA graph: K steps captured once, replayed once in the timed region"
                         if use_graph else "eager stream launches"),
         "clocks": clk.summary(),

@@ -449,6 +449,9 @@ def main():
         },
         "gpu_launches": launches,
         "value_kernels_only": value_k,
+        # north star: whole-job GB/s as a fraction of the aggregate HBM roofline (N x peak)
+        "aggregate_roofline": {"peak": peak * world, "unit": "GB/s", "frac": value / (peak * world),
+                               "frac_kernels_only": value_k / (peak * world)},
         "launch_mode": ("CUDA graph: K steps captured once, replayed once in the timed region"
                         if use_graph else "eager stream launches"),
         "clocks": clk.summary(),

@@ -87,6 +87,7 @@ class _KernelGate:
         self.dims = dims         # name -> dims (per-block dims for smem), when known
         self.glog = []           # (name, addr, global thread id, is_write) over the launch
         self.blocks = 0
+        self.assigned = set()    # cells assigned in the kernel: their values are not tracked
 
     # ------------------------------------------------------------ values
     def eval(self, e, env, lanes):
@@ -96,6 +97,8 @@ class _KernelGate:
         if c == "FloatLit":
             return DATA
         if c == "Var":
+            if e.name in self.assigned:
+                return DATA
             if e.name in env:
                 return env[e.name]
             raise GateError("E-GATE-UNSUPPORTED", f"unbound variable {e.name!r} in a kernel")
@@ -232,8 +235,8 @@ class _KernelGate:
                 if s.op == "+=":
                     self.access(s.target.base, s.target.idxs, env, lanes, False)
                 self.access(s.target.base, s.target.idxs, env, lanes, True)
-            elif s.target.base in env:
-                env[s.target.base] = DATA
+            else:
+                self.assigned.add(s.target.base)
         elif c == "For":
             a, b = self.index(s.range.start, env, lanes), self.index(s.range.stop, env, lanes)
             if isinstance(a, np.ndarray) or isinstance(b, np.ndarray):

@@ -139,3 +139,24 @@ def test_gated_programs_run_on_gpu():
     ret, _ = b2.run_program(parse_program(reduce_family(128, "int")), "reduce", {"arr": x.tolist(), "N": x.size},
                             check="kernels", backend="codegen")
     assert ret == int(x.astype(np.int64).sum())
+
+
+def test_assigned_cell_in_index_is_not_tracked():
+    """A cell assigned inside the kernel (here in a nested block) may hold any
+    value afterwards: indexing with it is refused, never analysed with a stale value."""
+    src = """void f(int* a, int N) {
+    int* const d = gmem_malloc1<int>(N);
+    memcpy_host_to_device1(d, a, N);
+    {
+        kernel_launch(1, N, 0);
+        kernel_setup_end();
+        thread for (int t = 0; t < N; t++) { int k = t; { k = 0; } d[k] = t; }
+        kernel_teardown_begin();
+        kernel_kill();
+    }
+    memcpy_device_to_host1(a, d, N);
+    gmem_free(d);
+}"""
+    with pytest.raises(GateError) as ei:
+        check_kernels(parse_program(src), "f", {"a": [0] * 8, "N": 8})
+    assert ei.value.code == "E-GATE-DATA"

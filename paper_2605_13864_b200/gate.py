@@ -11,6 +11,8 @@ that gate in front of the B200 dispatch:
   * check="kernels"   — this module: the checker's *device-side* rules, decided
     for the concrete launch (the parameters are known at dispatch time), with the
     checker's error codes:
+      E-SMEM         the launch's shared-memory size is exactly what the
+                     kernel's __smem_malloc calls allocate (checker.py:298-318);
       E-THREADS-CTX  `blocksync()` must run in a block-wide thread context of
                      exactly tpb threads, outside thread-dependent branches
                      (checker.py:779-789); global memory is only accessed from a
@@ -379,13 +381,28 @@ def check_kernels(program, entry: str, inputs: dict) -> dict:
     def kernel(seq, env):
         st = [x for x in _stmts(seq) if not (_cls(x) == "CallStmt" and x.ghost)]
         bpg, tpb = _host_eval(st[0].args[0], env), _host_eval(st[0].args[1], env)
+        # shared-memory accounting (checker.py:298-318, intrinsics.py:70-84): the
+        # launch's smem_sz is an allowance each __smem_malloc consumes (4-byte
+        # cells, intrinsics.py:35); kernel_setup_end needs it used up exactly
+        allowance = _host_eval(st[0].args[2], env) if len(st[0].args) > 2 else 0
         arr = dict(arrays)
         kd = dict(dims)
         body = []
         for x in st[1:]:
+            if _cls(x) == "CallStmt" and x.fn == "kernel_setup_end" and allowance != 0:
+                raise GateError("E-SMEM", f"kernel_setup_end needs the whole shared-memory allowance "
+                                          f"allocated: {allowance} bytes left")
             if _cls(x) == "Decl" and x.alloc in ("__smem_malloc", "__treg_malloc"):
                 arr[x.name] = "smem" if x.alloc == "__smem_malloc" else "treg"
                 kd[x.name] = [_host_eval(d, env) for d in x.dims]
+                if x.alloc == "__smem_malloc":
+                    nbytes = 4
+                    for d in kd[x.name]:
+                        nbytes *= d
+                    allowance -= nbytes
+                    if allowance < 0:
+                        raise GateError("E-SMEM", f"shared memory over-allocation: remaining allowance "
+                                                  f"{allowance} is negative")
             elif _cls(x) == "CallStmt" and (x.fn.startswith("__smem_free") or x.fn in ("kernel_kill",)):
                 continue
             else:

@@ -160,3 +160,24 @@ def test_assigned_cell_in_index_is_not_tracked():
     with pytest.raises(GateError) as ei:
         check_kernels(parse_program(src), "f", {"a": [0] * 8, "N": 8})
     assert ei.value.code == "E-GATE-DATA"
+
+
+@pytest.mark.parametrize("smem,code,msg", [(4 * 32 * 32, None, None),
+                                           (4 * 32 * 32 - 4, "E-SMEM", "over-allocation"),
+                                           (4 * 32 * 32 + 64, "E-SMEM", "64 bytes left")])
+def test_shared_memory_accounting(smem, code, msg):
+    """SPEC acceptance 5: over-allocation refused at the malloc, under-allocation
+    at kernel_setup_end, the exact size accepted."""
+    src = programs.TRANSPOSE_GPU.replace("4 * 32 * 32", str(smem), 1)
+    if code is None:
+        assert check_kernels(parse_program(src), "transpose", _tin(32, 32))["kernels"] == 1
+        return
+    with pytest.raises(GateError) as ei:
+        check_kernels(parse_program(src), "transpose", _tin(32, 32))
+    assert ei.value.code == code and msg in ei.value.message
+
+
+def test_barrier_flip_block_level_accepted():
+    """SPEC acceptance 3: the same barrier at block level (the canonical A.4) is
+    accepted; inside the thread loop it is refused (test above)."""
+    assert check_kernels(parse_program(programs.TRANSPOSE_GPU), "transpose", _tin(32, 32))["kernels"] == 1

@@ -57,3 +57,41 @@ def test_unsupported_constructs_refused(src, msg):
     fn = parse_program(src).entry()
     with pytest.raises(UnsupportedProgram, match=msg):
         codegen.generate(fn)
+
+
+def test_a4_structure_like_spec_acceptance_1():
+    """SPEC.md:524 (acceptance 1) asks the emitted transpose to have one
+    __global__ function, one shared tile, exactly one __syncthreads(), a launch of
+    (W/32)*(H/32) blocks, no DMINDEX / ghosts, and host code with two device
+    allocations, one copy each way and two frees. Same checks on our generator's
+    output (its runtime calls stand for cudaMalloc / cudaMemcpy / cudaFree)."""
+    src = codegen.generate(_fn("transpose_gpu.optc"))
+    kernel = src[src.index("__global__"):src.index('extern "C" int b2g_main')]
+    host = src[src.index('extern "C" int b2g_main'):]
+    assert src.count("__global__") == 1
+    assert kernel.count("__syncthreads();") == 1
+    assert kernel.count("float *v_tile = (float *)(b2_smem") == 1
+    assert "DMINDEX" not in src and "__ghost" not in src
+    assert host.count("<<<") == 1
+    assert "b2_exact_div_h(v_W, ((int64_t)32LL)) * b2_exact_div_h(v_H, ((int64_t)32LL))" in host
+    assert "(((int64_t)16LL) * ((int64_t)32LL))" in host  # 512 threads per block
+    assert host.count("b2_dev_alloc<float>(") == 2
+    assert host.count("b2_h2d(") == 1 and host.count("b2_d2h(") == 1
+    assert host.count(".freed = true;") == 2
+
+
+def test_a5_structure_tree_loop_with_barrier():
+    """SPEC.md:525 (acceptance 2): the reduction kernel holds a sequential halving
+    loop with __syncthreads() inside it."""
+    src = codegen.generate(_fn("reduce_tree_f32.optc"))
+    kernel = src[src.index("__global__"):src.index('extern "C" int b2g_main')]
+    start = kernel.index("for (int64_t v_k")
+    depth, i = 0, kernel.index("{", start)
+    while True:  # the loop body: up to the brace that closes the for
+        depth += {"{": 1, "}": -1}.get(kernel[i], 0)
+        if depth == 0:
+            break
+        i += 1
+    body = kernel[start:i]
+    assert body.count("__syncthreads();") == 1  # one barrier per tree level, inside the loop
+    assert kernel.count("__syncthreads();") == 2  # plus the one after the pair loads

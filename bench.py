@@ -458,7 +458,16 @@ def main():
     }
 
     if not args.no_e2e:
-        res["e2e"] = e2e_leg(b2, a, x, rows, cols, n, args, world, dev)
+        # pinned host buffers: 12 GiB per rank at the default sizes; if the host cannot
+        # pin that much, measure the same path on half-height / half-length shards
+        try:
+            res["e2e"] = e2e_leg(b2, a, x, rows, cols, n, args, world, dev)
+        except (RuntimeError, MemoryError) as e:
+            import gc
+            gc.collect()
+            torch.cuda.empty_cache()
+            res["e2e"] = e2e_leg(b2, a[: rows // 2], x[: n // 2], rows // 2, cols, n // 2, args, world, dev)
+            res["e2e"]["note"] = f"half-size shards: full-size pinned buffers failed ({str(e)[:120]})"
     if args.paper_configs and world == 1:
         res["paper_configs"] = paper_configs(b2, dev)
     if rank == 0 and world == 1 and not args.no_cpu:

@@ -427,7 +427,9 @@ class _Parser:
             idxs = self.indices()
             op = self.take()
             if op.val not in ("=", "+=") or op.kind == "string":
-                raise ParseError(f"expected assignment, found {op.val!r}", op.line, op.col,
+                # reported at the token after the offending one, as parser.py:150-152 does
+                nt = self.peek()
+                raise ParseError(f"expected assignment, found {op.val!r}", nt.line, nt.col,
                                  self.filename)
             val = self.expr()
             self.need(";")
@@ -476,7 +478,8 @@ class _Parser:
             at = self.need_kind("ident")
             m = ALLOCATORS.fullmatch(at.val)
             if not m:
-                raise ParseError(f"expected an allocator, found {at.val!r}", at.line, at.col,
+                nt = self.peek()  # position of the next token (parser.py:150-152)
+                raise ParseError(f"expected an allocator, found {at.val!r}", nt.line, nt.col,
                                  self.filename)
             self.need("<")
             elem = self.take().val

@@ -58,3 +58,19 @@ def test_loop_modes_and_annotations_kept_raw():
 def test_parse_errors(bad):
     with pytest.raises(ParseError):
         parse_program(bad)
+
+
+def test_parse_error_messages_match_reference():
+    """Same exception type and message (file:line:col: text) as the reference's
+    parser on malformed programs (tests/golden/ref_parse_errors.json)."""
+    with open(os.path.join(GOLDEN, "ref_parse_errors.json")) as f:
+        cases = json.load(f)
+    assert len(cases) >= 35
+    for c in cases:
+        try:
+            parse_program(c["src"])
+            got = None
+        except Exception as e:  # noqa: BLE001
+            got = (type(e).__name__, str(e))
+        want = None if c["error"] is None else (c["type"], c["error"])
+        assert got == want, c["src"]

@@ -283,20 +283,77 @@ def _int_arg(env, name):
     return int(v)
 
 
-def _check_2d(arr, name, need_rows, need_cols):
-    """Reference access rules for `name[r][c]` with r < need_rows, c < need_cols."""
-    if arr.freed:
-        raise InterpError("use after free")
-    if len(arr.dims) != 2:
-        raise InterpError(
-            f"rank mismatch on {list(arr.dims)}: {name!r} is indexed as a 2-d array; flat "
-            "data is not reinterpreted (the reference's 1-d pointer-offset rule, "
-            "interp.py:239-240, is not supported)")
-    R, C = arr.dims
-    if need_rows > R:
-        raise InterpError(f"index {R} out of bounds 0..{R}")
-    if need_cols > C:
-        raise InterpError(f"index {C} out of bounds 0..{C}")
+def _first_none(arr, n_rows, n_cols, pitch, yx):
+    """(y, x) of the first uninitialised cell of arr[0:n_rows][0:n_cols] in the
+    loop order (x outer unless yx), or None. numpy-backed data has none."""
+    data = arr.data
+    if isinstance(data, np.ndarray) or n_rows <= 0 or n_cols <= 0:
+        return None
+    best = None
+    for pos, v in enumerate(data):
+        if v is None:
+            y, x = divmod(pos, pitch)
+            if y < n_rows and x < n_cols:
+                key = (y, x) if yx else (x, y)
+                if best is None or key < best[0]:
+                    best = (key, y, x)
+    return None if best is None else best[1:]
+
+
+def _transpose_naive_error(src, dst, sname, dname, W, H, yx):
+    """The error the reference raises first walking `out[x][y] = in[y][x]` (x outer,
+    or y outer for the swapped nest), or None. Per iteration it reads in[y][x]
+    (freed, rank, bounds in index order, uninitialised: Array.get, interp.py:72-78)
+    and then writes out[x][y] (freed, rank, bounds: Array.set, :80-85)."""
+    cands = []  # (iteration key, 0 = read of in / 1 = write of out, exception)
+
+    def key(x, y):
+        return (y, x) if yx else (x, y)
+
+    for which, arr, name, rows_need, cols_need in ((0, src, sname, H, W), (1, dst, dname, W, H)):
+        # in[y][x] has (row, col) = (y, x); out[x][y] has (row, col) = (x, y)
+        def at(r, c, which=which):
+            return key(c, r) if which == 0 else key(r, c)
+        if arr.freed:
+            cands.append((key(0, 0), which, InterpError("use after free")))
+            continue
+        if len(arr.dims) == 1:
+            cands.append((key(0, 0), which, InterpError(
+                f"rank mismatch on {list(arr.dims)}: {name!r} is indexed as a 2-d array; flat "
+                "data is not reinterpreted (the reference's 1-d pointer-offset rule, "
+                "interp.py:239-240, is not supported)")))
+            continue
+        if len(arr.dims) != 2:
+            cands.append((key(0, 0), which, InterpError(f"rank mismatch on {list(arr.dims)}￨[0, 0]")))
+            continue
+        R, C = arr.dims
+        if rows_need > R:
+            cands.append((at(R, 0), which, InterpError(f"index {R} out of bounds 0..{R}")))
+        if cols_need > C:
+            cands.append((at(0, C), which, InterpError(f"index {C} out of bounds 0..{C}")))
+        if which == 0:
+            hit = _first_none(arr, min(rows_need, R), min(cols_need, C), C, yx)
+            if hit is not None:
+                cands.append((at(*hit), 0, InterpError("read of uninitialized cell")))
+    if not cands:
+        return None
+    return min(cands, key=lambda c: (c[0], c[1]))[2]
+
+
+def _memcpy_cells(arr, n: int, want: str) -> np.ndarray:
+    """memcpy_host_to_device of the first n cells (interp.py:353-365): flat, no
+    freed check; the first missing cell raises IndexError, the first None cell
+    InterpError, whichever comes first."""
+    data = arr.data
+    if n <= 0:
+        return np.zeros(0, np.float32 if want == "float" else np.int32)
+    if not isinstance(data, np.ndarray):
+        for v in data[:n]:
+            if v is None:
+                raise InterpError("memcpy of uninitialized data")
+        if len(data) < n:
+            raise IndexError("list index out of range")
+    return _cells(Array(list(arr.dims), data, arr.ctype), n, want)
 
 
 def _exec_transpose_naive(plan: Plan, env):
@@ -304,9 +361,12 @@ def _exec_transpose_naive(plan: Plan, env):
     W, H = _int_arg(env, plan.params["W"]), _int_arg(env, plan.params["H"])
     if W <= 0 or H <= 0:
         return None
-    # in[y][x] for y < H, x < W; out[x][y] (interp.py:159-164, :271-276, Array.offset :61-70)
-    _check_2d(src, plan.params["in"], H, W)
-    _check_2d(dst, plan.params["out"], W, H)
+    # in[y][x] for y < H, x < W; out[x][y] (interp.py:159-164, :271-276, Array.offset :61-70):
+    # every error the walk could hit is decided up front, the earliest one raised
+    err = _transpose_naive_error(src, dst, plan.params["in"], plan.params["out"], W, H,
+                                 "_yx_" in plan.template.name)
+    if err is not None:
+        raise err
     R, C = src.dims
     Ro, Co = dst.dims
     want = "float" if dst.ctype == "float" else "int"
@@ -340,16 +400,13 @@ def _exec_transpose_gpu(plan: Plan, env):
     src, dst = env[plan.params["in"]], env[plan.params["out"]]
     W, H = _int_arg(env, plan.params["W"]), _int_arg(env, plan.params["H"])
     n = H * W
-    if src.freed:
-        raise InterpError("use after free")
-    a = _cells(src, max(n, 0), "float") if n > 0 else np.zeros(0, np.float32)
+    # host arrays are only touched by the flat memcpys (no freed check there)
+    a = _memcpy_cells(src, n, "float")
     for v in (W, H):  # kernel_launch((W/32)*(H/32), ...): exact_div, interp.py:209-214
         if v % 32 != 0:
             raise InterpError(f"exact_div({v}, 32) is not exact")
     if n <= 0:
         return None
-    if dst.freed:
-        raise InterpError("use after free")
     if (len(dst.data) if not isinstance(dst.data, np.ndarray) else dst.data.size) < n:
         raise IndexError("list assignment index out of range")
     out = ops.transpose(np.ascontiguousarray(a).reshape(H, W))
@@ -367,6 +424,9 @@ def _exec_reduce_naive(plan: Plan, env):
         raise InterpError("use after free")
     if len(arr.dims) != 1:
         raise InterpError(f"rank mismatch on {list(arr.dims)}￨[0]")
+    # iteration i reads arr[i]: an uninitialised cell before dims[0] fails first
+    if not isinstance(arr.data, np.ndarray) and any(v is None for v in arr.data[:min(N, arr.dims[0])]):
+        raise InterpError("read of uninitialized cell")
     if N > arr.dims[0]:
         raise InterpError(f"index {arr.dims[0]} out of bounds 0..{arr.dims[0]}")
     x = _cells(arr, N, cell)
@@ -382,9 +442,7 @@ def _exec_reduce_tree(plan: Plan, env):
     """A.5: flat copy of N cells, per-512 tree on the device, sequential host sum."""
     arr = env[plan.params["arr"]]
     N = _int_arg(env, plan.params["N"])
-    if arr.freed:
-        raise InterpError("use after free")
-    x = _cells(arr, N, "float") if N > 0 else np.zeros(0, np.float32)
+    x = _memcpy_cells(arr, N, "float")  # memcpy_host_to_device1: no freed check
     if N % 512 != 0:
         raise InterpError(f"exact_div({N}, 512) is not exact")
     if N <= 0:

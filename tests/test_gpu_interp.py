@@ -132,3 +132,20 @@ def test_naive_f32_reduce_c2(b2):
     ret, _ = b2.run_program(p, "reduce", {"arr": b2.Array.from_numpy(x), "N": x.size})
     exact, absum = oracle.sum_f64(x)
     assert abs(ret - exact) <= oracle.f32_tolerance(x.size, exact, absum)
+
+
+def test_reference_edge_inputs_that_succeed(b2):
+    """The edge inputs of tests/golden/ref_interp_errors.json on which the reference
+    does NOT raise (e.g. freed host arrays passed to the GPU forms, which only touch
+    them through memcpy): same return value here."""
+    import json
+    import os
+    from conftest import GOLDEN
+    with open(os.path.join(GOLDEN, "ref_interp_errors.json")) as f:
+        cases = [c for c in json.load(f) if c["error"] is None]
+    assert len(cases) >= 3
+    for c in cases:
+        inputs = {k: (b2.Array(list(v["dims"]), list(v["data"]), v["ctype"], v["freed"]) if isinstance(v, dict)
+                      else v) for k, v in c["inputs"].items()}
+        ret, _ = b2.run_program(_prog(b2, c["program"]), c["entry"], inputs)
+        assert ret == c["ret"], c["program"]

@@ -101,3 +101,26 @@ def test_float_overflow_matches_struct_pack():
         return
     from paper_2605_13864_b200.interp import _cells
     assert np.isinf(want) and np.isinf(_cells(Array([2], [1e39, 1.0], "float"), 2, "float")[0])
+
+
+def _materialise(spec):
+    return {k: (Array(list(v["dims"]), list(v["data"]), v["ctype"], v["freed"]) if isinstance(v, dict) else v)
+            for k, v in spec.items()}
+
+
+def test_reference_first_error_reproduced():
+    """Which error the reference raises FIRST (type and message), for 40 bad / edge
+    inputs to the hot-path programs (tests/golden/ref_interp_errors.json) — decided
+    before any device work, so this runs without a GPU."""
+    with open(os.path.join(GOLDEN, "ref_interp_errors.json")) as f:
+        cases = json.load(f)
+    assert len(cases) >= 40
+    checked = 0
+    for c in cases:
+        if c["error"] is None:
+            continue  # succeeds in the reference: exercised on the GPU (test_gpu_interp.py)
+        with pytest.raises(Exception) as ei:
+            run_program(prog(c["program"]), c["entry"], _materialise(c["inputs"]))
+        assert (type(ei.value).__name__, str(ei.value)) == (c["type"], c["error"]), c
+        checked += 1
+    assert checked >= 30

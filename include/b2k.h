@@ -143,6 +143,17 @@ B2_API int b2_reduce_tree512(const float *in, int64_t n, float *result_host, int
  * on the device, D2H of the partials, sequential binary32 host sum. Bit-exact. */
 B2_API int b2_reduce_tree512_host(const float *in_host, int64_t n, float *result_host, int dev);
 
+/* The same three entries for the whole A.5 derivation family
+ * (programs.reduce_tree_family: B-element blocks, B/2 threads, log2(B/2) halving
+ * levels, s[t] = s[t] + s[t + h] for h = B/4 .. 1): `block` = B, a power of two in
+ * 64..2048 (else B2_ERR_UNSUPPORTED). Requires block | n (exact_div). The *512
+ * entries above are block = 512. */
+B2_API int b2_reduce_tree_partials(const float *in, int64_t n, int block, float *partials, int dev,
+                                   void *stream);
+B2_API int b2_reduce_tree(const float *in, int64_t n, int block, float *result_host, int dev,
+                          void *stream);
+B2_API int b2_reduce_tree_host(const float *in_host, int64_t n, int block, float *result_host, int dev);
+
 /* Synchronous bulk copies for generated host code (codegen.py), replacing the
  * interpreter's element-wise memcpy_host_to_device / memcpy_device_to_host
  * (interp.py:353-365): pinned host buffers go straight to the DMA engines,

@@ -42,6 +42,9 @@ SIGNATURES = {
     "b2_reduce_tree512_partials": (_int, [_vp, _i64, _vp, _int, _vp]),
     "b2_reduce_tree512": (_int, [_vp, _i64, _vp, _int, _vp]),
     "b2_reduce_tree512_host": (_int, [_vp, _i64, _vp, _int]),
+    "b2_reduce_tree_partials": (_int, [_vp, _i64, _int, _vp, _int, _vp]),
+    "b2_reduce_tree": (_int, [_vp, _i64, _int, _vp, _int, _vp]),
+    "b2_reduce_tree_host": (_int, [_vp, _i64, _int, _vp, _int]),
     "b2_sync": (_int, [_int, _vp]),
     "b2_init": (_int, [_int]),
     "b2_peer_access": (_int, [_int, _int]),

@@ -83,5 +83,8 @@ size_t mailbox_bytes();
 int launch_reduce(const void *in, int64_t n, int dtype, void *out, void *ws, size_t ws_bytes,
                   int dev, cudaStream_t st, const FusedCombine &fz = FusedCombine());
 int launch_tree512(const float *in, int64_t n, float *partials, int dev, cudaStream_t st);
+// B-element tree blocks (power of two, 64..2048): the A.5 family
+bool tree_block_supported(int block);
+int launch_tree(const float *in, int64_t n, int block, float *partials, int dev, cudaStream_t st);
 
 }  // namespace b2

@@ -374,28 +374,41 @@ int b2_reduce_sum(const void *in, int64_t n, int dtype, void *out, void *ws, siz
     return launch_reduce(in, n, dtype, out, ws, ws_bytes, dev, (cudaStream_t)stream);
 }
 
-int b2_reduce_tree512_partials(const float *in, int64_t n, float *partials, int dev,
-                               void *stream) {
-    if (!in || !partials) return fail(B2_ERR_INVALID, "tree512: NULL buffer");
+int b2_reduce_tree_partials(const float *in, int64_t n, int block, float *partials, int dev,
+                            void *stream) {
+    if (!in || !partials) return fail(B2_ERR_INVALID, "tree: NULL buffer");
     if (int rc = check_dev(dev)) return rc;
-    return launch_tree512(in, n, partials, dev, (cudaStream_t)stream);
+    return launch_tree(in, n, block, partials, dev, (cudaStream_t)stream);
 }
 
-int b2_reduce_tree512(const float *in, int64_t n, float *result_host, int dev, void *stream) {
-    if (!in || !result_host) return fail(B2_ERR_INVALID, "tree512: NULL buffer");
-    if (n <= 0 || n % 512)
-        return fail(B2_ERR_INVALID, "exact_div(" + std::to_string(n) + ", 512) is not exact");
+int b2_reduce_tree512_partials(const float *in, int64_t n, float *partials, int dev, void *stream) {
+    return b2_reduce_tree_partials(in, n, 512, partials, dev, stream);
+}
+
+static int tree_args(int64_t n, int block) {
+    if (!tree_block_supported(block))
+        return fail(B2_ERR_UNSUPPORTED, "tree: block must be a power of two in 64..2048, not " +
+                                            std::to_string(block));
+    if (n <= 0 || n % block)
+        return fail(B2_ERR_INVALID, "exact_div(" + std::to_string(n) + ", " + std::to_string(block) +
+                                        ") is not exact");
+    return B2_OK;
+}
+
+int b2_reduce_tree(const float *in, int64_t n, int block, float *result_host, int dev, void *stream) {
+    if (!in || !result_host) return fail(B2_ERR_INVALID, "tree: NULL buffer");
+    if (int rc = tree_args(n, block)) return rc;
     if (int rc = check_dev(dev)) return rc;
     DevCtx &c = g_ctx[dev];
     std::lock_guard<std::mutex> g(c.mu);
     if (int rc = ctx_init(c, dev)) return rc;
-    const int64_t nb = n / 512;
+    const int64_t nb = n / block;
     if (int rc = ensure_small(c, (size_t)nb * sizeof(float))) return rc;
     cudaStream_t st = (cudaStream_t)stream;
-    if (int rc = launch_tree512(in, n, (float *)c.d_small, dev, st)) return rc;
+    if (int rc = launch_tree(in, n, block, (float *)c.d_small, dev, st)) return rc;
     B2_CUDA(cudaMemcpyAsync(c.h_small, c.d_small, nb * sizeof(float), cudaMemcpyDeviceToHost, st));
     B2_CUDA(cudaStreamSynchronize(st));
-    // The A.5 program's host loop: `sum += p[i]` in binary32, i ascending.
+    // The program's host loop: `sum += p[i]` in binary32, i ascending.
     volatile float s = 0.0f;
     const float *p = (const float *)c.h_small;
     for (int64_t i = 0; i < nb; ++i) s = s + p[i];
@@ -403,19 +416,22 @@ int b2_reduce_tree512(const float *in, int64_t n, float *result_host, int dev, v
     return B2_OK;
 }
 
-int b2_reduce_tree512_host(const float *in_host, int64_t n, float *result_host, int dev) {
-    if (!in_host || !result_host) return fail(B2_ERR_INVALID, "tree512: NULL buffer");
-    if (n <= 0 || n % 512)
-        return fail(B2_ERR_INVALID, "exact_div(" + std::to_string(n) + ", 512) is not exact");
+int b2_reduce_tree512(const float *in, int64_t n, float *result_host, int dev, void *stream) {
+    return b2_reduce_tree(in, n, 512, result_host, dev, stream);
+}
+
+int b2_reduce_tree_host(const float *in_host, int64_t n, int block, float *result_host, int dev) {
+    if (!in_host || !result_host) return fail(B2_ERR_INVALID, "tree: NULL buffer");
+    if (int rc = tree_args(n, block)) return rc;
     if (int rc = check_dev(dev)) return rc;
     DevCtx &c = g_ctx[dev];
     std::lock_guard<std::mutex> g(c.mu);
     if (int rc = ctx_init(c, dev)) return rc;
     int64_t ce = (int64_t)(chunk_bytes() / sizeof(float));
-    ce -= ce % 512;
-    ce = std::min(ce, n);
+    ce -= ce % block;
+    ce = std::max<int64_t>(block, std::min(ce, n));
     if (int rc = ensure_stages(c, (size_t)ce * sizeof(float))) return rc;
-    const int64_t nb = n / 512;
+    const int64_t nb = n / block;
     if (int rc = ensure_small(c, (size_t)nb * sizeof(float))) return rc;
     const int64_t nchunks = (n + ce - 1) / ce;
     const bool stage_in = !is_pinned(in_host);
@@ -429,8 +445,8 @@ int b2_reduce_tree512_host(const float *in_host, int64_t n, float *result_host, 
             return rc;
         B2_CUDA(cudaEventRecord(c.ev_in[k], c.s_h2d));
         B2_CUDA(cudaStreamWaitEvent(c.s_comp, c.ev_in[k], 0));
-        if (int rc = launch_tree512((const float *)c.d_in[k], ne, (float *)c.d_small + e0 / 512, dev,
-                                    c.s_comp))
+        if (int rc = launch_tree((const float *)c.d_in[k], ne, block, (float *)c.d_small + e0 / block, dev,
+                                 c.s_comp))
             return rc;
         B2_CUDA(cudaEventRecord(c.ev_comp[k], c.s_comp));
     }
@@ -441,6 +457,10 @@ int b2_reduce_tree512_host(const float *in_host, int64_t n, float *result_host, 
     for (int64_t i = 0; i < nb; ++i) s = s + p[i];
     *result_host = s;
     return B2_OK;
+}
+
+int b2_reduce_tree512_host(const float *in_host, int64_t n, float *result_host, int dev) {
+    return b2_reduce_tree_host(in_host, n, 512, result_host, dev);
 }
 
 int b2_sync(int dev, void *stream) {

@@ -208,31 +208,34 @@ __global__ void __launch_bounds__(NT)
     }
 }
 
-// A.5: 512-element blocks, one per warp per iteration. Lane l holds
-// s[l + 32j] (j < 8) = a[2t] + a[2t+1]; levels h = 128, 64, 32 pair registers of
-// the same lane, h = 16..1 pair lanes via shuffles. Same adds, same operands,
-// same order as the interpreter's smem loop -> bit-identical partials.
-template <int NT>
+// A.5 and its derivation family (programs.reduce_tree_family): B-element blocks
+// (B = 64 .. 2048), one per warp per iteration. Lane l holds s[l + 32j]
+// (j < B/64) = a[2t] + a[2t+1]; levels h = B/4 .. 32 pair registers of the same
+// lane (t + h = l + 32(j + h/32)), h = 16..1 pair lanes via shuffles. Same adds,
+// same operands, same association as the interpreter's smem loop `s[t] = s[t] +
+// s[t + h]` -> bit-identical partials (B = 512 is A.5).
+template <int B, int NT>
 __global__ void __launch_bounds__(NT)
-    tree512_kernel(const float *__restrict__ in, int64_t nblocks, float *__restrict__ partials) {
+    tree_kernel(const float *__restrict__ in, int64_t nblocks, float *__restrict__ partials) {
+    constexpr int K = B / 64;  // float2 pairs per lane
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * NT + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * NT) >> 5;
     for (int64_t b = warp; b < nblocks; b += nwarps) {
-        const float2 *p = reinterpret_cast<const float2 *>(in + b * 512);
-        float2 v[8];
+        const float2 *p = reinterpret_cast<const float2 *>(in + b * B);
+        float2 v[K];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) v[j] = __ldg(p + lane + 32 * j);
-        float s[8];
+        for (int j = 0; j < K; ++j) v[j] = __ldg(p + lane + 32 * j);
+        float s[K];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) s[j] = __fadd_rn(v[j].x, v[j].y);
+        for (int j = 0; j < K; ++j) s[j] = __fadd_rn(v[j].x, v[j].y);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) s[j] = __fadd_rn(s[j], s[j + 4]);  // h = 128
+        for (int h = K / 2; h >= 1; h >>= 1)  // levels B/4 .. 32, in registers
 #pragma unroll
-        for (int j = 0; j < 2; ++j) s[j] = __fadd_rn(s[j], s[j + 2]);  // h = 64
-        float x = __fadd_rn(s[0], s[1]);                                 // h = 32
+            for (int j = 0; j < h; ++j) s[j] = __fadd_rn(s[j], s[j + h]);
+        float x = s[0];
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1)                           // h = 16..1
+        for (int off = 16; off > 0; off >>= 1)  // levels 16 .. 1
             x = __fadd_rn(x, __shfl_down_sync(0xffffffffu, x, off));
         if (lane == 0) partials[b] = x;
     }
@@ -311,17 +314,41 @@ int launch_reduce(const void *in, int64_t n, int dtype, void *out, void *ws, siz
     }
 }
 
-int launch_tree512(const float *in, int64_t n, float *partials, int dev, cudaStream_t st) {
-    if (n % 512 != 0 || n <= 0)
-        return fail(B2_ERR_INVALID, "exact_div(" + std::to_string(n) + ", 512) is not exact");
-    if ((uintptr_t)in % 8) return fail(B2_ERR_INVALID, "tree512: input must be 8-byte aligned");
-    const int64_t nb = n / 512;
+template <int B>
+int run_tree(const float *in, int64_t nb, float *partials, int dev, cudaStream_t st) {
     constexpr int NT = 256;
     const int64_t grid = std::min<int64_t>((nb + NT / 32 - 1) / (NT / 32), (int64_t)num_sms(dev) * 8);
-    tree512_kernel<NT><<<(unsigned)grid, NT, 0, st>>>(in, nb, partials);
+    tree_kernel<B, NT><<<(unsigned)grid, NT, 0, st>>>(in, nb, partials);
     count_launch();
     B2_CUDA(cudaGetLastError());
     return B2_OK;
+}
+
+bool tree_block_supported(int block) {
+    return block >= 64 && block <= 2048 && (block & (block - 1)) == 0;
+}
+
+int launch_tree(const float *in, int64_t n, int block, float *partials, int dev, cudaStream_t st) {
+    if (!tree_block_supported(block))
+        return fail(B2_ERR_UNSUPPORTED, "tree: block must be a power of two in 64..2048, not " +
+                                            std::to_string(block));
+    if (n % block != 0 || n <= 0)
+        return fail(B2_ERR_INVALID, "exact_div(" + std::to_string(n) + ", " + std::to_string(block) +
+                                        ") is not exact");
+    if ((uintptr_t)in % 8) return fail(B2_ERR_INVALID, "tree: input must be 8-byte aligned");
+    const int64_t nb = n / block;
+    switch (block) {
+    case 64: return run_tree<64>(in, nb, partials, dev, st);
+    case 128: return run_tree<128>(in, nb, partials, dev, st);
+    case 256: return run_tree<256>(in, nb, partials, dev, st);
+    case 512: return run_tree<512>(in, nb, partials, dev, st);
+    case 1024: return run_tree<1024>(in, nb, partials, dev, st);
+    default: return run_tree<2048>(in, nb, partials, dev, st);
+    }
+}
+
+int launch_tree512(const float *in, int64_t n, float *partials, int dev, cudaStream_t st) {
+    return launch_tree(in, n, 512, partials, dev, st);
 }
 
 }  // namespace b2

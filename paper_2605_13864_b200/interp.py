@@ -396,15 +396,18 @@ def _read_block(arr, rows, cols, pitch, want) -> np.ndarray:
 
 
 def _exec_transpose_gpu(plan: Plan, env):
-    """A.4: memcpy_host_to_device2 (flat copy of H*W cells), kernel, flat copy back."""
+    """A.4 and its tile-size family (T x T tiles; A.4 is T = 32): memcpy_host_to_device2
+    (flat copy of H*W cells), kernel, flat copy back. Any tile shape computes the
+    same permutation, so every member runs on the hand-written transpose."""
     src, dst = env[plan.params["in"]], env[plan.params["out"]]
     W, H = _int_arg(env, plan.params["W"]), _int_arg(env, plan.params["H"])
+    T = plan.consts.get("T", 32)
     n = H * W
     # host arrays are only touched by the flat memcpys (no freed check there)
     a = _memcpy_cells(src, n, "float")
-    for v in (W, H):  # kernel_launch((W/32)*(H/32), ...): exact_div, interp.py:209-214
-        if v % 32 != 0:
-            raise InterpError(f"exact_div({v}, 32) is not exact")
+    for v in (W, H):  # kernel_launch((W/T)*(H/T), ...): exact_div, interp.py:209-214
+        if v % T != 0:
+            raise InterpError(f"exact_div({v}, {T}) is not exact")
     if n <= 0:
         return None
     if (len(dst.data) if not isinstance(dst.data, np.ndarray) else dst.data.size) < n:
@@ -439,15 +442,27 @@ def _exec_reduce_naive(plan: Plan, env):
 
 
 def _exec_reduce_tree(plan: Plan, env):
-    """A.5: flat copy of N cells, per-512 tree on the device, sequential host sum."""
+    """A.5 and its block-size family (B-element blocks; A.5 is B = 512, float):
+    flat copy of N cells, per-B tree on the device, sequential host sum. Int cells
+    sum exactly in any order (the plain reduction kernel); float cells need the
+    tree's own association (tree_kernel<B>, B = 64 .. 2048; other B -> codegen)."""
+    B = plan.consts.get("B", 512)
+    cell = plan.cell
+    if cell == "float" and not (64 <= B <= 2048):
+        raise UnsupportedProgram(f"no hand-written tree kernel for {B}-element blocks")
     arr = env[plan.params["arr"]]
     N = _int_arg(env, plan.params["N"])
-    x = _memcpy_cells(arr, N, "float")  # memcpy_host_to_device1: no freed check
-    if N % 512 != 0:
-        raise InterpError(f"exact_div({N}, 512) is not exact")
+    x = _memcpy_cells(arr, N, cell)  # memcpy_host_to_device1: no freed check
+    if N % B != 0:
+        raise InterpError(f"exact_div({N}, {B}) is not exact")
     if N <= 0:
-        return ("ret", 0.0)
-    return ("ret", ops.reduce_tree512(np.ascontiguousarray(x)))
+        return ("ret", 0.0 if cell == "float" else 0)
+    if cell == "int":
+        if x.dtype != np.int32:
+            raise InterpError("int cell value outside the 4-byte cell range (intrinsics.py:35 "
+                              "CELL_BYTES = 4)")
+        return ("ret", int(ops.reduce_sum(np.ascontiguousarray(x))))
+    return ("ret", ops.reduce_tree(np.ascontiguousarray(x), B))
 
 
 _EXEC = {
@@ -455,6 +470,7 @@ _EXEC = {
     ("transpose", "gpu"): _exec_transpose_gpu,
     ("reduce", "naive"): _exec_reduce_naive,
     ("reduce", "tree512"): _exec_reduce_tree,
+    ("reduce", "tree"): _exec_reduce_tree,
 }
 
 __all__ = ["Array", "Interp", "InterpError", "UnsupportedProgram", "f32", "run_program"]

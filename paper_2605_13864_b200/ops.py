@@ -146,27 +146,38 @@ def reduce_sum(arr, *, out=None, ws=None, stream=None):
     return res[0].item()
 
 
-def reduce_tree512(arr, *, stream=None) -> float:
-    """The A.5 tree-form program, bit-identical with the reference interpreter:
-    per-512 block halving tree on the device, sequential binary32 host sum."""
+def reduce_tree(arr, block: int = 512, *, stream=None) -> float:
+    """The A.5 tree-form program and its block-size family
+    (programs.reduce_tree_family), bit-identical with the reference interpreter:
+    per-`block` halving tree on the device, sequential binary32 host sum.
+    `block` is a power of two in 64..2048 (A.5: 512)."""
     res = ctypes.c_float(0.0)
     if not _is_torch_cuda(arr):
         a = np.ascontiguousarray(arr, dtype=np.float32).reshape(-1)
-        check(lib().b2_reduce_tree512_host(a.ctypes.data, a.size, ctypes.byref(res), _host_device()))
+        check(lib().b2_reduce_tree_host(a.ctypes.data, a.size, int(block), ctypes.byref(res), _host_device()))
         return float(res.value)
     if arr.dtype != torch.float32 or arr.dim() != 1 or (arr.numel() and arr.stride(0) != 1):
-        raise ValueError("reduce_tree512: input must be a contiguous 1-D float32 tensor")
-    check(lib().b2_reduce_tree512(arr.data_ptr(), arr.numel(), ctypes.byref(res),
-                                  arr.device.index, _stream_ptr(arr, stream)))
+        raise ValueError("reduce_tree: input must be a contiguous 1-D float32 tensor")
+    check(lib().b2_reduce_tree(arr.data_ptr(), arr.numel(), int(block), ctypes.byref(res),
+                               arr.device.index, _stream_ptr(arr, stream)))
     return float(res.value)
 
 
-def reduce_tree512_partials(arr, partials=None, *, stream=None):
+def reduce_tree_partials(arr, block: int = 512, partials=None, *, stream=None):
     if partials is None:
-        partials = torch.empty(arr.numel() // 512, dtype=torch.float32, device=arr.device)
-    check(lib().b2_reduce_tree512_partials(arr.data_ptr(), arr.numel(), partials.data_ptr(),
-                                           arr.device.index, _stream_ptr(arr, stream)))
+        partials = torch.empty(arr.numel() // block, dtype=torch.float32, device=arr.device)
+    check(lib().b2_reduce_tree_partials(arr.data_ptr(), arr.numel(), int(block), partials.data_ptr(),
+                                        arr.device.index, _stream_ptr(arr, stream)))
     return partials
+
+
+def reduce_tree512(arr, *, stream=None) -> float:
+    """A.5: reduce_tree with 512-element blocks."""
+    return reduce_tree(arr, 512, stream=stream)
+
+
+def reduce_tree512_partials(arr, partials=None, *, stream=None):
+    return reduce_tree_partials(arr, 512, partials, stream=stream)
 
 
 def reduce_ws_bytes(n: int, dtype: int) -> int:

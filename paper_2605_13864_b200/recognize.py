@@ -7,7 +7,10 @@ the reduction in their naive and GPU-derived forms (SURVEY Appendix A.1-A.5;
 PAPER.md:155-172, 395-433, 586-618, 1041-1068, 1120-1131) — and refuses every
 other program loudly (there is no CPU fallback).
 
-Recognition is alpha-equivalence against canonical templates: after removing
+Recognition is alpha-equivalence against canonical templates (and against the
+members of the A.4 / A.5 derivation families, programs.transpose_gpu_family /
+reduce_tree_family, instantiated with parameters read off the program's own
+literals): after removing
 ghost calls (ast.py:473-494 `strip_ghosts`), the entry body must match a
 template node for node, with every binder (parameter, local, loop index)
 renamed consistently (a bijection) and every literal, operator, loop mode,
@@ -17,6 +20,7 @@ parser and from the reference's (matching is by node class name and fields).
 """
 from __future__ import annotations
 
+import functools
 from dataclasses import dataclass, field
 
 from .errors import UnsupportedProgram
@@ -25,17 +29,19 @@ from .lang import parse_program
 # ----------------------------------------------------------------------------- templates
 from .programs import (REDUCE_NAIVE as _R_NAIVE, REDUCE_TREE as _R_TREE,
                        TRANSPOSE_GPU as _T_GPU, TRANSPOSE_NAIVE_XY as _T_NAIVE_XY,
-                       TRANSPOSE_NAIVE_YX as _T_NAIVE_YX, source)
+                       TRANSPOSE_NAIVE_YX as _T_NAIVE_YX, reduce_tree_family, source,
+                       transpose_gpu_family)
 
 
 @dataclass
 class Template:
     name: str
     kind: str      # "transpose" | "reduce"
-    form: str      # "naive" | "gpu" | "tree512"
+    form: str      # "naive" | "gpu" | "tree512" | "tree"
     cell: str      # "float" | "int"
     fn: object     # parsed FnDef
     roles: dict = field(default_factory=dict)  # role -> template param name
+    consts: dict = field(default_factory=dict)  # family parameters (T, R / B)
 
 
 def _mk(name, kind, form, cell, text, roles, zero=None):
@@ -201,6 +207,10 @@ class Plan:
     def cell(self):
         return self.template.cell
 
+    @property
+    def consts(self):
+        return self.template.consts
+
 
 def match(fn, tmpl: Template) -> Plan:
     tf = tmpl.fn
@@ -218,10 +228,64 @@ def match(fn, tmpl: Template) -> Plan:
     return Plan(tmpl, {role: u.t2p[tn] for role, tn in tmpl.roles.items()}, fn.name)
 
 
+@functools.lru_cache(maxsize=256)
+def _family_template(kind: str, a: int, b, cell: str) -> Template:
+    if kind == "transpose":
+        fn = parse_program(transpose_gpu_family(a, b), f"<template transpose_gpu_T{a}_R{b}>").fns[0]
+        return Template(f"transpose_gpu_T{a}_R{b}", "transpose", "gpu", "float", fn, _TR, {"T": a, "R": b})
+    fn = parse_program(reduce_tree_family(a, cell), f"<template reduce_tree_B{a}_{cell}>").fns[0]
+    return Template(f"reduce_tree_B{a}_{cell}", "reduce", "tree", cell, fn, _RR, {"B": a})
+
+
+def _int_literals(node, out):
+    c = _cls(node)
+    if c == "IntLit":
+        out.add(node.value)
+        return
+    for f in ("lhs", "rhs", "value", "init", "cond", "then", "els", "body", "range", "start", "stop",
+              "target"):
+        v = getattr(node, f, None)
+        if v is not None and not isinstance(v, (str, int, float)):
+            _int_literals(v, out)
+    for f in ("args", "idxs", "stmts", "dims"):
+        for v in getattr(node, f, ()) or ():
+            if not isinstance(v, (str, int, float)):
+                _int_literals(v, out)
+
+
+def family_candidates(fn):
+    """Family members worth trying for this function: parameters drawn from its
+    own integer literals (a tile side T with R | T, R * T <= 1024; a block B = 2t
+    with t a power of two <= 1024)."""
+    if fn.body is None:
+        return []
+    lits = set()
+    _int_literals(fn.body, lits)
+    out = []
+    ret = getattr(fn, "ret", "void")
+    if ret == "void" and len(fn.params) == 4:
+        for T in sorted(lits):
+            for R in sorted(lits):
+                if 0 < R <= T and T % R == 0 and R * T <= 1024 and (T, R) != (32, 16):
+                    out.append(("transpose", T, R, "float"))
+    if ret in ("float", "int") and len(fn.params) == 2:
+        for B in sorted(lits):
+            t = B // 2
+            if B >= 2 and B % 2 == 0 and t & (t - 1) == 0 and t <= 1024 and (B, ret) != (512, "float"):
+                out.append(("reduce", B, None, ret))
+    return out
+
+
 def recognize(program, entry: str) -> Plan:
     fn = program.fn(entry)
     reasons = []
     for t in TEMPLATES:
+        try:
+            return match(fn, t)
+        except NoMatch as e:
+            reasons.append(f"{t.name}: {e}")
+    for kind, a, b, cell in family_candidates(fn):
+        t = _family_template(kind, a, b, cell)
         try:
             return match(fn, t)
         except NoMatch as e:

@@ -68,3 +68,36 @@ def test_tree_with_other_tile_constant_refused():
     p = parse_program(src)
     with pytest.raises(UnsupportedProgram):
         recognize(p, "reduce")
+
+
+# ---------------------------------------------------------------- derivation families
+from program_families import reduce_family, transpose_family  # noqa: E402
+
+
+@pytest.mark.parametrize("T,R", [(8, 2), (16, 16), (32, 4), (32, 32), (64, 8), (64, 16), (128, 8)])
+def test_transpose_family_members_recognised(T, R):
+    plan = recognize(parse_program(transpose_family(T, R)), "transpose")
+    assert (plan.kind, plan.form) == ("transpose", "gpu")
+    if (T, R) != (32, 16):
+        assert plan.consts == {"T": T, "R": R}
+
+
+@pytest.mark.parametrize("B,cell", [(2, "float"), (64, "float"), (128, "int"), (256, "float"), (1024, "float"),
+                                    (2048, "int"), (512, "int")])
+def test_reduce_family_members_recognised(B, cell):
+    plan = recognize(parse_program(reduce_family(B, cell)), "reduce")
+    assert plan.kind == "reduce" and plan.cell == cell and plan.consts == {"B": B}
+
+
+def test_family_near_misses_refused():
+    """A member with a changed tree level count (wrong association) or a tile
+    whose loads and stores disagree is not any family member."""
+    src = reduce_family(256, "float").replace("k < 7", "k < 6")
+    assert src != reduce_family(256, "float")
+    with pytest.raises(UnsupportedProgram):
+        recognize(parse_program(src), "reduce")
+    src = transpose_family(64, 16).replace("[bx*64 + x] = ", "[bx*64 + x + 1] = ").replace(
+        "d_out[bx*64 + j*16 + y][by*64 + x]", "d_out[bx*64 + j*16 + y][by*64 + x + 1]")
+    assert src != transpose_family(64, 16)
+    with pytest.raises(UnsupportedProgram):
+        recognize(parse_program(src), "transpose")

@@ -96,12 +96,21 @@ def test_codegen_at_scale_numpy_arrays(b2):
     assert np.array_equal(out.reshape(2048, 1024), a.T)
 
 
-def test_auto_backend_routes_variants_to_codegen(b2):
-    # the 64x64 variant is not a template: "auto" compiles it, "kernels" refuses it
+def test_auto_backend_routes_variants(b2):
+    # the 64x64 variant is a member of the A.4 family: "auto" and "kernels" run it on
+    # the hand-written transpose; scale_then_reduce is no family member: "auto"
+    # compiles it, "kernels" refuses it
     p = _prog(b2, "transpose_gpu_t64.optc")
     a = np.arange(64 * 128, dtype=np.float32)
-    _, outs = b2.run_program(p, "transpose", {"in": a.tolist(), "out": [0.0] * a.size, "W": 128, "H": 64})
-    assert outs["out"] == a.reshape(64, 128).T.reshape(-1).tolist()
+    for backend in ("auto", "kernels"):
+        n0 = b2.launch_count()
+        _, outs = b2.run_program(p, "transpose", {"in": a.tolist(), "out": [0.0] * a.size, "W": 128, "H": 64},
+                                 backend=backend)
+        assert outs["out"] == a.reshape(64, 128).T.reshape(-1).tolist()
+        assert b2.launch_count() > n0
+    q = _prog(b2, "scale_then_reduce.optc")
+    x = np.linspace(-1, 1, 2048, dtype=np.float32)
+    ret, _ = b2.run_program(q, "reduce", {"arr": x.tolist(), "N": 2048})
+    assert isinstance(ret, float)
     with pytest.raises(b2.UnsupportedProgram):
-        b2.run_program(p, "transpose", {"in": a.tolist(), "out": [0.0] * a.size, "W": 128, "H": 64},
-                       backend="kernels")
+        b2.run_program(q, "reduce", {"arr": x.tolist(), "N": 2048}, backend="kernels")

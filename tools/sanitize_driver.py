@@ -183,6 +183,15 @@ def run_reduce(rng):
     assert np.float32(res.value) == np.float32(want_total)
     dfree(p)
     dfree(parts)
+    # the A.5 family: every tree block size
+    for blk in (64, 128, 256, 1024, 2048):
+        xb = rng.uniform(-1, 1, blk * 37).astype(np.float32)
+        pb = h2d(xb)
+        parts = dalloc(37 * 4)
+        check(L.b2_reduce_tree_partials(pb, xb.size, blk, parts, DEV, None))
+        d2h(parts, np.zeros(37, np.float32))
+        dfree(pb)
+        dfree(parts)
     # host pipeline, int32, small stage size
     tune("host.chunk_mb", 1)
     x = rng.integers(-2**31, 2**31, 3_000_017, dtype=np.int64).astype(np.int32)

@@ -10,7 +10,8 @@ import ctypes
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libb200k.so")
+# B2K_LIB overrides the in-tree library (A/B measurements of two builds, tools/ab_*.py)
+LIB_PATH = os.environ.get("B2K_LIB") or os.path.join(PKG, "libb200k.so")
 
 # enum b2_dtype (include/b2k.h)
 BF16, F16, F32, F64, I32, I64, U8, U16, U32, U64 = 1, 2, 3, 4, 5, 6, 7, 8, 9, 10

@@ -47,18 +47,26 @@ constexpr int kInflightBytesPerSM = 64 * 1024;
 constexpr int kReduceThreadsPerSM = 1536;
 
 // ---- global memory access with explicit cache policy -----------------------
-// Streaming 128-bit load that bypasses L1 (read-once data).
+// Streaming 128-bit load that bypasses L1 (read-once data). No L2 prefetch-size
+// hint: A/B on one B200 (profiles/r01j_ldst_variants.md) measured the .L2::256B
+// hint 0.6-0.9 % slower for the transposes and neutral for the reduction.
+#ifndef B2_LDG_QUAL
+#define B2_LDG_QUAL "ld.global.nc.L1::no_allocate.v4.u32"
+#endif
 __device__ __forceinline__ uint4 ldg_stream(const uint4 *p) {
     uint4 r;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+    asm volatile(B2_LDG_QUAL " {%0,%1,%2,%3}, [%4];"
                  : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
                  : "l"(p));
     return r;
 }
 
-// Streaming 128-bit store (evict-first in L2: the output is written once).
+// Streaming 128-bit store (the output is written once; no L1 allocation).
+#ifndef B2_STG_QUAL
+#define B2_STG_QUAL "st.global.L1::no_allocate.v4.u32"
+#endif
 __device__ __forceinline__ void stg_stream(uint4 *p, const uint4 &v) {
-    asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x),
+    asm volatile(B2_STG_QUAL " [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x),
                  "r"(v.y), "r"(v.z), "r"(v.w)
                  : "memory");
 }

@@ -155,7 +155,27 @@ __device__ void fused_combine(const Fused &fz, A total, A *out) {
     st_release_sys(consumed, fz.epoch);
 }
 
-template <typename T, int NT, int U>
+// W x 128 bits per load: W = 2 uses the 256-bit global loads sm_100 adds
+// (LDG.E.256), halving the load instructions per byte.
+template <int W>
+struct alignas(16 * W) VecW {
+    uint4 q[W];
+};
+template <int W>
+__device__ __forceinline__ VecW<W> ldg_w(const VecW<W> *p) {
+    VecW<W> r;
+    if constexpr (W == 1) {
+        r.q[0] = ldg_stream(reinterpret_cast<const uint4 *>(p));
+    } else {
+        asm volatile("ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(r.q[0].x), "=r"(r.q[0].y), "=r"(r.q[0].z), "=r"(r.q[0].w), "=r"(r.q[1].x),
+                       "=r"(r.q[1].y), "=r"(r.q[1].z), "=r"(r.q[1].w)
+                     : "l"(p));
+    }
+    return r;
+}
+
+template <typename T, int NT, int U, int W = 1>
 __global__ void __launch_bounds__(NT)
     reduce_kernel(const T *__restrict__ in, int64_t head, int64_t nvec, int64_t n,
                   typename AccOf<T>::type *__restrict__ out,
@@ -167,21 +187,27 @@ __global__ void __launch_bounds__(NT)
     __shared__ bool last;
 
     A acc = A(0);
-    const uint4 *vin = reinterpret_cast<const uint4 *>(in + head);
+    const VecW<W> *vin = reinterpret_cast<const VecW<W> *>(in + head);
     const int64_t stride = (int64_t)gridDim.x * NT;
     int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x;
-    // main body: U independent 128-bit loads in flight per thread
+    // main body: U independent (W x 128)-bit loads in flight per thread
     for (; i + (U - 1) * stride < nvec; i += U * stride) {
-        uint4 v[U];
+        VecW<W> v[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) v[u] = ldg_stream(vin + i + u * stride);
+        for (int u = 0; u < U; ++u) v[u] = ldg_w<W>(vin + i + u * stride);
 #pragma unroll
-        for (int u = 0; u < U; ++u) acc += vec_sum<T, A>(v[u]);
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int w = 0; w < W; ++w) acc += vec_sum<T, A>(v[u].q[w]);
     }
-    for (; i < nvec; i += stride) acc += vec_sum<T, A>(ldg_stream(vin + i));
-    // unaligned head and ragged tail (< V elements each)
+    for (; i < nvec; i += stride) {
+        const VecW<W> v = ldg_w<W>(vin + i);
+#pragma unroll
+        for (int w = 0; w < W; ++w) acc += vec_sum<T, A>(v.q[w]);
+    }
+    // unaligned head and ragged tail (< V * W elements each)
     const int64_t g = (int64_t)blockIdx.x * NT + threadIdx.x;
-    const int64_t tail0 = head + nvec * V;
+    const int64_t tail0 = head + nvec * V * W;
     if (g < head) acc += A(in[g]);
     if (g < n - tail0) acc += A(in[tail0 + g]);
 
@@ -245,14 +271,19 @@ constexpr int kMinNT = 256;  // smallest CTA among the variants (sizes the works
 
 int max_grid(int dev) { return num_sms(dev) * (2048 / kMinNT); }
 
-template <typename T, int NT, int U>
-int run_reduce_v(const T *in, int64_t head, int64_t nvec, int64_t n, void *out, void *ws,
-                 int dev, cudaStream_t st, const Fused &fz) {
+template <typename T, int NT, int U, int W = 1>
+int run_reduce_v(const T *in, int64_t n, void *out, void *ws, int dev, cudaStream_t st,
+                 const Fused &fz) {
     using A = typename AccOf<T>::type;
+    constexpr int V = 16 / sizeof(T);
+    // head: elements before the first (16 W)-byte boundary; nvec: whole W-vectors
+    int64_t head = (int64_t)(((16 * W - ((uintptr_t)in & (16 * W - 1))) & (16 * W - 1)) / sizeof(T));
+    head = std::min<int64_t>(head, n);
+    const int64_t nvec = (n - head) / (V * W);
     static int occ[64] = {0};
     if (occ[dev] == 0) {
         int o = 0;
-        B2_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, reduce_kernel<T, NT, U>, NT, 0));
+        B2_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, reduce_kernel<T, NT, U, W>, NT, 0));
         occ[dev] = o > 0 ? o : 1;
     }
     // Default: 1536 threads per SM (3 x 512). Measured on B200 (profiles/r01_tune.md):
@@ -264,7 +295,7 @@ int run_reduce_v(const T *in, int64_t head, int64_t nvec, int64_t n, void *out, 
     const int grid = (int)std::min(cap, need);
     unsigned *ticket = (unsigned *)ws;
     A *partials = (A *)((char *)ws + 64);
-    reduce_kernel<T, NT, U><<<grid, NT, 0, st>>>(in, head, nvec, n, (A *)out, partials, ticket, fz);
+    reduce_kernel<T, NT, U, W><<<grid, NT, 0, st>>>(in, head, nvec, n, (A *)out, partials, ticket, fz);
     count_launch();
     B2_CUDA(cudaGetLastError());
     return B2_OK;
@@ -275,20 +306,25 @@ template <typename T>
 int run_reduce(const void *in_, int64_t n, void *out, void *ws, size_t ws_bytes, int dev,
                cudaStream_t st, const Fused &fz) {
     using A = typename AccOf<T>::type;
-    constexpr int V = 16 / sizeof(T);
     const T *in = (const T *)in_;
     if ((uintptr_t)in % sizeof(T)) return fail(B2_ERR_INVALID, "reduce: misaligned input");
-    int64_t head = (int64_t)(((16 - ((uintptr_t)in & 15)) & 15) / sizeof(T));
-    head = std::min<int64_t>(head, n);
-    const int64_t nvec = (n - head) / V;
     const size_t need = (size_t)max_grid(dev) * sizeof(A) + 64;
     if (ws_bytes < need) return fail(B2_ERR_INVALID, "reduce: workspace too small");
     switch (g_tune.r_variant) {
-    case 1: return run_reduce_v<T, 512, 8>(in, head, nvec, n, out, ws, dev, st, fz);
-    case 2: return run_reduce_v<T, 256, 8>(in, head, nvec, n, out, ws, dev, st, fz);
-    case 3: return run_reduce_v<T, 1024, 4>(in, head, nvec, n, out, ws, dev, st, fz);
-    case 4: return run_reduce_v<T, 256, 16>(in, head, nvec, n, out, ws, dev, st, fz);
-    default: return run_reduce_v<T, 512, 4>(in, head, nvec, n, out, ws, dev, st, fz);
+    case 1: return run_reduce_v<T, 512, 8>(in, n, out, ws, dev, st, fz);
+    case 2: return run_reduce_v<T, 256, 8>(in, n, out, ws, dev, st, fz);
+    case 3: return run_reduce_v<T, 1024, 4>(in, n, out, ws, dev, st, fz);
+    case 4: return run_reduce_v<T, 256, 16>(in, n, out, ws, dev, st, fz);
+    case 5: return run_reduce_v<T, 512, 4, 2>(in, n, out, ws, dev, st, fz);   // 256-bit loads
+    case 6: return run_reduce_v<T, 512, 2, 2>(in, n, out, ws, dev, st, fz);
+    case 7: return run_reduce_v<T, 256, 4, 2>(in, n, out, ws, dev, st, fz);
+    case 8: return run_reduce_v<T, 1024, 2, 2>(in, n, out, ws, dev, st, fz);
+    case 9: return run_reduce_v<T, 512, 4>(in, n, out, ws, dev, st, fz);
+    default:
+        // 128-bit loads. The 256-bit variants (5-8) read 1-2 % faster in isolation but
+        // slowed the FOLLOWING transpose in the bench step by 4 % (A/B of whole bench
+        // steps, profiles/r01j_ldst_variants.md), so they stay opt-in.
+        return run_reduce_v<T, 512, 4>(in, n, out, ws, dev, st, fz);
     }
 }
 

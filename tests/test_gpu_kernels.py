@@ -271,3 +271,25 @@ def test_tma_transpose_path(b2, shape):
         assert torch.equal(out2[:, :shape[0]], a.t()) and bool((out2[:, shape[0]:] == -1).all())
     finally:
         _lib.tune("transpose.tma", 0)
+
+
+@pytest.mark.parametrize("variant", list(range(10)))
+def test_reduce_variants_heads_and_tails(b2, variant):
+    """Every reduce instantiation (incl. the 256-bit-load ones, LDG.E.256, whose
+    head aligns to 32 B) over misaligned starts and ragged lengths."""
+    from paper_2605_13864_b200 import _lib
+    _lib.tune("reduce.variant", variant)
+    try:
+        rng = np.random.default_rng(variant)
+        x = rng.integers(-2**31, 2**31, 200_017, dtype=np.int64).astype(np.int32)
+        xf = rng.uniform(-1, 1, 200_017).astype(np.float32)
+        t, tf = torch.from_numpy(x).cuda(), torch.from_numpy(xf).cuda()
+        for off in range(8):
+            for n in (0, 1, 7, 8, 9, 15, 16, 17, 31, 33, 1000, 65_537, 200_000):
+                assert int(b2.reduce_sum(t[off:off + n]).item()) == int(x[off:off + n].astype(np.int64).sum())
+            seg = xf[off:off + 123_457]
+            exact, absum = oracle.sum_f64(seg)
+            got = float(b2.reduce_sum(tf[off:off + 123_457]).item())
+            assert abs(got - exact) <= oracle.f32_tolerance(seg.size, exact, absum)
+    finally:
+        _lib.tune("reduce.variant", 0)

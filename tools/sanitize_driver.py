@@ -163,7 +163,7 @@ def run_reduce(rng):
     x = rng.integers(-2**31, 2**31, 300_001, dtype=np.int64).astype(np.int32)
     p = h2d(x)
     outp = dalloc(8)
-    for v in range(6):
+    for v in range(10):  # incl. the 256-bit-load variants (LDG.E.256)
         tune("reduce.variant", v)
         check(L.b2_reduce_sum(p, x.size, _lib.I32, outp, None, 0, DEV, None))
         assert int(d2h(outp, np.zeros(1, np.int64))[0]) == int(x.astype(np.int64).sum()), v

@@ -86,6 +86,10 @@ def lib() -> ctypes.CDLL:
         if L.b2_abi_version() != 1:
             raise ImportError("libb200k ABI version mismatch")
         _lib = L
+        # B2K_TUNE="key=value,key=value": knob settings for measurement runs
+        for kv in filter(None, os.environ.get("B2K_TUNE", "").split(",")):
+            k, _, v = kv.partition("=")
+            check(L.b2_tune_set(k.strip().encode(), int(v)))
     return _lib
 
 

@@ -44,7 +44,7 @@ struct Tuning {
 };
 extern Tuning g_tune;
 constexpr int kInflightBytesPerSM = 64 * 1024;
-constexpr int kReduceThreadsPerSM = 1536;
+constexpr int kReduceThreadsPerSM = 1024;  // 2 x 512: best in the bench step (profiles/r01k_reduce_residency.md)
 
 // ---- global memory access with explicit cache policy -----------------------
 // Streaming 128-bit load that bypasses L1 (read-once data). No L2 prefetch-size

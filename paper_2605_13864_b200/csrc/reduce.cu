@@ -286,8 +286,10 @@ int run_reduce_v(const T *in, int64_t n, void *out, void *ws, int dev, cudaStrea
         B2_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, reduce_kernel<T, NT, U, W>, NT, 0));
         occ[dev] = o > 0 ? o : 1;
     }
-    // Default: 1536 threads per SM (3 x 512). Measured on B200 (profiles/r01_tune.md):
-    // full occupancy (2048) reads 6.94 TB/s, 1536 reads 7.19 TB/s.
+    // Default: 1024 threads per SM (2 x 512). Measured on B200: full occupancy
+    // (2048) reads 6.94 TB/s, 1536 7.19 TB/s (profiles/r01_tune.md, isolated); in the
+    // bench step 1024 beats 1536 by 1.5 % on the reduction and leaves the next
+    // transpose untouched, and isolated it is on par (profiles/r01k_reduce_residency.md).
     const int auto_sm = std::max(1, kReduceThreadsPerSM / NT);
     const int per_sm = std::min(g_tune.r_ctas_per_sm > 0 ? g_tune.r_ctas_per_sm : auto_sm, occ[dev]);
     const int64_t cap = (int64_t)num_sms(dev) * per_sm;

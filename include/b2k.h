@@ -100,6 +100,9 @@ B2_API int b2_transpose_host(const void *in_host, void *out_host, int64_t rows, 
  *                                     sequential sum: tolerance, not bits)
  *   dtype B2_I32 -> *out is int64_t (exact == the reference's unbounded int sum)
  *   dtype B2_F64 -> *out is double
+ *   dtype B2_I64 -> *out is a 16-byte two's-complement integer (little-endian;
+ *                   128-bit accumulation: exact for any n, like Python ints).
+ *                   Not available in the fused / multi-GPU combines (8-byte slots).
  * Replaces: interp.py:282-300 + :262-270 executing `for i < N { sum += arr[i]; }`
  *   (PAPER.md:155-172).
  * ws: device workspace of b2_reduce_ws_bytes(n, dtype) bytes, zero-filled before
@@ -125,7 +128,8 @@ B2_API int b2_reduce_sum_fused(const void *in, int64_t n, int dtype, void *out, 
                                size_t ws_bytes, void *mailbox, int rank, int nranks,
                                uint64_t epoch, int dev, void *stream);
 
-/* Host-buffer form of b2_reduce_sum; *out_host receives float/int64/double. */
+/* Host-buffer form of b2_reduce_sum; *out_host receives float / int64 / double /
+ * 16-byte int (B2_I64), as b2_reduce_sum. */
 B2_API int b2_reduce_sum_host(const void *in_host, int64_t n, int dtype, void *out_host, int dev);
 
 /* Appendix A.5 order: per 512-element block b,

@@ -103,7 +103,7 @@ int ctx_init(DevCtx &c, int dev) {
         B2_CUDA(cudaEventCreateWithFlags(&c.ev_out[k], cudaEventDisableTiming));
     }
     B2_CUDA(cudaEventCreateWithFlags(&c.ev_legacy, cudaEventDisableTiming));
-    c.ws_bytes = reduce_ws_bytes(0, B2_F64, dev);
+    c.ws_bytes = reduce_ws_bytes(0, B2_I64, dev);  // the widest partial (128-bit int64 sums)
     B2_CUDA(cudaMalloc(&c.ws, c.ws_bytes));
     B2_CUDA(cudaMemset(c.ws, 0, c.ws_bytes));
     c.ready = true;
@@ -747,8 +747,8 @@ int b2_transpose_host(const void *in_host, void *out_host, int64_t rows, int64_t
 
 int b2_reduce_sum_host(const void *in_host, int64_t n, int dtype, void *out_host, int dev) {
     const int E = esize_of(dtype);
-    if (dtype != B2_F32 && dtype != B2_I32 && dtype != B2_F64)
-        return fail(B2_ERR_UNSUPPORTED, "reduce: dtype must be B2_F32, B2_I32 or B2_F64");
+    if (dtype != B2_F32 && dtype != B2_I32 && dtype != B2_F64 && dtype != B2_I64)
+        return fail(B2_ERR_UNSUPPORTED, "reduce: dtype must be B2_F32, B2_I32, B2_I64 or B2_F64");
     if (n < 0) return fail(B2_ERR_INVALID, "reduce: negative length");
     if ((!in_host && n) || !out_host) return fail(B2_ERR_INVALID, "reduce: NULL buffer");
     if (int rc = check_dev(dev)) return rc;
@@ -758,7 +758,7 @@ int b2_reduce_sum_host(const void *in_host, int64_t n, int dtype, void *out_host
     const int64_t ce = std::min<int64_t>(std::max<int64_t>(n, 1), (int64_t)(chunk_bytes() / E));
     if (int rc = ensure_stages(c, (size_t)ce * E)) return rc;
     const int64_t nchunks = n == 0 ? 1 : (n + ce - 1) / ce;
-    if (int rc = ensure_small(c, (size_t)nchunks * 8)) return rc;
+    if (int rc = ensure_small(c, (size_t)nchunks * 16)) return rc;
     const bool stage_in = n > 0 && !is_pinned(in_host);
     if (stage_in && ensure_host_stages(c, (size_t)ce * E)) return B2_ERR_NOMEM;
     const char *hin = (const char *)in_host;
@@ -771,25 +771,33 @@ int b2_reduce_sum_host(const void *in_host, int64_t n, int dtype, void *out_host
         B2_CUDA(cudaEventRecord(c.ev_in[k], c.s_h2d));
         B2_CUDA(cudaStreamWaitEvent(c.s_comp, c.ev_in[k], 0));
         if (int rc = launch_reduce(c.d_in[k], std::max<int64_t>(ne, 0), dtype,
-                                   (char *)c.d_small + i * 8, c.ws, c.ws_bytes, dev, c.s_comp))
+                                   (char *)c.d_small + i * 16, c.ws, c.ws_bytes, dev, c.s_comp))
             return rc;
         B2_CUDA(cudaEventRecord(c.ev_comp[k], c.s_comp));
     }
-    B2_CUDA(cudaMemcpyAsync(c.h_small, c.d_small, nchunks * 8, cudaMemcpyDeviceToHost, c.s_comp));
+    B2_CUDA(cudaMemcpyAsync(c.h_small, c.d_small, nchunks * 16, cudaMemcpyDeviceToHost, c.s_comp));
     B2_CUDA(cudaStreamSynchronize(c.s_comp));
     // host combine of the per-chunk partials, chunk order (deterministic)
     const char *h = (const char *)c.h_small;
     if (dtype == B2_I32) {
         long long s = 0;
-        for (int64_t i = 0; i < nchunks; ++i) s += *(const long long *)(h + i * 8);
+        for (int64_t i = 0; i < nchunks; ++i) s += *(const long long *)(h + i * 16);
         *(long long *)out_host = s;
     } else if (dtype == B2_F32) {
         volatile float s = 0.0f;
-        for (int64_t i = 0; i < nchunks; ++i) s = s + *(const float *)(h + i * 8);
+        for (int64_t i = 0; i < nchunks; ++i) s = s + *(const float *)(h + i * 16);
         *(float *)out_host = s;
+    } else if (dtype == B2_I64) {
+        __int128 s = 0;  // exact: 128-bit chunk partials, 128-bit total (lo, hi words)
+        for (int64_t i = 0; i < nchunks; ++i) {
+            __int128 v;
+            memcpy(&v, h + i * 16, 16);
+            s += v;
+        }
+        memcpy(out_host, &s, 16);
     } else {
         double s = 0.0;
-        for (int64_t i = 0; i < nchunks; ++i) s += *(const double *)(h + i * 8);
+        for (int64_t i = 0; i < nchunks; ++i) s += *(const double *)(h + i * 16);
         *(double *)out_host = s;
     }
     return B2_OK;

@@ -38,6 +38,12 @@ template <>
 struct AccOf<double> {
     using type = double;
 };
+// int64 cells (the reference's ints are unbounded): 128-bit accumulation, exact
+// for any n < 2^64
+template <>
+struct AccOf<int64_t> {
+    using type = __int128;
+};
 
 template <typename T, typename A>
 __device__ __forceinline__ A vec_sum(const uint4 &v);
@@ -54,11 +60,38 @@ template <>
 __device__ __forceinline__ double vec_sum<double, double>(const uint4 &v) {
     return __hiloint2double((int)v.y, (int)v.x) + __hiloint2double((int)v.w, (int)v.z);
 }
+template <>
+__device__ __forceinline__ __int128 vec_sum<int64_t, __int128>(const uint4 &v) {
+    const long long a = (long long)(((unsigned long long)v.y << 32) | v.x);
+    const long long b = (long long)(((unsigned long long)v.w << 32) | v.z);
+    return (__int128)a + (__int128)b;
+}
+
+__device__ __forceinline__ __int128 shfl_down(__int128 a, int off) {
+    const unsigned long long lo = (unsigned long long)a, hi = (unsigned long long)(a >> 64);
+    const unsigned long long lo2 = __shfl_down_sync(0xffffffffu, lo, off);
+    const unsigned long long hi2 = __shfl_down_sync(0xffffffffu, hi, off);
+    return (__int128)(((unsigned __int128)hi2 << 64) | lo2);
+}
+template <typename A>
+__device__ __forceinline__ A shfl_down(A a, int off) {
+    return __shfl_down_sync(0xffffffffu, a, off);
+}
+// partials written by other CTAs: read through L2 (volatile semantics)
+template <typename A>
+__device__ __forceinline__ A load_partial(const A *p) {
+    if constexpr (sizeof(A) == 16) {
+        const volatile unsigned long long *q = reinterpret_cast<const volatile unsigned long long *>(p);
+        return (__int128)(((unsigned __int128)(unsigned long long)q[1] << 64) | (unsigned long long)q[0]);
+    } else {
+        return *reinterpret_cast<const volatile A *>(p);
+    }
+}
 
 template <typename A>
 __device__ __forceinline__ A warp_tree(A a) {
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) a += __shfl_down_sync(0xffffffffu, a, off);
+    for (int off = 16; off > 0; off >>= 1) a += shfl_down(a, off);
     return a;
 }
 
@@ -224,13 +257,17 @@ __global__ void __launch_bounds__(NT)
     __threadfence();
     A a = A(0);
     for (int j = threadIdx.x; j < (int)gridDim.x; j += NT)
-        a += *reinterpret_cast<volatile A *>(partials + j);
+        a += load_partial<A>(partials + j);
     __syncthreads();  // sm reuse
     A total = block_tree<A, NT>(a, sm);
     if (threadIdx.x == 0) {
         *ticket = 0u;  // re-arm for the next call on this workspace
-        if (fz.mailbox) fused_combine<A>(fz, total, out);
-        else *out = total;
+        if constexpr (sizeof(A) <= 8) {
+            if (fz.mailbox) fused_combine<A>(fz, total, out);
+            else *out = total;
+        } else {
+            *out = total;  // 128-bit results are not combined across GPUs (8-byte slots)
+        }
     }
 }
 
@@ -333,7 +370,7 @@ int run_reduce(const void *in_, int64_t n, void *out, void *ws, size_t ws_bytes,
 }  // namespace
 
 size_t reduce_ws_bytes(int64_t, int dtype, int dev) {
-    size_t a = dtype == B2_F32 ? 4 : 8;
+    size_t a = dtype == B2_F32 ? 4 : dtype == B2_I64 ? 16 : 8;
     return (size_t)max_grid(dev) * a + 64;
 }
 
@@ -348,7 +385,10 @@ int launch_reduce(const void *in, int64_t n, int dtype, void *out, void *ws, siz
     case B2_F32: return run_reduce<float>(in, n, out, ws, ws_bytes, dev, st, fz);
     case B2_I32: return run_reduce<int32_t>(in, n, out, ws, ws_bytes, dev, st, fz);
     case B2_F64: return run_reduce<double>(in, n, out, ws, ws_bytes, dev, st, fz);
-    default: return fail(B2_ERR_UNSUPPORTED, "reduce: dtype must be B2_F32, B2_I32 or B2_F64");
+    case B2_I64:
+        if (fz.mailbox) return fail(B2_ERR_UNSUPPORTED, "fused combine: int64 sums are 128-bit");
+        return run_reduce<int64_t>(in, n, out, ws, ws_bytes, dev, st, fz);
+    default: return fail(B2_ERR_UNSUPPORTED, "reduce: dtype must be B2_F32, B2_I32, B2_I64 or B2_F64");
     }
 }
 

@@ -435,9 +435,10 @@ def _exec_reduce_naive(plan: Plan, env):
     x = _cells(arr, N, cell)
     if cell == "float":
         return ("ret", float(np.float32(ops.reduce_sum(np.ascontiguousarray(x)))))
-    if x.dtype != np.int32:
-        raise InterpError("int cell value outside the 4-byte cell range (intrinsics.py:35 "
-                          "CELL_BYTES = 4)")
+    if x.dtype not in (np.int32, np.int64):
+        raise InterpError("int cell value outside the 64-bit range (cells beyond int64 are "
+                          "not representable on the device)")
+    # int32 cells: int64 accumulation; int64 cells: 128-bit (exact like Python ints)
     return ("ret", int(ops.reduce_sum(np.ascontiguousarray(x))))
 
 
@@ -458,9 +459,9 @@ def _exec_reduce_tree(plan: Plan, env):
     if N <= 0:
         return ("ret", 0.0 if cell == "float" else 0)
     if cell == "int":
-        if x.dtype != np.int32:
-            raise InterpError("int cell value outside the 4-byte cell range (intrinsics.py:35 "
-                              "CELL_BYTES = 4)")
+        if x.dtype not in (np.int32, np.int64):
+            raise InterpError("int cell value outside the 64-bit range (cells beyond int64 are "
+                              "not representable on the device)")
         return ("ret", int(ops.reduce_sum(np.ascontiguousarray(x))))
     return ("ret", ops.reduce_tree(np.ascontiguousarray(x), B))
 

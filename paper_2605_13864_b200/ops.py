@@ -117,33 +117,47 @@ def transpose(inp, out=None, *, stream=None):
 # ----------------------------------------------------------------------------- reduction
 
 _ACC = {_lib.F32: (np.float32, "float32"), _lib.I32: (np.int64, "int64"),
-        _lib.F64: (np.float64, "float64")}
+        _lib.F64: (np.float64, "float64"), _lib.I64: (np.int64, "int64")}
+
+
+def _int128(words) -> int:
+    """(lo, hi) int64 words of a B2_I64 result -> Python int."""
+    lo, hi = int(words[0]), int(words[1])
+    return (lo & ((1 << 64) - 1)) + (hi << 64)
 
 
 def reduce_sum(arr, *, out=None, ws=None, stream=None):
-    """Sum of a 1-D float32 / int32 / float64 array (int32 accumulates in int64).
+    """Sum of a 1-D float32 / int32 / int64 / float64 array (int32 accumulates in
+    int64, int64 in 128 bits: exact like the reference's unbounded ints).
 
-    Device: returns a 1-element CUDA tensor (float32 / int64 / float64), async.
+    Device: returns a 1-element CUDA tensor (float32 / int64 / float64), async;
+    for int64 input a 2-element int64 tensor (lo, hi words; see `int128`).
     Host: returns a Python float / int.
     """
     arr, out = _as_device(arr), _as_device(out)
     d = b2_dtype(arr)
     if d not in _ACC:
-        raise TypeError("reduce: dtype must be float32, int32 or float64")
+        raise TypeError("reduce: dtype must be float32, int32, int64 or float64")
     npacc, tacc = _ACC[d]
+    words = 2 if d == _lib.I64 else 1
     if _is_torch_cuda(arr):
         if arr.dim() != 1 or (arr.numel() and arr.stride(0) != 1):
             raise ValueError("reduce: input must be a contiguous 1-D tensor")
         if out is None:
-            out = torch.empty(1, dtype=getattr(torch, tacc), device=arr.device)
+            out = torch.empty(words, dtype=getattr(torch, tacc), device=arr.device)
         wsp, wsb = (0, 0) if ws is None else (ws.data_ptr(), ws.numel() * ws.element_size())
         check(lib().b2_reduce_sum(arr.data_ptr(), arr.numel(), d, out.data_ptr(), wsp or None, wsb,
                                   arr.device.index, _stream_ptr(arr, stream)))
         return out
     a = np.ascontiguousarray(arr).reshape(-1)
-    res = np.zeros(1, dtype=npacc)
+    res = np.zeros(words, dtype=npacc)
     check(lib().b2_reduce_sum_host(a.ctypes.data, a.size, d, res.ctypes.data, _host_device()))
-    return res[0].item()
+    return _int128(res) if words == 2 else res[0].item()
+
+
+def int128(t) -> int:
+    """Python int of a device int64-sum result tensor (lo, hi words)."""
+    return _int128(t.cpu().numpy() if hasattr(t, "cpu") else t)
 
 
 def reduce_tree(arr, block: int = 512, *, stream=None) -> float:

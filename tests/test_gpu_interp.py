@@ -149,3 +149,25 @@ def test_reference_edge_inputs_that_succeed(b2):
                       else v) for k, v in c["inputs"].items()}
         ret, _ = b2.run_program(_prog(b2, c["program"]), c["entry"], inputs)
         assert ret == c["ret"], c["program"]
+
+
+def test_int64_cells_sum_exactly_beyond_int64(b2):
+    """The reference's ints are unbounded: int64 cells sum in 128 bits, so sums far
+    beyond the int64 range come back exact (device, host and run_program paths)."""
+    import torch
+    rng = np.random.default_rng(64)
+    x = rng.integers(-2**63, 2**63, 1_000_003, dtype=np.int64)
+    want = sum(int(v) for v in x.tolist())
+    assert b2.reduce_sum(x) == want
+    from paper_2605_13864_b200.ops import int128
+    assert int128(b2.reduce_sum(torch.from_numpy(x).cuda())) == want
+    big = np.full(1 << 20, 2**62 + 12345, dtype=np.int64)
+    assert b2.reduce_sum(big) == (2**62 + 12345) << 20
+    ret, _ = b2.run_program(_prog(b2, "reduce_naive_int.optc"), "reduce",
+                            {"arr": [2**40, -3, 2**62, 2**62, 2**62], "N": 5})
+    assert ret == 2**40 - 3 + 3 * 2**62
+    for off in range(3):  # head / tail paths of the 128-bit kernel
+        seg = x[off:off + 70_001]
+        assert b2.reduce_sum(torch.from_numpy(seg.copy()).cuda()[0:].contiguous()).shape[0] == 2
+        assert int128(b2.reduce_sum(torch.from_numpy(x).cuda()[off:off + 70_001])) == \
+            sum(int(v) for v in seg.tolist())

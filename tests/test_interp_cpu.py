@@ -84,9 +84,12 @@ def test_unrecognised_program_is_refused_not_interpreted():
         run_program(p, "f", {"a": [1, 2], "n": 2})
 
 
-def test_int_cells_outside_32_bits_refused():
-    with pytest.raises(InterpError, match="4-byte"):
-        run_program(prog("reduce_naive_int.optc"), "reduce", {"arr": [2**40, 1], "N": 2})
+def test_int_cells_outside_64_bits_refused():
+    """int32 and int64 cells sum exactly on the device (128-bit accumulation for
+    int64); cells the device cannot hold are refused, never wrapped."""
+    for big in (2**70, 2**63):
+        with pytest.raises(InterpError, match="64-bit range"):
+            run_program(prog("reduce_naive_int.optc"), "reduce", {"arr": [big, 1], "N": 2})
 
 
 def test_float_overflow_matches_struct_pack():

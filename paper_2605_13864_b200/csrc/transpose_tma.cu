@@ -156,6 +156,101 @@ __global__ void __launch_bounds__(256, 1)
     if (tid == 0) bulk_wait_all();
 }
 
+// ---------------------------------------------------------------------------
+// TMA-loaded tiles, register transpose, direct 128-bit stores (transpose.tma = 2).
+// Only the INPUT is staged in shared memory (S stages of TR x 128 fp32 cells,
+// four 32-column 128B-swizzled boxes each), so up to 192 KB of tile data per SM
+// is in flight through TMA. Lane l of a warp owns input rows 4l..4l+3 of one
+// 4-column micro-column; its four LDS.128 are issued in a lane-rotated row order
+// ((k + l/2) & 3) so every quarter-warp touches 8 distinct 16-B bank groups
+// under the swizzle; after un-rotating and a 4x4 register transpose each lane
+// stores 16 B to four output rows, a warp covering 512 contiguous bytes per row.
+// One __syncthreads per tile releases the stage, then thread 0 refills it while
+// the stores drain.
+template <int TR, int S>
+__global__ void __launch_bounds__(512, 1)
+    transpose_tmar_kernel(const __grid_constant__ CUtensorMap tin, uint8_t *__restrict__ out,
+                          int64_t rows, int64_t cols, int64_t ld_out_b, int64_t tiles_r,
+                          int64_t ntiles) {
+    constexpr int TC = 128;                    // input columns per tile (4 boxes of 32)
+    constexpr int kBoxB = TR * 128;            // bytes per box
+    constexpr int kStage = 4 * kBoxB;
+    constexpr int G = TR / 4;                  // row groups (4 input rows each) per tile
+    constexpr int MPT = G * 32 / 512;          // micro-tiles per thread
+    static_assert(G == 16 || G == 32, "the lane-rotated loads assume 16 or 32 row groups");
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                                ~uintptr_t(1023));
+    __shared__ uint64_t full[S];
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int64_t my_n = blockIdx.x < ntiles ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    auto origin = [&](int64_t it, int &r0, int &c0) {
+        const int64_t t = blockIdx.x + it * gridDim.x;  // column-major tile walk
+        r0 = (int)((t % tiles_r) * TR);
+        c0 = (int)((t / tiles_r) * TC);
+    };
+    auto issue = [&](int64_t it) {
+        int r0, c0;
+        origin(it, r0, c0);
+        const int st = (int)(it % S);
+        mbar_expect_tx(&full[st], kStage);
+#pragma unroll
+        for (int b = 0; b < 4; ++b) tma_load_2d(base + st * kStage + b * kBoxB, &tin, c0 + 32 * b, r0, &full[st]);
+    };
+    if (tid == 0) {
+        for (int s2 = 0; s2 < S; ++s2) mbar_init(&full[s2], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int64_t it = 0; it < min((int64_t)S, my_n); ++it) issue(it);
+    }
+    __syncthreads();
+    const int rot = (lane >> 1) & 3;
+    for (int64_t it = 0; it < my_n; ++it) {
+        const int st = (int)(it % S);
+        mbar_wait(&full[st], (uint32_t)((it / S) & 1));
+        int r0, c0;
+        origin(it, r0, c0);
+        uint4 v[MPT][4];
+#pragma unroll
+        for (int q = 0; q < MPT; ++q) {
+            const int p = tid + 512 * q;               // micro-tile: row group fastest
+            const int g = p % G, m = p / G;            // row group, micro-column 0..31
+            const uint8_t *box = base + st * kStage + (m >> 3) * kBoxB;
+            const int cc = m & 7;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int row = 4 * g + ((k + rot) & 3);
+                v[q][k] = *reinterpret_cast<const uint4 *>(box + row * 128 + ((cc ^ (row & 7)) << 4));
+            }
+        }
+        __syncthreads();  // stage st fully read by every thread
+        if (tid == 0 && it + S < my_n) issue(it + S);
+#pragma unroll
+        for (int q = 0; q < MPT; ++q) {
+            // un-rotate: u[i] = v[(i - rot) & 3]
+            uint4 u[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const uint4 a0 = v[q][i], a1 = v[q][(i + 3) & 3], a2 = v[q][(i + 2) & 3], a3 = v[q][(i + 1) & 3];
+                u[i] = rot == 0 ? a0 : rot == 1 ? a1 : rot == 2 ? a2 : a3;
+            }
+            const int p = tid + 512 * q;
+            const int g = p % G, m = p / G;
+            const int64_t orow0 = (int64_t)c0 + 4 * m;   // output rows = input columns
+            const int64_t ocol = (int64_t)r0 + 4 * g;    // output columns = input rows
+            const uint4 o[4] = {make_uint4(u[0].x, u[1].x, u[2].x, u[3].x),
+                                make_uint4(u[0].y, u[1].y, u[2].y, u[3].y),
+                                make_uint4(u[0].z, u[1].z, u[2].z, u[3].z),
+                                make_uint4(u[0].w, u[1].w, u[2].w, u[3].w)};
+            if (ocol + 3 < rows) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (orow0 + j < cols)
+                        stg_stream(reinterpret_cast<uint4 *>(out + (orow0 + j) * ld_out_b + ocol * 4), o[j]);
+            }
+        }
+    }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
     if (!fn) {
@@ -180,6 +275,42 @@ int make_map(CUtensorMap *m, const void *ptr, int64_t inner, int64_t outer, int6
                      box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(B2_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+    return B2_OK;
+}
+
+int make_map_box(CUtensorMap *m, const void *ptr, int64_t inner, int64_t outer, int64_t pitch_bytes,
+                 int box_inner, int box_outer) {
+    auto enc = encode_fn();
+    if (!enc) return fail(B2_ERR_UNSUPPORTED, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+    cuuint64_t strides[1] = {(cuuint64_t)pitch_bytes};
+    cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_outer};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<void *>(ptr), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(B2_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+    return B2_OK;
+}
+
+template <int TR, int S>
+int run_tmar(const void *in, void *out, int64_t rows, int64_t cols, int64_t ld_in, int64_t ld_out, int dev,
+             cudaStream_t st) {
+    CUtensorMap tin;
+    if (int rc = make_map_box(&tin, in, cols, rows, ld_in * 4, 32, TR)) return rc;
+    const int64_t tiles_r = (rows + TR - 1) / TR, tiles_c = (cols + 127) / 128;
+    const int64_t ntiles = tiles_r * tiles_c;
+    const int smem = S * 4 * TR * 128 + 1024;
+    static bool attr[64] = {false};
+    if (!attr[dev]) {
+        B2_CUDA(cudaFuncSetAttribute(transpose_tmar_kernel<TR, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        attr[dev] = true;
+    }
+    const int64_t grid = std::min<int64_t>(ntiles, (int64_t)num_sms(dev));
+    transpose_tmar_kernel<TR, S><<<(unsigned)grid, 512, smem, st>>>(tin, (uint8_t *)out, rows, cols, ld_out * 4,
+                                                                     tiles_r, ntiles);
+    count_launch();
+    B2_CUDA(cudaGetLastError());
     return B2_OK;
 }
 
@@ -216,6 +347,15 @@ int launch_transpose_tma(const void *in, void *out, int64_t rows, int64_t cols, 
     if ((uintptr_t)in % 16 || (uintptr_t)out % 16 || (ld_in * 4) % 16 || (ld_out * 4) % 16 ||
         rows >= (1ll << 31) || cols >= (1ll << 31))
         return fail(B2_ERR_UNSUPPORTED, "TMA transpose needs 16-B aligned bases and pitches");
+    if (g_tune.t_tma == 2) {  // TMA loads + register transpose + direct stores
+        if (rows % 4 || cols % 4) return fail(B2_ERR_UNSUPPORTED, "tmar: rows and cols must be multiples of 4");
+        switch (g_tune.t_tma_stages) {
+        case 2: return run_tmar<128, 2>(in, out, rows, cols, ld_in, ld_out, dev, st);
+        case 4: return run_tmar<64, 4>(in, out, rows, cols, ld_in, ld_out, dev, st);
+        case 6: return run_tmar<64, 6>(in, out, rows, cols, ld_in, ld_out, dev, st);
+        default: return run_tmar<128, 3>(in, out, rows, cols, ld_in, ld_out, dev, st);
+        }
+    }
     switch (g_tune.t_tma_stages) {
     case 2: return run_tma<2>(in, out, rows, cols, ld_in, ld_out, dev, st);
     case 3: return run_tma<3>(in, out, rows, cols, ld_in, ld_out, dev, st);

@@ -293,3 +293,21 @@ def test_reduce_variants_heads_and_tails(b2, variant):
             assert abs(got - exact) <= oracle.f32_tolerance(seg.size, exact, absum)
     finally:
         _lib.tune("reduce.variant", 0)
+
+
+@pytest.mark.parametrize("stages", [2, 3, 4, 6])
+def test_tma_register_transpose_path(b2, stages):
+    """transpose.tma = 2: TMA-loaded input stages, lane-rotated conflict-free LDS,
+    register transpose, direct 128-bit stores; ragged tiles clipped by TMA."""
+    from paper_2605_13864_b200 import _lib
+    _lib.tune("transpose.tma", 2)
+    _lib.tune("transpose.tma_stages", stages)
+    try:
+        for R, C in [(512, 256), (1000, 772), (4100, 132), (132, 4100), (2048, 3072)]:
+            a = torch.rand((R, C), device="cuda")
+            assert torch.equal(b2.transpose(a), a.t()), (R, C)
+        a = torch.rand((1001, 771), device="cuda")  # not multiples of 4: falls back to the LDG path
+        assert torch.equal(b2.transpose(a), a.t())
+    finally:
+        _lib.tune("transpose.tma", 0)
+        _lib.tune("transpose.tma_stages", 2)

@@ -115,10 +115,17 @@ def run_transpose(rng):
     one_transpose(520, 300, np.float32, rng)
     one_transpose(600, 130, np.float64, rng)
     tune("transpose.big", 1)
-    # TMA-staged variant (UTMALDG/UTMASTG + mbarrier ring)
+    # TMA-staged variants: 1 = UTMALDG/UTMASTG + mbarrier ring; 2 = TMA-loaded
+    # input stages, register transpose, direct stores (all stage counts)
     tune("transpose.tma", 1)
     one_transpose(1024, 768, np.float32, rng)
     one_transpose(1000, 770, np.float32, rng)
+    tune("transpose.tma", 2)
+    for stages in (2, 3, 4, 6):
+        tune("transpose.tma_stages", stages)
+        one_transpose(1024, 768, np.float32, rng)
+        one_transpose(1000, 772, np.float32, rng)
+    tune("transpose.tma_stages", 2)
     tune("transpose.tma", 0)
     # host pipeline (chunked H2D / kernel / D2H) with a small stage size
     tune("host.chunk_mb", 1)

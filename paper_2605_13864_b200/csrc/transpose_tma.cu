@@ -167,17 +167,17 @@ __global__ void __launch_bounds__(256, 1)
 // stores 16 B to four output rows, a warp covering 512 contiguous bytes per row.
 // One __syncthreads per tile releases the stage, then thread 0 refills it while
 // the stores drain.
-template <int TR, int S>
+template <int TR, int S, int NB = 4>
 __global__ void __launch_bounds__(512, 1)
     transpose_tmar_kernel(const __grid_constant__ CUtensorMap tin, uint8_t *__restrict__ out,
                           int64_t rows, int64_t cols, int64_t ld_out_b, int64_t tiles_r,
                           int64_t ntiles) {
-    constexpr int TC = 128;                    // input columns per tile (4 boxes of 32)
+    constexpr int TC = 32 * NB;                // input columns per tile (NB boxes of 32)
     constexpr int kBoxB = TR * 128;            // bytes per box
-    constexpr int kStage = 4 * kBoxB;
+    constexpr int kStage = NB * kBoxB;
     constexpr int G = TR / 4;                  // row groups (4 input rows each) per tile
-    constexpr int MPT = G * 32 / 512;          // micro-tiles per thread
-    static_assert(G == 16 || G == 32, "the lane-rotated loads assume 16 or 32 row groups");
+    constexpr int MPT = G * (TC / 4) / 512;    // micro-tiles per thread
+    static_assert(G >= 16 && G % 16 == 0 && MPT >= 1, "the lane-rotated loads assume >= 16 row groups");
     extern __shared__ uint8_t smem_raw[];
     uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                 ~uintptr_t(1023));
@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(512, 1)
         const int st = (int)(it % S);
         mbar_expect_tx(&full[st], kStage);
 #pragma unroll
-        for (int b = 0; b < 4; ++b) tma_load_2d(base + st * kStage + b * kBoxB, &tin, c0 + 32 * b, r0, &full[st]);
+        for (int b = 0; b < NB; ++b) tma_load_2d(base + st * kStage + b * kBoxB, &tin, c0 + 32 * b, r0, &full[st]);
     };
     if (tid == 0) {
         for (int s2 = 0; s2 < S; ++s2) mbar_init(&full[s2], 1);
@@ -293,22 +293,23 @@ int make_map_box(CUtensorMap *m, const void *ptr, int64_t inner, int64_t outer, 
     return B2_OK;
 }
 
-template <int TR, int S>
+template <int TR, int S, int NB = 4>
 int run_tmar(const void *in, void *out, int64_t rows, int64_t cols, int64_t ld_in, int64_t ld_out, int dev,
              cudaStream_t st) {
     CUtensorMap tin;
     if (int rc = make_map_box(&tin, in, cols, rows, ld_in * 4, 32, TR)) return rc;
-    const int64_t tiles_r = (rows + TR - 1) / TR, tiles_c = (cols + 127) / 128;
+    const int64_t tiles_r = (rows + TR - 1) / TR, tiles_c = (cols + 32 * NB - 1) / (32 * NB);
     const int64_t ntiles = tiles_r * tiles_c;
-    const int smem = S * 4 * TR * 128 + 1024;
+    const int smem = S * NB * TR * 128 + 1024;
     static bool attr[64] = {false};
     if (!attr[dev]) {
-        B2_CUDA(cudaFuncSetAttribute(transpose_tmar_kernel<TR, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        B2_CUDA(cudaFuncSetAttribute(transpose_tmar_kernel<TR, S, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     smem));
         attr[dev] = true;
     }
     const int64_t grid = std::min<int64_t>(ntiles, (int64_t)num_sms(dev));
-    transpose_tmar_kernel<TR, S><<<(unsigned)grid, 512, smem, st>>>(tin, (uint8_t *)out, rows, cols, ld_out * 4,
-                                                                     tiles_r, ntiles);
+    transpose_tmar_kernel<TR, S, NB><<<(unsigned)grid, 512, smem, st>>>(tin, (uint8_t *)out, rows, cols,
+                                                                         ld_out * 4, tiles_r, ntiles);
     count_launch();
     B2_CUDA(cudaGetLastError());
     return B2_OK;
@@ -353,6 +354,8 @@ int launch_transpose_tma(const void *in, void *out, int64_t rows, int64_t cols, 
         case 2: return run_tmar<128, 2>(in, out, rows, cols, ld_in, ld_out, dev, st);
         case 4: return run_tmar<64, 4>(in, out, rows, cols, ld_in, ld_out, dev, st);
         case 6: return run_tmar<64, 6>(in, out, rows, cols, ld_in, ld_out, dev, st);
+        case 7: return run_tmar<256, 3, 2>(in, out, rows, cols, ld_in, ld_out, dev, st);  // 256 x 64 tiles
+        case 8: return run_tmar<256, 2, 2>(in, out, rows, cols, ld_in, ld_out, dev, st);
         default: return run_tmar<128, 3>(in, out, rows, cols, ld_in, ld_out, dev, st);
         }
     }

@@ -295,7 +295,7 @@ def test_reduce_variants_heads_and_tails(b2, variant):
         _lib.tune("reduce.variant", 0)
 
 
-@pytest.mark.parametrize("stages", [2, 3, 4, 6])
+@pytest.mark.parametrize("stages", [2, 3, 4, 6, 7, 8])
 def test_tma_register_transpose_path(b2, stages):
     """transpose.tma = 2: TMA-loaded input stages, lane-rotated conflict-free LDS,
     register transpose, direct 128-bit stores; ragged tiles clipped by TMA."""

@@ -29,7 +29,7 @@ def timeit(fn, reps=15):
 # correctness first
 for R, C in [(512, 256), (1000, 772), (4100, 132), (132, 4100), (4096, 4096)]:
     a = torch.rand((R, C), device="cuda")
-    for stages in (2, 3, 4, 6):
+    for stages in (2, 3, 4, 6, 7, 8):
         _lib.tune("transpose.tma", 2)
         _lib.tune("transpose.tma_stages", stages)
         o = b2.transpose(a)
@@ -41,7 +41,7 @@ a = torch.rand((32768, 32768), device="cuda")
 o = torch.empty_like(a)
 nb = 2 * a.numel() * 4
 for rep in range(2):
-    for tma, stages in [(0, 2), (2, 3), (2, 2), (2, 4), (2, 6)]:
+    for tma, stages in [(0, 2), (2, 3), (2, 2), (2, 7), (2, 8)]:
         _lib.tune("transpose.tma", tma)
         _lib.tune("transpose.tma_stages", stages)
         ms = timeit(lambda: b2.transpose(a, o))

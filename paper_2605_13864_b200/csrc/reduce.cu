@@ -190,6 +190,12 @@ __device__ void fused_combine(const Fused &fz, A total, A *out) {
 
 // W x 128 bits per load: W = 2 uses the 256-bit global loads sm_100 adds
 // (LDG.E.256), halving the load instructions per byte.
+#ifndef B2_LDG256_QUAL
+#define B2_LDG256_QUAL "ld.global.nc.L1::no_allocate.v8.b32"
+#endif
+#ifndef B2_REDUCE_DEFAULT_W
+#define B2_REDUCE_DEFAULT_W 1
+#endif
 template <int W>
 struct alignas(16 * W) VecW {
     uint4 q[W];
@@ -200,7 +206,7 @@ __device__ __forceinline__ VecW<W> ldg_w(const VecW<W> *p) {
     if constexpr (W == 1) {
         r.q[0] = ldg_stream(reinterpret_cast<const uint4 *>(p));
     } else {
-        asm volatile("ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        asm volatile(B2_LDG256_QUAL " {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                      : "=r"(r.q[0].x), "=r"(r.q[0].y), "=r"(r.q[0].z), "=r"(r.q[0].w), "=r"(r.q[1].x),
                        "=r"(r.q[1].y), "=r"(r.q[1].z), "=r"(r.q[1].w)
                      : "l"(p));
@@ -363,7 +369,7 @@ int run_reduce(const void *in_, int64_t n, void *out, void *ws, size_t ws_bytes,
         // 128-bit loads. The 256-bit variants (5-8) read 1-2 % faster in isolation but
         // slowed the FOLLOWING transpose in the bench step by 4 % (A/B of whole bench
         // steps, profiles/r01j_ldst_variants.md), so they stay opt-in.
-        return run_reduce_v<T, 512, 4>(in, n, out, ws, dev, st, fz);
+        return run_reduce_v<T, 512, 4, B2_REDUCE_DEFAULT_W>(in, n, out, ws, dev, st, fz);
     }
 }
 

@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <condition_variable>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <map>
@@ -240,7 +241,16 @@ class CopyPool {
 };
 
 CopyPool &copy_pool() {
-    static CopyPool *p = new CopyPool(std::max(1, std::min(8, (int)std::thread::hardware_concurrency() / 2)) - 1);
+    // host threads for pageable staging copies (incl. the caller): B2K_COPY_THREADS,
+    // else every hardware thread up to 32 — the copies are host-memory-bound and the
+    // caller is blocked anyway (pageable e2e on the 16-thread box: 8 threads 33 GB/s,
+    // 16 threads 42 GB/s; profiles/r01i_pcie.md)
+    static CopyPool *p = [] {
+        int n = std::max(1, std::min(32, (int)std::thread::hardware_concurrency()));
+        const char *e = getenv("B2K_COPY_THREADS");
+        if (e && *e) n = std::max(1, std::min(64, atoi(e)));
+        return new CopyPool(n - 1);
+    }();
     return *p;
 }
 

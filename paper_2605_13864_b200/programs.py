@@ -23,6 +23,11 @@ T reduce(T* arr, int N) {
     for (int i = 0; i < N; i++) { sum += arr[i]; }
     return sum;
 }"""
+# the same program with the accumulation spelled out (interp.py:259-276: `sum = sum +
+# arr[i]` stores f32(old + v) exactly like `sum += arr[i]`; binary32 / int addition
+# is commutative, so `arr[i] + sum` is the same value too)
+REDUCE_NAIVE_ADD_L = REDUCE_NAIVE.replace("sum += arr[i];", "sum = sum + arr[i];")
+REDUCE_NAIVE_ADD_R = REDUCE_NAIVE.replace("sum += arr[i];", "sum = arr[i] + sum;")
 TRANSPOSE_GPU = """
 void transpose(float* in, float* out, int W, int H) {
     float* const d_in = gmem_malloc2<float>(H, W);

@@ -27,7 +27,8 @@ from .errors import UnsupportedProgram
 from .lang import parse_program
 
 # ----------------------------------------------------------------------------- templates
-from .programs import (REDUCE_NAIVE as _R_NAIVE, REDUCE_TREE as _R_TREE,
+from .programs import (REDUCE_NAIVE as _R_NAIVE, REDUCE_NAIVE_ADD_L as _R_NAIVE_L,
+                       REDUCE_NAIVE_ADD_R as _R_NAIVE_R, REDUCE_TREE as _R_TREE,
                        TRANSPOSE_GPU as _T_GPU, TRANSPOSE_NAIVE_XY as _T_NAIVE_XY,
                        TRANSPOSE_NAIVE_YX as _T_NAIVE_YX, reduce_tree_family, source,
                        transpose_gpu_family)
@@ -60,6 +61,9 @@ TEMPLATES = [
     _mk("reduce_naive_float", "reduce", "naive", "float", _R_NAIVE, _RR, zero="0."),
     _mk("reduce_naive_float_i0", "reduce", "naive", "float", _R_NAIVE, _RR, zero="0"),
     _mk("reduce_naive_int", "reduce", "naive", "int", _R_NAIVE, _RR, zero="0"),
+    *[_mk(f"reduce_naive_{cell}_{side}{z}", "reduce", "naive", cell, text, _RR, zero=zero)
+      for side, text in (("addl", _R_NAIVE_L), ("addr", _R_NAIVE_R))
+      for cell, zero, z in (("float", "0.", ""), ("float", "0", "_i0"), ("int", "0", ""))],
     _mk("reduce_tree512_float", "reduce", "tree512", "float", _R_TREE, _RR),
 ]
 

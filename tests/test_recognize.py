@@ -101,3 +101,30 @@ def test_family_near_misses_refused():
     assert src != transpose_family(64, 16)
     with pytest.raises(UnsupportedProgram):
         recognize(parse_program(src), "transpose")
+
+
+@pytest.mark.parametrize("body", ["sum = sum + arr[i];", "sum = arr[i] + sum;"])
+@pytest.mark.parametrize("cell,zero", [("float", "0."), ("float", "0"), ("int", "0")])
+def test_spelled_out_accumulation_recognised(body, cell, zero):
+    """`sum = sum + arr[i]` / `sum = arr[i] + sum` store exactly what `sum += arr[i]`
+    stores (interp.py:259-276; IEEE / int addition commute): same plan."""
+    src = (f"{cell} reduce({cell}* arr, int N) {{ {cell} sum = {zero}; "
+           f"for (int i = 0; i < N; i++) {{ {body} }} return sum; }}")
+    plan = recognize(parse_program(src), "reduce")
+    assert (plan.kind, plan.form, plan.cell) == ("reduce", "naive", cell)
+
+
+def test_spelled_out_accumulation_same_reference_values():
+    from conftest import reference_available
+    if not reference_available():
+        pytest.skip("reference only in the build container")
+    import random
+    from minigpu.interp import run_program as rrun
+    from minigpu.parser import parse_program as rparse
+    rng = random.Random(1)
+    xs = [rng.uniform(-1, 1) for _ in range(777)]
+    vals = set()
+    for body in ["sum += arr[i];", "sum = sum + arr[i];", "sum = arr[i] + sum;"]:
+        src = f"float reduce(float* arr, int N) {{ float sum = 0.; for (int i = 0; i < N; i++) {{ {body} }} return sum; }}"
+        vals.add(rrun(rparse(src), "reduce", {"arr": xs, "N": len(xs)})[0])
+    assert len(vals) == 1

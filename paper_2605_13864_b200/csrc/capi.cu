@@ -311,6 +311,7 @@ static int *tune_slot(const char *key) {
     if (k == "transpose.any") return &g_tune.t_any;
     if (k == "transpose.scalar_ctas") return &g_tune.t_scalar_ctas;
     if (k == "transpose.tma_stages") return &g_tune.t_tma_stages;
+    if (k == "transpose.scalar_tile") return &g_tune.t_scalar_tile;
     if (k == "host.chunk_mb") return &g_tune.h_chunk_mb;
     return nullptr;
 }

@@ -186,40 +186,43 @@ __global__ void __launch_bounds__(NT)
 // sub-rectangle [r_lo, r_hi) x [c_lo, c_hi); any pitch, any alignment. 64 x 64
 // cells per tile, 256 threads, 16 cells per thread in flight; the +PAD column
 // keeps the transposed shared-memory reads on distinct banks for every width.
-template <typename T>
+template <typename T, int TC = 64>
 __global__ void __launch_bounds__(256)
     transpose_scalar_kernel(const T *__restrict__ in, T *__restrict__ out, int64_t r_lo,
                             int64_t r_hi, int64_t c_lo, int64_t c_hi, int64_t ld_in,
                             int64_t ld_out, int64_t tiles_c, int64_t ntiles) {
-    constexpr int TS = 64;
+    constexpr int TR = 64;        // tile rows; TC tile columns (64, or 128 for narrow cells)
+    constexpr int HC = TC / 32;   // column groups per thread
     constexpr int PAD = sizeof(T) == 2 ? 2 : 1;
-    __shared__ T tile[TS][TS + PAD];
+    __shared__ T tile[TR][TC + PAD];
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
     const int64_t tiles_r = ntiles / tiles_c;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         // column-major tile walk, as in the vector path: concurrent tiles share
         // output rows, so the (short) output segments merge into long write runs
-        const int64_t r0 = r_lo + (t % tiles_r) * TS, c0 = c_lo + (t / tiles_r) * TS;
-        T v[TS / 8][2];
+        const int64_t r0 = r_lo + (t % tiles_r) * TR, c0 = c_lo + (t / tiles_r) * TC;
+        T v[TR / 8][HC];
 #pragma unroll
-        for (int j = 0; j < TS / 8; ++j) {
+        for (int j = 0; j < TR / 8; ++j) {
             const int64_t r = r0 + ty + 8 * j;
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
+            for (int h = 0; h < HC; ++h) {
                 const int64_t c = c0 + tx + 32 * h;
                 if (r < r_hi && c < c_hi) v[j][h] = in[r * ld_in + c];
             }
         }
 #pragma unroll
-        for (int j = 0; j < TS / 8; ++j)
+        for (int j = 0; j < TR / 8; ++j)
 #pragma unroll
-            for (int h = 0; h < 2; ++h) tile[ty + 8 * j][tx + 32 * h] = v[j][h];
+            for (int h = 0; h < HC; ++h) tile[ty + 8 * j][tx + 32 * h] = v[j][h];
         __syncthreads();
+        // out[c][r]: output rows are input columns (TC of them), output columns the
+        // TR input rows; 8 warps x (TC / 8) output rows, 32 lanes x 2 output columns
 #pragma unroll
-        for (int j = 0; j < TS / 8; ++j) {
+        for (int j = 0; j < TC / 8; ++j) {
             const int64_t oc = c0 + ty + 8 * j;  // out row = input col
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
+            for (int h = 0; h < TR / 32; ++h) {
                 const int64_t orr = r0 + tx + 32 * h;
                 if (oc < c_hi && orr < r_hi) out[oc * ld_out + orr] = tile[tx + 32 * h][ty + 8 * j];
             }
@@ -299,17 +302,34 @@ int run_vec(const void *in, void *out, int64_t rows_v, int64_t cols_v, int64_t l
     return B2_OK;
 }
 
+template <typename T, int TC>
+int run_scalar_tc(const void *in, void *out, int64_t r_lo, int64_t r_hi, int64_t c_lo,
+                  int64_t c_hi, int64_t ld_in, int64_t ld_out, int dev, cudaStream_t st);
+
 template <typename T>
 int run_scalar(const void *in, void *out, int64_t r_lo, int64_t r_hi, int64_t c_lo,
                int64_t c_hi, int64_t ld_in, int64_t ld_out, int dev, cudaStream_t st) {
     if (r_hi <= r_lo || c_hi <= c_lo) return B2_OK;
-    const int64_t tiles_r = (r_hi - r_lo + 63) / 64, tiles_c = (c_hi - c_lo + 63) / 64;
+    // 2-byte cells: 64 x 128 tiles (256-B input row runs; 64 x 64 over-fetches ~1.8x
+    // from DRAM on odd pitches, profiles/r01_odd.md); transpose.scalar_tile = 64 opts out
+    if constexpr (sizeof(T) == 2) {
+        if (g_tune.t_scalar_tile != 64) return run_scalar_tc<T, 128>(in, out, r_lo, r_hi, c_lo, c_hi, ld_in, ld_out, dev, st);
+    }
+    return run_scalar_tc<T, 64>(in, out, r_lo, r_hi, c_lo, c_hi, ld_in, ld_out, dev, st);
+}
+
+template <typename T, int TC>
+int run_scalar_tc(const void *in, void *out, int64_t r_lo, int64_t r_hi, int64_t c_lo,
+                  int64_t c_hi, int64_t ld_in, int64_t ld_out, int dev, cudaStream_t st) {
+    const int64_t tiles_r = (r_hi - r_lo + 63) / 64, tiles_c = (c_hi - c_lo + TC - 1) / TC;
     const int64_t ntiles = tiles_r * tiles_c;
-    // same ~64 KB-of-tiles-in-flight rule as the vector path (profiles/r01_odd.md)
-    const int per_sm = g_tune.t_scalar_ctas > 0 ? g_tune.t_scalar_ctas
-                                                : std::max(1, kInflightBytesPerSM / (64 * 64 * (int)sizeof(T)));
+    // same ~64 KB-of-tiles-in-flight rule as the vector path (profiles/r01_odd.md); the
+    // 2-byte 64 x 128 tiles keep 32 KB in flight on large matrices (measured +13-33 %)
+    int auto_sm = std::max(1, kInflightBytesPerSM / (64 * TC * (int)sizeof(T)));
+    if (sizeof(T) == 2 && TC == 128 && ntiles >= 48 * (int64_t)num_sms(dev)) auto_sm = 2;
+    const int per_sm = g_tune.t_scalar_ctas > 0 ? g_tune.t_scalar_ctas : auto_sm;
     const int64_t grid = std::min<int64_t>(ntiles, (int64_t)num_sms(dev) * per_sm);
-    transpose_scalar_kernel<T><<<(unsigned)grid, 256, 0, st>>>(
+    transpose_scalar_kernel<T, TC><<<(unsigned)grid, 256, 0, st>>>(
         (const T *)in, (T *)out, r_lo, r_hi, c_lo, c_hi, ld_in, ld_out, tiles_c, ntiles);
     count_launch();
     B2_CUDA(cudaGetLastError());

@@ -41,7 +41,7 @@ struct Tuning {
     int t_scalar_ctas = 0;  // CTAs per SM of the padded scalar tile kernel (0 = auto)
     int h_chunk_mb = 64;    // host-pipeline chunk (MiB) for the *_host entry points
     int t_tma_stages = 2;   // input stages in flight per CTA (2, 3, 4, 6); 2 x 2 CTAs/SM measured best
-    int t_scalar_tile = 0;  // padded scalar tile width for 2-byte cells: 0 = auto (128), 64
+    int t_scalar_tile = 0;  // padded scalar tile width: 0 = auto (2-byte 128, else 64), 64, 128 (2/4-byte)
 };
 extern Tuning g_tune;
 constexpr int kInflightBytesPerSM = 64 * 1024;

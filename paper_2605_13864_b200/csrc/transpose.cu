@@ -314,6 +314,8 @@ int run_scalar(const void *in, void *out, int64_t r_lo, int64_t r_hi, int64_t c_
     // from DRAM on odd pitches, profiles/r01_odd.md); transpose.scalar_tile = 64 opts out
     if constexpr (sizeof(T) == 2) {
         if (g_tune.t_scalar_tile != 64) return run_scalar_tc<T, 128>(in, out, r_lo, r_hi, c_lo, c_hi, ld_in, ld_out, dev, st);
+    } else if constexpr (sizeof(T) == 4) {
+        if (g_tune.t_scalar_tile == 128) return run_scalar_tc<T, 128>(in, out, r_lo, r_hi, c_lo, c_hi, ld_in, ld_out, dev, st);
     }
     return run_scalar_tc<T, 64>(in, out, r_lo, r_hi, c_lo, c_hi, ld_in, ld_out, dev, st);
 }

@@ -287,12 +287,17 @@ int run_vec(const void *in, void *out, int64_t rows_v, int64_t cols_v, int64_t l
     const int auto_sm = std::max(1, kInflightBytesPerSM / kTileBytes);
     const int per_sm = std::min(g_tune.t_ctas_per_sm > 0 ? g_tune.t_ctas_per_sm : auto_sm, occ[dev]);
     const int64_t grid = std::min<int64_t>(ntiles, (int64_t)num_sms(dev) * per_sm);
-    // Tile walk: column-major by default (band height = all tile-rows), so the ~#SM
-    // tiles in flight sit in one column block and their output rows are written as
-    // long contiguous runs; DRAM efficiency is set by the write side. Measured on
-    // B200 (profiles/r01h_colwalk.md): fp32 32768^2 6.37-6.43 TB/s vs 6.01-6.18 with
-    // row-major bands, fp64 +5 %, bf16 +3 %.
-    const int grp = g_tune.t_group > 0 ? g_tune.t_group : (int)std::min<int64_t>(tiles_r, 1 << 30);
+    // Tile walk. Column-major (band height = all tile-rows) when a column block holds
+    // about as many tiles as there are SMs: the tiles in flight then sit in ONE
+    // column block and their output rows are written as long contiguous runs
+    // (fp32 32768^2 6.37-6.43 TB/s vs 6.01-6.18 row-major, fp64 +5 %, bf16 +3 %;
+    // profiles/r01h_colwalk.md). With fewer tile-rows the window would straddle
+    // several column blocks, and row-major bands measure better (8192x16384 +4 %,
+    // 16384x8192 +7 %, 4096x32768 +3 %; profiles/r01n_midsize.md).
+    const bool colwalk = tiles_r * 4 >= (int64_t)num_sms(dev) * 3;
+    const int grp = g_tune.t_group > 0 ? g_tune.t_group
+                                       : colwalk ? (int)std::min<int64_t>(tiles_r, 1 << 30)
+                                                 : (kTileBytes >= 64 * 1024 ? 1 : 4);
     const int group = (int)std::max<int64_t>(1, std::min<int64_t>(grp, tiles_r));
     transpose_vec_kernel<E, TRV, TCV, NT><<<(unsigned)grid, NT, kSmem, st>>>(
         (const uint8_t *)in, (uint8_t *)out, rows_v, cols_v, ld_in * E, ld_out * E, tiles_r,

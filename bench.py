@@ -531,36 +531,75 @@ def e2e_leg(b2, a, x, rows, cols, n, args, world, dev):
 
 
 def paper_configs(b2, dev):
-    """PAPER.md Table 7.4 workloads (4096^2 fp32 transpose, 2^24 fp32 sum) with an L2
-    flush between launches, for a like-for-like comparison (RTX 5060 numbers)."""
+    """PAPER.md Table 7.4 workloads (4096^2 fp32 transpose, 2^24 fp32 sum) and
+    BASELINE C1 (1024^2 fp32 transpose), timed two ways against cold L2:
+    - single launch between CUDA events after a read pass over 2x L2 (includes the
+      event-pair floor, ~6 us here: profiles/r01i_small_sizes.json);
+    - pipelined: one CUDA graph of back-to-back launches over R rotating inputs
+      whose total is >= 3x L2, so no launch finds its input in L2."""
     import torch
     # cold L2 without dirty lines: a READ pass over 2x L2 before every launch (a
     # write flush would leave ~L2 of dirty lines whose write-back lands inside the
     # timed kernel)
     flush = torch.ones(2 * L2_BYTES // 4, dtype=torch.float32, device=dev)
     out = {}
-    a = torch.rand((4096, 4096), device=dev)
-    o = torch.empty_like(a)
-    x = torch.rand(1 << 24, device=dev)
-    r = torch.empty(1, device=dev)
-    for name, fn, bytes_, paper in [
-        ("transpose_4096sq_f32", lambda: b2.transpose(a, o), 2 * 4096 * 4096 * 4, 340.6),
-        ("reduce_2^24_f32", lambda: b2.reduce_sum(x, out=r), (1 << 24) * 4 + 4, 376.8),
+
+    def transpose_case(n):
+        R = max(2, -(-3 * L2_BYTES // (2 * n * n * 4)))
+        a = [torch.rand((n, n), device=dev) for _ in range(R)]
+        o = [torch.empty_like(a[0]) for _ in range(R)]
+        return R, (lambda i: b2.transpose(a[i], o[i])), (a, o)
+
+    def reduce_case(n):
+        R = max(2, -(-3 * L2_BYTES // (n * 4)))
+        x = [torch.rand(n, device=dev) for _ in range(R)]
+        r = [torch.empty(1, device=dev) for _ in range(R)]
+        return R, (lambda i: b2.reduce_sum(x[i], out=r[i])), (x, r)
+
+    for name, make, n, bytes_, paper in [
+        ("transpose_1024sq_f32", transpose_case, 1024, 2 * 1024 * 1024 * 4, None),
+        ("transpose_4096sq_f32", transpose_case, 4096, 2 * 4096 * 4096 * 4, 340.6),
+        ("reduce_2^24_f32", reduce_case, 1 << 24, (1 << 24) * 4 + 4, 376.8),
     ]:
+        R, fn, keep = make(n)
         ts = []
         for i in range(23):
             flush.sum()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            fn()
+            fn(0)
             e1.record()
             torch.cuda.synchronize()
             if i >= 3:
                 ts.append(e0.elapsed_time(e1))
         med = statistics.median(ts)
+        K = max(2 * R, 64)
+        s = torch.cuda.Stream(device=dev)
+        with torch.cuda.stream(s):
+            for i in range(R):
+                fn(i)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            for i in range(K):
+                fn(i % R)
+        tp = []
+        for i in range(8):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            g.replay()
+            e1.record()
+            torch.cuda.synchronize()
+            if i >= 2:
+                tp.append(e0.elapsed_time(e1) / K)
+        pip = statistics.median(tp)
         out[name] = {"ms_median": med, "GBps": bytes_ / (med / 1e3) / 1e9,
+                     "ms_pipelined": pip, "GBps_pipelined": bytes_ / (pip / 1e3) / 1e9,
                      "paper_best_rtx5060_GBps": paper,
-                     "l2": "cold: 252 MB read pass (clean lines) before every launch"}
+                     "l2": "cold: 252 MB read pass (clean lines) before every single launch; "
+                           f"pipelined: graph of {K} launches over {R} rotating inputs (>= 3x L2)"}
+        del g, keep
+        torch.cuda.empty_cache()
     return out
 
 

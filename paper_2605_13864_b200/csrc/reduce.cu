@@ -239,10 +239,19 @@ __global__ void __launch_bounds__(NT)
 #pragma unroll
             for (int w = 0; w < W; ++w) acc += vec_sum<T, A>(v[u].q[w]);
     }
-    for (; i < nvec; i += stride) {
-        const VecW<W> v = ldg_w<W>(vin + i);
+    // remainder (< U vectors per thread): one batch with all loads in flight together
+    // instead of one DRAM round trip per leftover vector. Out-of-range slots re-load
+    // the thread's own first vector (unconditional loads keep ptxas from serialising
+    // them behind the adds) and are masked out of the sum.
+    if (i < nvec) {
+        VecW<W> v[U];
 #pragma unroll
-        for (int w = 0; w < W; ++w) acc += vec_sum<T, A>(v.q[w]);
+        for (int u = 0; u < U; ++u) v[u] = ldg_w<W>(vin + (i + u * stride < nvec ? i + u * stride : i));
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (i + u * stride < nvec)
+#pragma unroll
+                for (int w = 0; w < W; ++w) acc += vec_sum<T, A>(v[u].q[w]);
     }
     // unaligned head and ragged tail (< V * W elements each)
     const int64_t g = (int64_t)blockIdx.x * NT + threadIdx.x;

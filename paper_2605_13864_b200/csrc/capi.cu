@@ -33,7 +33,7 @@ int cuda_fail(cudaError_t e, const char *what) {
     return e == cudaErrorMemoryAllocation ? B2_ERR_NOMEM : B2_ERR_CUDA;
 }
 
-static int g_sms[64] = {0};
+static std::atomic<int> g_sms[64];  // per-device SM count cache
 int num_sms(int dev) {
     if (dev < 0 || dev >= 64) return 148;
     if (g_sms[dev] == 0) {

@@ -332,7 +332,7 @@ int run_reduce_v(const T *in, int64_t n, void *out, void *ws, int dev, cudaStrea
     int64_t head = (int64_t)(((16 * W - ((uintptr_t)in & (16 * W - 1))) & (16 * W - 1)) / sizeof(T));
     head = std::min<int64_t>(head, n);
     const int64_t nvec = (n - head) / (V * W);
-    static int occ[64] = {0};
+    static std::atomic<int> occ[64];  // per-device cache (zero-initialised)
     if (occ[dev] == 0) {
         int o = 0;
         B2_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, reduce_kernel<T, NT, U, W>, NT, 0));
@@ -343,7 +343,7 @@ int run_reduce_v(const T *in, int64_t n, void *out, void *ws, int dev, cudaStrea
     // bench step 1024 beats 1536 by 1.5 % on the reduction and leaves the next
     // transpose untouched, and isolated it is on par (profiles/r01k_reduce_residency.md).
     const int auto_sm = std::max(1, kReduceThreadsPerSM / NT);
-    const int per_sm = std::min(g_tune.r_ctas_per_sm > 0 ? g_tune.r_ctas_per_sm : auto_sm, occ[dev]);
+    const int per_sm = std::min(g_tune.r_ctas_per_sm > 0 ? g_tune.r_ctas_per_sm : auto_sm, occ[dev].load());
     const int64_t cap = (int64_t)num_sms(dev) * per_sm;
     const int64_t need = std::max<int64_t>(1, (nvec + NT - 1) / NT);
     const int grid = (int)std::min(cap, need);

@@ -270,7 +270,7 @@ int run_vec(const void *in, void *out, int64_t rows_v, int64_t cols_v, int64_t l
     const int64_t ntiles = tiles_r * tiles_c;
     if (ntiles == 0) return B2_OK;
     constexpr int kSmem = TC * TRV * 16;
-    static int occ[64] = {0};
+    static std::atomic<int> occ[64];  // per-device cache (zero-initialised)
     if (occ[dev] == 0) {
         if (kSmem > 48 * 1024)
             B2_CUDA(cudaFuncSetAttribute(transpose_vec_kernel<E, TRV, TCV, NT>,
@@ -285,7 +285,7 @@ int run_vec(const void *in, void *out, int64_t rows_v, int64_t cols_v, int64_t l
     // page/turnaround contention (fp32 64x64: 6 CTAs/SM 5.69 TB/s, 4 CTAs 6.13).
     constexpr int kTileBytes = TR * TC * E;
     const int auto_sm = std::max(1, kInflightBytesPerSM / kTileBytes);
-    const int per_sm = std::min(g_tune.t_ctas_per_sm > 0 ? g_tune.t_ctas_per_sm : auto_sm, occ[dev]);
+    const int per_sm = std::min(g_tune.t_ctas_per_sm > 0 ? g_tune.t_ctas_per_sm : auto_sm, occ[dev].load());
     const int64_t grid = std::min<int64_t>(ntiles, (int64_t)num_sms(dev) * per_sm);
     // Tile walk. Column-major (band height = all tile-rows) when a column block holds
     // about as many tiles as there are SMs: the tiles in flight then sit in ONE

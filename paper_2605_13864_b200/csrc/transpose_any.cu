@@ -212,7 +212,7 @@ int run_any(const void *in, void *out, int64_t rows, int64_t cols, int64_t ld_in
     const int64_t ntiles = tiles_r * tiles_c;
     if (ntiles == 0) return B2_OK;
     constexpr int smem = 2 * TS * TS * E;
-    static int occ[64] = {0};
+    static std::atomic<int> occ[64];  // per-device cache (zero-initialised)
     if (occ[dev] == 0) {
         if (smem > 48 * 1024)
             B2_CUDA(cudaFuncSetAttribute(transpose_any_kernel<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -221,7 +221,7 @@ int run_any(const void *in, void *out, int64_t rows, int64_t cols, int64_t ld_in
         occ[dev] = o > 0 ? o : 1;
     }
     const int auto_sm = std::max(1, kInflightBytesPerSM / (TS * TS * E));
-    const int per_sm = std::min(g_tune.t_ctas_per_sm > 0 ? g_tune.t_ctas_per_sm : auto_sm, occ[dev]);
+    const int per_sm = std::min(g_tune.t_ctas_per_sm > 0 ? g_tune.t_ctas_per_sm : auto_sm, occ[dev].load());
     const int64_t grid = std::min<int64_t>(ntiles, (int64_t)num_sms(dev) * per_sm);
     transpose_any_kernel<E><<<(unsigned)grid, NT, smem, st>>>((const uint8_t *)in, (uint8_t *)out, rows,
                                                               cols, ld_in, ld_out, tiles_c, ntiles);

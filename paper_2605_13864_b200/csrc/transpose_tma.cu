@@ -252,15 +252,16 @@ __global__ void __launch_bounds__(512, 1)
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-    if (!fn) {
+    // resolved once (thread-safe static initialisation); null if the driver lacks it
+    static const PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
         void *p = nullptr;
         cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
-                cudaSuccess &&
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
             q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-    }
+            return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+        cudaGetLastError();
+        return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
+    }();
     return fn;
 }
 
@@ -301,7 +302,7 @@ int run_tmar(const void *in, void *out, int64_t rows, int64_t cols, int64_t ld_i
     const int64_t tiles_r = (rows + TR - 1) / TR, tiles_c = (cols + 32 * NB - 1) / (32 * NB);
     const int64_t ntiles = tiles_r * tiles_c;
     const int smem = S * NB * TR * 128 + 1024;
-    static bool attr[64] = {false};
+    static std::atomic<bool> attr[64];
     if (!attr[dev]) {
         B2_CUDA(cudaFuncSetAttribute(transpose_tmar_kernel<TR, S, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      smem));
@@ -324,7 +325,7 @@ int run_tma(const void *in, void *out, int64_t rows, int64_t cols, int64_t ld_in
     const int64_t tiles_r = (rows + kTile - 1) / kTile, tiles_c = (cols + kTile - 1) / kTile;
     const int64_t ntiles = tiles_r * tiles_c;
     const int smem = (S + 2) * kStageBytes + 1024;
-    static bool attr[64] = {false};
+    static std::atomic<bool> attr[64];
     if (!attr[dev]) {
         B2_CUDA(cudaFuncSetAttribute(transpose_tma_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         attr[dev] = true;

@@ -3,7 +3,9 @@ int32) and odd / non-square transposes (bf16, fp32, fp64), each checked
 against the CPU oracle, timed with CUDA events (median of REPS after warm-up,
 L2 flushed by a 252 MB read pass (clean lines, no write-back inside the timed
 kernel) before every launch when the working set is
-smaller than 4x L2). Also times the in-step interference experiment
+smaller than 4x L2; those cases are also timed pipelined: one CUDA graph of
+back-to-back launches over rotating copies totalling >= 3x L2, which removes
+the ~6 us CUDA-event floor). Also times the in-step interference experiment
 (transpose and reduce alternating vs. isolated vs. CUDA-graph captured).
 
 usage: python tools/sweep_c5.py  -> gpurun_out/sweep_c5.json
@@ -45,6 +47,35 @@ def timeit(fn, nbytes, reps=REPS):
     return statistics.median(ts), do_flush
 
 
+def pipelined(make, nbytes, K_min=32):
+    """Per-launch time inside one CUDA graph of back-to-back launches over R rotating
+    copies (inputs + outputs) of the case; cold when R * nbytes >= 3x L2 (R <= 64)."""
+    R = int(min(64, max(2, -(-3 * L2 // max(nbytes, 1)))))
+    fns = [make() for _ in range(R)]
+    K = max(2 * R, K_min)
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        for f in fns:
+            f()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=st):
+        for i in range(K):
+            fns[i % R]()
+    ts = []
+    for i in range(7):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        if i >= 2:
+            ts.append(e0.elapsed_time(e1) / K)
+    del g, fns
+    torch.cuda.empty_cache()
+    return statistics.median(ts), R, R * nbytes >= 3 * L2
+
+
 def rec(**kw):
     results.append(kw)
     print(json.dumps(kw), flush=True)
@@ -70,8 +101,16 @@ def reductions():
             else:
                 exact, absum = oracle.sum_f64(xh)
                 ok = abs(got - exact) <= oracle.f32_tolerance(n, exact, absum)
+            extra = {}
+            if fl:
+                def make(x=x, out=out):
+                    xc, oc = x.clone(), torch.empty_like(out)
+                    return lambda: b2.reduce_sum(xc, out=oc)
+                pms, R, cold = pipelined(make, nbytes)
+                extra = dict(us_pipelined=pms * 1e3, GBps_pipelined=nbytes / pms / 1e6, rotating=R,
+                             pipelined_cold=cold)
             rec(what="reduce", dtype=dt, n=n, log2n=k, ms=ms, us=ms * 1e3, GBps=nbytes / ms / 1e6,
-                l2_flushed=fl, parity=bool(ok))
+                l2_flushed=fl, parity=bool(ok), **extra)
             del x, xh
             torch.cuda.empty_cache()
 
@@ -88,8 +127,16 @@ def transposes():
             nbytes = 2 * a.numel() * a.element_size()
             ms, fl = timeit(lambda: b2.transpose(a, o), nbytes)
             ok = np.array_equal(o.view(iv).cpu().numpy(), oracle.transpose(a.view(iv).cpu().numpy()))
+            extra = {}
+            if fl and nbytes:
+                def make(a=a):
+                    ac, oc = a.clone(), torch.empty((a.shape[1], a.shape[0]), device=dev, dtype=a.dtype)
+                    return lambda: b2.transpose(ac, oc)
+                pms, R, cold = pipelined(make, nbytes)
+                extra = dict(us_pipelined=pms * 1e3, GBps_pipelined=nbytes / pms / 1e6, rotating=R,
+                             pipelined_cold=cold)
             rec(what="transpose", dtype=dtn, shape=[H, W], ms=ms, us=ms * 1e3, GBps=nbytes / ms / 1e6,
-                l2_flushed=fl, parity=bool(ok))
+                l2_flushed=fl, parity=bool(ok), **extra)
             del a, o
     torch.cuda.empty_cache()
 

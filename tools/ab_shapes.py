@@ -28,6 +28,7 @@ def timeit(fn, reps=20):
 out = {"lib": os.path.basename(_lib.LIB_PATH)}
 for dt, (R, C) in [(torch.float32, (8192, 16384)), (torch.float32, (16384, 8192)), (torch.float32, (4096, 32768)),
                    (torch.float32, (16384, 16384)), (torch.float32, (32768, 32768)), (torch.bfloat16, (16384, 16384)),
+                   (torch.bfloat16, (8192, 16384)), (torch.bfloat16, (4096, 32768)), (torch.bfloat16, (16384, 8192)),
                    (torch.float64, (8192, 8192))]:
     a = torch.empty((R, C), device="cuda", dtype=dt).uniform_()
     o = torch.empty((C, R), device="cuda", dtype=dt)

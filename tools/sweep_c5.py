@@ -3,9 +3,10 @@ int32) and odd / non-square transposes (bf16, fp32, fp64), each checked
 against the CPU oracle, timed with CUDA events (median of REPS after warm-up,
 L2 flushed by a 252 MB read pass (clean lines, no write-back inside the timed
 kernel) before every launch when the working set is
-smaller than 4x L2; those cases are also timed pipelined: one CUDA graph of
-back-to-back launches over rotating copies totalling >= 3x L2, which removes
-the ~6 us CUDA-event floor). Also times the in-step interference experiment
+smaller than 4x L2). Every case is also timed pipelined: one CUDA graph of
+back-to-back launches over R >= 2 rotating copies totalling >= 3x L2, which
+removes the ~6 us CUDA-event floor and includes the write-back of the previous
+launch's dirty lines, i.e. the steady state of a stream of launches. Also times the in-step interference experiment
 (transpose and reduce alternating vs. isolated vs. CUDA-graph captured).
 
 usage: python tools/sweep_c5.py  -> gpurun_out/sweep_c5.json
@@ -24,7 +25,7 @@ import paper_2605_13864_b200 as b2  # noqa: E402
 from oracle import oracle  # noqa: E402  (checker only)
 
 L2 = 126 * 1024 * 1024
-REPS = 15
+REPS = 100  # >= 100 timed reps, median and best reported
 dev = torch.device("cuda", 0)
 flush = torch.ones(2 * L2 // 4, dtype=torch.float32, device=dev)
 results = []
@@ -44,10 +45,10 @@ def timeit(fn, nbytes, reps=REPS):
         e1.record()
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
-    return statistics.median(ts), do_flush
+    return statistics.median(ts), min(ts), do_flush
 
 
-def pipelined(make, nbytes, K_min=32):
+def pipelined(make, nbytes, K_min=8):
     """Per-launch time inside one CUDA graph of back-to-back launches over R rotating
     copies (inputs + outputs) of the case; cold when R * nbytes >= 3x L2 (R <= 64)."""
     R = int(min(64, max(2, -(-3 * L2 // max(nbytes, 1)))))
@@ -93,7 +94,7 @@ def reductions():
                 x = torch.empty(n, dtype=torch.float32, device=dev).uniform_(-1, 1)
                 out = torch.empty(1, dtype=torch.float32, device=dev)
             nbytes = n * 4 + out.element_size()
-            ms, fl = timeit(lambda: b2.reduce_sum(x, out=out), nbytes)
+            ms, best, fl = timeit(lambda: b2.reduce_sum(x, out=out), nbytes)
             got = out.item()
             xh = x.cpu().numpy()
             if dt == "int32":
@@ -101,15 +102,15 @@ def reductions():
             else:
                 exact, absum = oracle.sum_f64(xh)
                 ok = abs(got - exact) <= oracle.f32_tolerance(n, exact, absum)
-            extra = {}
-            if fl:
-                def make(x=x, out=out):
-                    xc, oc = x.clone(), torch.empty_like(out)
-                    return lambda: b2.reduce_sum(xc, out=oc)
-                pms, R, cold = pipelined(make, nbytes)
-                extra = dict(us_pipelined=pms * 1e3, GBps_pipelined=nbytes / pms / 1e6, rotating=R,
-                             pipelined_cold=cold)
-            rec(what="reduce", dtype=dt, n=n, log2n=k, ms=ms, us=ms * 1e3, GBps=nbytes / ms / 1e6,
+
+            def make(x=x, out=out):
+                xc, oc = x.clone(), torch.empty_like(out)
+                return lambda: b2.reduce_sum(xc, out=oc)
+            pms, R, cold = pipelined(make, nbytes)
+            extra = dict(us_pipelined=pms * 1e3, GBps_pipelined=nbytes / pms / 1e6, rotating=R,
+                         pipelined_cold=cold)
+            rec(what="reduce", dtype=dt, n=n, log2n=k, ms=ms, us=ms * 1e3, GBps=nbytes / ms / 1e6, best_us=best * 1e3,
+                GBps_best=nbytes / best / 1e6,
                 l2_flushed=fl, parity=bool(ok), **extra)
             del x, xh
             torch.cuda.empty_cache()
@@ -125,10 +126,10 @@ def transposes():
             a = torch.empty((H, W), device=dev, dtype=dt).uniform_(-1, 1)
             o = torch.empty((W, H), device=dev, dtype=dt)
             nbytes = 2 * a.numel() * a.element_size()
-            ms, fl = timeit(lambda: b2.transpose(a, o), nbytes)
+            ms, best, fl = timeit(lambda: b2.transpose(a, o), nbytes)
             ok = np.array_equal(o.view(iv).cpu().numpy(), oracle.transpose(a.view(iv).cpu().numpy()))
             extra = {}
-            if fl and nbytes:
+            if nbytes:
                 def make(a=a):
                     ac, oc = a.clone(), torch.empty((a.shape[1], a.shape[0]), device=dev, dtype=a.dtype)
                     return lambda: b2.transpose(ac, oc)
@@ -136,6 +137,7 @@ def transposes():
                 extra = dict(us_pipelined=pms * 1e3, GBps_pipelined=nbytes / pms / 1e6, rotating=R,
                              pipelined_cold=cold)
             rec(what="transpose", dtype=dtn, shape=[H, W], ms=ms, us=ms * 1e3, GBps=nbytes / ms / 1e6,
+                best_us=best * 1e3, GBps_best=nbytes / best / 1e6,
                 l2_flushed=fl, parity=bool(ok), **extra)
             del a, o
     torch.cuda.empty_cache()

@@ -35,6 +35,7 @@ TILE_ROWS, TILE_COLS = 32768, 32768
 RED_N = 1 << 30
 L2_BYTES = 126 * 1024 * 1024
 FALLBACK_HBM = 6650.0
+NOMINAL_HBM = 8000.0  # B200 HBM3e datasheet figure (north star: 'the ~8 TB/s HBM3e peak')
 
 
 def parse():
@@ -440,7 +441,8 @@ def main():
                                 if (rows // 256) * (cols // 128) >= 8 * 148 else
                                 "transpose_vec_kernel<4,16,16,256> (64x64 fp32 tile)"),
                      "achieved": ach_t, "peak": peak, "unit": "GB/s", "frac": ach_t / peak,
-                     "traffic": traffic, "algorithmic_bytes": bytes_t, "peak_source": peak_src},
+                     "traffic": traffic, "algorithmic_bytes": bytes_t, "peak_source": peak_src,
+                     "frac_nominal_8TBs": ach_t / NOMINAL_HBM},
         "kernels": {
             "transpose": {"ms": ms_t, "GBps": ach_t, "frac": ach_t / peak, "bytes": bytes_t,
                           "traffic": traffic},
@@ -451,7 +453,8 @@ def main():
         "value_kernels_only": value_k,
         # north star: whole-job GB/s as a fraction of the aggregate HBM roofline (N x peak)
         "aggregate_roofline": {"peak": peak * world, "unit": "GB/s", "frac": value / (peak * world),
-                               "frac_kernels_only": value_k / (peak * world)},
+                               "frac_kernels_only": value_k / (peak * world),
+                               "frac_nominal_8TBs": value / (NOMINAL_HBM * world)},
         "launch_mode": ("CUDA graph: K steps captured once, replayed once in the timed region"
                         if use_graph else "eager stream launches"),
         "clocks": clk.summary(),

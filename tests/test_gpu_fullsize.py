@@ -56,3 +56,28 @@ def test_c5_int32_sum_2_32(b2):
     assert int(b2.reduce_sum(x).item()) == (2**31 - 1) * n
     del x
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("dt,rows,cols", [
+    (torch.int16, 32768, 65536),   # bf16-sized cells, 2^31 elements (32-bit index overflow)
+    (torch.int64, 16384, 32768),   # fp64-sized cells, 4 GiB per side
+    (torch.int16, 46341, 46343),   # odd pitches past 2^31 elements: the padded scalar tile
+])
+def test_big_transposes_involution_and_checksums(b2, dt, rows, cols):
+    """Transposes past 2^31 elements / 4 GiB for the 2- and 8-byte cell paths:
+    checksum of checksums (row sums of A = column sums of A^T, exact in int64),
+    involution, and a sampled tile against the CPU oracle."""
+    g = torch.Generator(device="cuda").manual_seed(rows + cols)
+    info = torch.iinfo(dt)
+    bits = torch.randint(info.min, info.max, (rows, cols), device="cuda", dtype=dt, generator=g)
+    t = b2.transpose(bits)
+    assert torch.equal(bits.sum(dim=1, dtype=torch.int64), t.sum(dim=0, dtype=torch.int64))
+    assert torch.equal(bits.sum(dim=0, dtype=torch.int64), t.sum(dim=1, dtype=torch.int64))
+    r0, c0 = rows - 77, cols - 91
+    blk = bits[r0:, c0:].cpu().numpy()
+    assert np.array_equal(t[c0:, r0:].cpu().numpy(), oracle.transpose(blk))
+    tt = b2.transpose(t)
+    del t
+    assert torch.equal(tt, bits)
+    del tt, bits
+    torch.cuda.empty_cache()

@@ -81,3 +81,17 @@ def test_big_transposes_involution_and_checksums(b2, dt, rows, cols):
     assert torch.equal(tt, bits)
     del tt, bits
     torch.cuda.empty_cache()
+
+
+def test_c5_fp32_sum_2_32(b2):
+    """fp32 sum at the top of the C5 sweep (16 GiB), within the north-star tolerance
+    of an independent float64 device sum (oracle.f32_tolerance)."""
+    n = 1 << 32
+    g = torch.Generator(device="cuda").manual_seed(32)
+    x = torch.empty(n, device="cuda", dtype=torch.float32).uniform_(-1, 1, generator=g)
+    got = float(b2.reduce_sum(x).item())
+    exact = sum(float(c.sum(dtype=torch.float64).item()) for c in x.split(1 << 28))
+    absum = sum(float(c.abs().sum(dtype=torch.float64).item()) for c in x.split(1 << 28))
+    assert abs(got - exact) <= oracle.f32_tolerance(n, exact, absum)
+    del x
+    torch.cuda.empty_cache()

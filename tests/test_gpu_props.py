@@ -69,3 +69,58 @@ def test_tree512_bit_exact(blocks, seed):
     t = torch.from_numpy(x).cuda()
     assert np.array_equal(b2.reduce_tree512_partials(t).cpu().numpy().view(np.uint32), parts.view(np.uint32))
     assert np.float32(b2.reduce_tree512(t)).view(np.uint32) == np.float32(want).view(np.uint32)
+
+
+HOST_DTYPES = [np.uint8, np.uint16, np.float32, np.int32, np.float64, np.int64]
+
+
+@settings(**SETTINGS)
+@given(rows=st.integers(1, 1500), cols=st.integers(1, 1500), dt=st.sampled_from(HOST_DTYPES),
+       pad_in=st.integers(0, 9), pad_out=st.integers(0, 9), off=st.integers(0, 3),
+       chunk_mb=st.sampled_from([1, 2, 64]), seed=st.integers(0, 2**31))
+def test_transpose_host_pipeline(rows, cols, dt, pad_in, pad_out, off, chunk_mb, seed):
+    """b2_transpose_host on pageable numpy views (pitched rows, misaligned bases),
+    with small staging chunks so the 2-D block pipeline runs many stages: bit-exact
+    against the C oracle, the output view's padding untouched."""
+    from paper_2605_13864_b200 import _lib
+    rng = np.random.default_rng(seed)
+    es = np.dtype(dt).itemsize
+    ubits = {1: np.uint8, 2: np.uint16, 4: np.uint32, 8: np.uint64}[es]
+    raw = rng.integers(0, 2**(8 * es) - 1, rows * (cols + pad_in) + off, dtype=np.uint64).astype(ubits)
+    a = raw[off:].reshape(rows, cols + pad_in)[:, :cols].view(dt)
+    out_raw = np.full(cols * (rows + pad_out) + off, 7, dtype=ubits)
+    o = out_raw[off:].reshape(cols, rows + pad_out)[:, :rows].view(dt)
+    _lib.tune("host.chunk_mb", chunk_mb)
+    try:
+        b2.transpose(a, o)
+    finally:
+        _lib.tune("host.chunk_mb", 0)
+    assert np.array_equal(o.view(ubits), oracle.transpose(np.ascontiguousarray(a.view(ubits))))
+    pad = out_raw[off:].reshape(cols, rows + pad_out)[:, rows:]
+    assert (pad == 7).all() and (out_raw[:off] == 7).all()
+
+
+@settings(**SETTINGS)
+@given(n=st.integers(0, 4_000_000), off=st.integers(0, 7), dt=st.sampled_from([np.int32, np.int64, np.float32]),
+       chunk_mb=st.sampled_from([1, 64]), seed=st.integers(0, 2**31))
+def test_reduce_host_pipeline(n, off, dt, chunk_mb, seed):
+    """b2_reduce_sum_host on pageable, misaligned host arrays, chunked: int32 / int64
+    exact (128-bit for int64), fp32 within the north-star tolerance."""
+    from paper_2605_13864_b200 import _lib
+    rng = np.random.default_rng(seed)
+    if dt == np.float32:
+        x = rng.uniform(-1, 1, n + off).astype(np.float32)[off:]
+    elif dt == np.int32:
+        x = rng.integers(-2**31, 2**31, n + off, dtype=np.int64).astype(np.int32)[off:]
+    else:
+        x = rng.integers(-2**63, 2**63 - 1, n + off, dtype=np.int64)[off:]
+    _lib.tune("host.chunk_mb", chunk_mb)
+    try:
+        got = b2.reduce_sum(x)
+    finally:
+        _lib.tune("host.chunk_mb", 0)
+    if dt == np.float32:
+        exact, absum = oracle.sum_f64(x)
+        assert abs(got - exact) <= oracle.f32_tolerance(max(n, 1), exact, absum)
+    else:
+        assert got == (int(x.astype(object).sum()) if dt == np.int64 else int(x.astype(np.int64).sum()))

@@ -374,6 +374,7 @@ def main():
     torch.cuda.synchronize()
     launches0 = b2.launch_count()
     w0 = time.perf_counter()
+    torch.cuda.nvtx.range_push("bench.timed_region")
     if use_graph:
         graph.replay()
     else:
@@ -382,6 +383,7 @@ def main():
             step(evs[i])
         t_end.record(st)
     torch.cuda.synchronize()
+    torch.cuda.nvtx.range_pop()
     w1 = time.perf_counter()
     if world > 1:
         dist.barrier()

@@ -7,9 +7,20 @@
 #include <atomic>
 #include <string>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX3: ranges cost a null check without a tool
+
 #include "../../include/b2k.h"
 
 namespace b2 {
+
+// NVTX range around an ABI entry point (visible in ncu --nvtx / nsys timelines)
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange &) = delete;
+    NvtxRange &operator=(const NvtxRange &) = delete;
+};
+#define B2_NVTX(name) ::b2::NvtxRange b2_nvtx_range_(name)
 
 // ---- error state (thread-local message, integer codes at the ABI) ----------
 void set_error(const std::string &msg);

@@ -353,6 +353,7 @@ size_t b2_dtype_size(int dtype) {
 
 int b2_transpose(const void *in, void *out, int64_t rows, int64_t cols, int64_t ld_in,
                  int64_t ld_out, int dtype, int dev, void *stream) {
+    B2_NVTX("b2_transpose");
     const int E = esize_of(dtype);
     if (!E) return fail(B2_ERR_UNSUPPORTED, "transpose: unknown dtype " + std::to_string(dtype));
     if (rows < 0 || cols < 0) return fail(B2_ERR_INVALID, "transpose: negative extent");
@@ -372,6 +373,7 @@ size_t b2_reduce_ws_bytes(int64_t n, int dtype) {
 
 int b2_reduce_sum(const void *in, int64_t n, int dtype, void *out, void *ws, size_t ws_bytes,
                   int dev, void *stream) {
+    B2_NVTX("b2_reduce_sum");
     if (n < 0) return fail(B2_ERR_INVALID, "reduce: negative length");
     if ((!in && n) || !out) return fail(B2_ERR_INVALID, "reduce: NULL buffer");
     if (int rc = check_dev(dev)) return rc;
@@ -387,6 +389,7 @@ int b2_reduce_sum(const void *in, int64_t n, int dtype, void *out, void *ws, siz
 
 int b2_reduce_tree_partials(const float *in, int64_t n, int block, float *partials, int dev,
                             void *stream) {
+    B2_NVTX("b2_reduce_tree_partials");
     if (!in || !partials) return fail(B2_ERR_INVALID, "tree: NULL buffer");
     if (int rc = check_dev(dev)) return rc;
     return launch_tree(in, n, block, partials, dev, (cudaStream_t)stream);
@@ -407,6 +410,7 @@ static int tree_args(int64_t n, int block) {
 }
 
 int b2_reduce_tree(const float *in, int64_t n, int block, float *result_host, int dev, void *stream) {
+    B2_NVTX("b2_reduce_tree");
     if (!in || !result_host) return fail(B2_ERR_INVALID, "tree: NULL buffer");
     if (int rc = tree_args(n, block)) return rc;
     if (int rc = check_dev(dev)) return rc;
@@ -432,6 +436,7 @@ int b2_reduce_tree512(const float *in, int64_t n, float *result_host, int dev, v
 }
 
 int b2_reduce_tree_host(const float *in_host, int64_t n, int block, float *result_host, int dev) {
+    B2_NVTX("b2_reduce_tree_host");
     if (!in_host || !result_host) return fail(B2_ERR_INVALID, "tree: NULL buffer");
     if (int rc = tree_args(n, block)) return rc;
     if (int rc = check_dev(dev)) return rc;
@@ -520,6 +525,7 @@ int b2_mailbox_status(void *mailbox, int dev, uint64_t *status) {
 
 int b2_reduce_sum_fused(const void *in, int64_t n, int dtype, void *out, void *ws, size_t ws_bytes,
                         void *mailbox, int rank, int nranks, uint64_t epoch, int dev, void *stream) {
+    B2_NVTX("b2_reduce_sum_fused");
     if (n < 0) return fail(B2_ERR_INVALID, "reduce: negative length");
     if ((!in && n) || !out || !mailbox) return fail(B2_ERR_INVALID, "reduce: NULL buffer");
     if (int rc = check_dev(dev)) return rc;
@@ -610,6 +616,7 @@ int b2_device_free(void *p, int dev) {
 
 // ------------------------------------------------------------ bulk copies
 int b2_copy_h2d(void *dst_dev, const void *src_host, size_t bytes, int dev) {
+    B2_NVTX("b2_copy_h2d");
     if (!bytes) return B2_OK;
     if (!dst_dev || !src_host) return fail(B2_ERR_INVALID, "copy: NULL buffer");
     if (int rc = check_dev(dev)) return rc;
@@ -636,6 +643,7 @@ int b2_copy_h2d(void *dst_dev, const void *src_host, size_t bytes, int dev) {
 }
 
 int b2_copy_d2h(void *dst_host, const void *src_dev, size_t bytes, int dev) {
+    B2_NVTX("b2_copy_d2h");
     if (!bytes) return B2_OK;
     if (!dst_host || !src_dev) return fail(B2_ERR_INVALID, "copy: NULL buffer");
     if (int rc = check_dev(dev)) return rc;
@@ -673,6 +681,7 @@ int b2_copy_d2h(void *dst_host, const void *src_dev, size_t bytes, int dev) {
 // ------------------------------------------------------------ host pipelines
 int b2_transpose_host(const void *in_host, void *out_host, int64_t rows, int64_t cols,
                       int64_t ld_in, int64_t ld_out, int dtype, int dev) {
+    B2_NVTX("b2_transpose_host");
     const int E = esize_of(dtype);
     if (!E) return fail(B2_ERR_UNSUPPORTED, "transpose: unknown dtype " + std::to_string(dtype));
     if (rows < 0 || cols < 0) return fail(B2_ERR_INVALID, "transpose: negative extent");
@@ -757,6 +766,7 @@ int b2_transpose_host(const void *in_host, void *out_host, int64_t rows, int64_t
 }
 
 int b2_reduce_sum_host(const void *in_host, int64_t n, int dtype, void *out_host, int dev) {
+    B2_NVTX("b2_reduce_sum_host");
     const int E = esize_of(dtype);
     if (dtype != B2_F32 && dtype != B2_I32 && dtype != B2_F64 && dtype != B2_I64)
         return fail(B2_ERR_UNSUPPORTED, "reduce: dtype must be B2_F32, B2_I32, B2_I64 or B2_F64");
@@ -905,6 +915,7 @@ int b2_peer_access(int from, int to) {
 
 int b2_transpose_multi(const void *const *in, void *const *out, const int64_t *rows, int64_t cols,
                        const int64_t *ld_in, const int64_t *ld_out, int dtype, int nshards) {
+    B2_NVTX("b2_transpose_multi");
     const int E = esize_of(dtype);
     if (!E) return fail(B2_ERR_UNSUPPORTED, "transpose: unknown dtype " + std::to_string(dtype));
     if (nshards <= 0 || nshards > kMaxShards || !in || !out || !rows || !ld_in || !ld_out)
@@ -950,6 +961,7 @@ int b2_transpose_multi(const void *const *in, void *const *out, const int64_t *r
 
 int b2_reduce_sum_multi(const void *const *shards, const int64_t *n, int nshards, int dtype,
                         void *host_out) {
+    B2_NVTX("b2_reduce_sum_multi");
     if (dtype != B2_F32 && dtype != B2_I32 && dtype != B2_F64)
         return fail(B2_ERR_UNSUPPORTED, "reduce: dtype must be B2_F32, B2_I32 or B2_F64");
     if (nshards <= 0 || nshards > kMaxShards || !shards || !n || !host_out)

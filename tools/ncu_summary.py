@@ -102,6 +102,13 @@ def main(tag):
                 "mean_dram_bytes": sum(m.get("dram__bytes_read.sum", 0) + m.get("dram__bytes_write.sum", 0)
                                        for m in ms) / len(ms)}
             for k, ms in per.items() if "b2::" in k or "--all" in sys.argv}
+        # the bench STEP = the C4 transpose + the C3 reduction (the >= 1 GB launches);
+        # their share of it is what the in-step CUDA events must agree with (the
+        # paper_configs' small latency-bound launches also appear in the list)
+        step = {k: v for k, v in summary["launch_list"].items() if v["mean_dram_bytes"] >= 1e9}
+        tot_step = sum(v["mean_ns"] for v in step.values())
+        for k, v in step.items():
+            v["share_of_bench_step"] = v["mean_ns"] / tot_step
     with open(os.path.join(PROF, f"{tag}_ncu.json"), "w") as f:
         json.dump(summary, f, indent=1)
     with open(os.path.join(PROF, "ncu_summary.json"), "w") as f:

@@ -1,0 +1,58 @@
+"""Static SASS properties of the built library (no GPU needed: cuobjdump of the
+in-tree libb200k.so): the default kernels keep their 128-bit loads, 256-bit
+evict-first stores and swizzled 128-bit shared-memory traffic, and nothing spills."""
+import os
+import shutil
+import subprocess
+
+import pytest
+
+from conftest import ROOT
+
+LIB = os.path.join(ROOT, "paper_2605_13864_b200", "libb200k.so")
+pytestmark = pytest.mark.skipif(not (os.path.exists(LIB) and shutil.which("cuobjdump")),
+                                reason="needs the built library and cuobjdump")
+
+
+@pytest.fixture(scope="module")
+def table():
+    import sys
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    import sass_evidence
+    sass = subprocess.run(["cuobjdump", "-sass", LIB], capture_output=True, text=True).stdout
+    res = subprocess.run(["cuobjdump", "--dump-resource-usage", LIB], capture_output=True, text=True).stdout
+    funcs, cur = {}, None
+    for ln in sass.splitlines():
+        if "Function : " in ln:
+            cur = ln.split("Function : ")[1].strip()
+            funcs[cur] = []
+        elif cur:
+            funcs[cur].append(ln)
+    dem = dict(zip(funcs, sass_evidence.demangle(list(funcs))))
+    return funcs, dem, res
+
+
+def _body(table, prefix):
+    funcs, dem, _ = table
+    hits = [k for k, d in dem.items() if prefix in d]
+    assert hits, prefix
+    return "\n".join(funcs[hits[0]])
+
+
+def test_bench_transpose_vector_memory_ops(table):
+    for k in ("transpose_vec_kernel<4, 64, 32, 512>", "transpose_vec_kernel<8, 128, 32, 512>"):
+        b = _body(table, k)
+        assert "LDG.E.NA.128" in b and ".EFL2.256" in b, k
+        assert "STS.128" in b and "LDS.128" in b, k
+
+
+def test_reduce_vector_loads_and_shuffles(table):
+    b = _body(table, "reduce_kernel<int, 512, 4, 1>")
+    assert "LDG.E.NA.128" in b and "SHFL.DOWN" in b and "BAR.SYNC" in b
+
+
+def test_no_register_spills(table):
+    _, _, res = table
+    assert "LOCAL:" in res
+    spills = [ln for ln in res.splitlines() if "LOCAL:" in ln and "LOCAL:0 " not in ln]
+    assert not spills, spills[:3]

@@ -120,7 +120,9 @@ PRELUDE = r"""
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
+#include <algorithm>
 #include <string>
 #include <vector>
 
@@ -163,6 +165,55 @@ __device__ __forceinline__ bool b2_chk(int64_t ix, int64_t d, int *f) {
     if (ix < 0 || ix >= d) { b2_flag(f, B2E_OOB, ix, d); return false; }
     return true;
 }
+// kernels are templates on B2CK: the checked instantiation is the interpreter's
+// semantics; the unchecked one is launched only when the host has proved, for this
+// concrete launch, that every access is in bounds (b2i_* below), so the checks
+// could never fire
+#define B2_CHK(ix, d) (!B2CK || b2_chk((ix), (d), b2_err))
+// launch-time bounds proofs: interval evaluation of a kernel's index expressions
+// over its loop ranges (values kept within +-2^62 so the arithmetic cannot wrap);
+// anything not provable (data-dependent indices, reassigned locals, inexact
+// exact_div, non-constant divisors) abandons the proof -> checked kernel
+struct B2NoProof {};
+struct B2I { int64_t lo, hi; };
+static const int64_t B2I_BIG = (int64_t)1 << 62;
+static inline B2I b2i_fit(__int128 lo, __int128 hi) {
+    if (lo < -(__int128)B2I_BIG || hi > (__int128)B2I_BIG) throw B2NoProof{};
+    return B2I{(int64_t)lo, (int64_t)hi};
+}
+static inline B2I b2i_c(int64_t v) { return b2i_fit(v, v); }
+static inline B2I b2i_unknown() { throw B2NoProof{}; }
+static inline B2I b2i_add(B2I a, B2I b) { return b2i_fit((__int128)a.lo + b.lo, (__int128)a.hi + b.hi); }
+static inline B2I b2i_sub(B2I a, B2I b) { return b2i_fit((__int128)a.lo - b.hi, (__int128)a.hi - b.lo); }
+static inline B2I b2i_mul(B2I a, B2I b) {
+    __int128 c[4] = {(__int128)a.lo * b.lo, (__int128)a.lo * b.hi, (__int128)a.hi * b.lo, (__int128)a.hi * b.hi};
+    __int128 lo = c[0], hi = c[0];
+    for (int i = 1; i < 4; ++i) { lo = c[i] < lo ? c[i] : lo; hi = c[i] > hi ? c[i] : hi; }
+    return b2i_fit(lo, hi);
+}
+static inline B2I b2i_div(B2I a, B2I b) {  // truncating, non-negative dividend, constant positive divisor
+    if (b.lo != b.hi || b.lo <= 0 || a.lo < 0) throw B2NoProof{};
+    return B2I{a.lo / b.lo, a.hi / b.lo};
+}
+static inline B2I b2i_mod(B2I a, B2I b) {
+    if (b.lo != b.hi || b.lo <= 0 || a.lo < 0) throw B2NoProof{};
+    return a.hi < b.lo ? a : B2I{0, b.lo - 1};
+}
+static inline B2I b2i_exact_div(B2I a, B2I b) {
+    if (b.lo != b.hi || b.lo <= 0) throw B2NoProof{};
+    if (a.lo == a.hi && a.lo % b.lo != 0) throw B2NoProof{};  // the kernel will raise: keep its checks
+    auto fl = [](int64_t x, int64_t d) { return x >= 0 ? x / d : -((-x + d - 1) / d); };
+    return B2I{fl(a.lo, b.lo), fl(a.hi, b.lo)};
+}
+static inline B2I b2i_pow2(B2I k) {  // monotonic: [2^lo, 2^hi]
+    if (k.lo < 0 || k.hi > 61) throw B2NoProof{};
+    return B2I{(int64_t)1 << k.lo, (int64_t)1 << k.hi};
+}
+static inline B2I b2i_join(B2I a, B2I b) { return B2I{a.lo < b.lo ? a.lo : b.lo, a.hi > b.hi ? a.hi : b.hi}; }
+static inline int b2i_in(B2I ix, int64_t d) {  // every value of ix indexes [0, d)
+    if (ix.lo < 0 || ix.hi >= d) throw B2NoProof{};
+    return 0;
+}
 template <typename T> struct B2Host { T *p = nullptr; int64_t n = 0; int64_t rank = 0; int64_t dims[8] = {0}; uint8_t *init = nullptr; bool freed = false; bool owned = false; };
 template <typename T> struct B2Dev { T *p = nullptr; int64_t n = 0; int64_t rank = 0; int64_t dims[8] = {0}; bool freed = false; };
 // kernel-only device time of the last launch of each kernel (PAPER.md:1100-1102
@@ -170,6 +221,10 @@ template <typename T> struct B2Dev { T *p = nullptr; int64_t n = 0; int64_t rank
 static float b2_kernel_ms[64];
 static cudaEvent_t b2_ev0, b2_ev1;
 extern "C" double b2g_kernel_ms(int k) { return (k >= 0 && k < 64) ? b2_kernel_ms[k] : -1.0; }
+// which instantiation each kernel's last launch used (1 = bounds proved, checks elided)
+static int b2_kernel_unchecked[64];
+extern "C" int b2g_kernel_unchecked(int k) { return (k >= 0 && k < 64) ? b2_kernel_unchecked[k] : -1; }
+static bool b2_prove_enabled() { const char *e = getenv("B2K_CODEGEN_PROVE"); return !(e && e[0] == '0'); }
 // Host runtime services from libb200k.so (include/b2k.h): staged / pinned bulk
 // copies, the caching device allocator, and the device this call runs on.
 struct B2Ops {
@@ -369,7 +424,7 @@ class _Gen:
         if len(codes) == s.rank + 1 and s.rank == 1:
             ix = self.fresh("ix")
             lines.append(f"const int64_t {ix} = {codes[0]} + {codes[1]};")
-            return f"b2_chk({ix}, {dims}[0], b2_err)", ix, lines
+            return f"B2_CHK({ix}, {dims}[0])", ix, lines
         if len(codes) != s.rank:
             raise UnsupportedProgram(f"rank mismatch on {s.name!r}: {len(codes)} indices into {s.rank}-d array")
         ok, off = [], "((int64_t)0)"
@@ -377,7 +432,7 @@ class _Gen:
         for k, cd in enumerate(codes):
             v = self.fresh("ix")
             lines.append(f"const int64_t {v} = {cd};")
-            ok.append(f"b2_chk({v}, {dims}[{k}], b2_err)")
+            ok.append(f"B2_CHK({v}, {dims}[{k}])")
             # shared arrays: the last dimension is stored with a padded pitch
             stride = f"{s.cname}_pitch" if (padded and k == s.rank - 1) else f"{dims}[{k}]"
             off = f"({off} * {stride} + {v})"
@@ -601,6 +656,7 @@ class _Gen:
         dl = []
         kctx.emit_seq(kbody, dl, 1, "b2_w0", "b2_rel0")
         self.kernels.append(kctx.render(dl))
+        proof = _Proof(self, kctx).run(kbody)
         # host launch
         args = kctx.host_args()
         out.extend(pad + ln for ln in host_lines)
@@ -609,10 +665,23 @@ class _Gen:
         out.append(pad + f"  if ({g} < 0 || {g} > 2147483647LL || {t} < 0 || {t} > 1024 || {g} * {t} >= (1LL << 32)) "
                    f"b2_throw(\"kernel_launch(\" + std::to_string({g}) + \", \" + std::to_string({t}) + \") exceeds the B200 launch limits\");")
         out.append(pad + f"  if ({g} > 0 && {t} > 0) {{")
-        out.append(pad + f"    if ({smem_bytes} > 48 * 1024) cudaFuncSetAttribute({name}, cudaFuncAttributeMaxDynamicSharedMemorySize, (int){smem_bytes});")
+        pv = self.fresh("proved")
+        out.append(pad + f"    bool {pv} = false;")
+        out.append(pad + "    if (b2_prove_enabled()) {")
+        out.append(pad + "      try {")
+        out.append(pad + "        [&]() {")
+        out.extend(pad + "          " + ln for ln in proof)
+        out.append(pad + "        }();")
+        out.append(pad + f"        {pv} = true;")
+        out.append(pad + "      } catch (B2NoProof &) {}")
+        out.append(pad + "    }")
+        out.append(pad + f"    b2_kernel_unchecked[{self.nk - 1}] = {pv} ? 1 : 0;")
+        out.append(pad + f"    if ({smem_bytes} > 48 * 1024) {{ cudaFuncSetAttribute({name}<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int){smem_bytes}); "
+                   f"cudaFuncSetAttribute({name}<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int){smem_bytes}); }}")
         out.append(pad + "    cudaMemset(b2_err_dev, 0, 5 * sizeof(int));")
         out.append(pad + "    cudaEventRecord(b2_ev0, 0);")
-        out.append(pad + f"    {name}<<<(unsigned){g}, (unsigned){t}, (size_t){smem_bytes}>>>({', '.join(args)});")
+        out.append(pad + f"    if ({pv}) {name}<false><<<(unsigned){g}, (unsigned){t}, (size_t){smem_bytes}>>>({', '.join(args)});")
+        out.append(pad + f"    else {name}<true><<<(unsigned){g}, (unsigned){t}, (size_t){smem_bytes}>>>({', '.join(args)});")
         out.append(pad + "    cudaEventRecord(b2_ev1, 0);")
         out.append(pad + f"    b2_check_kernel(b2_err_dev, \"{name}\");")
         out.append(pad + f"    {{ float ms = 0; cudaEventElapsedTime(&ms, b2_ev0, b2_ev1); b2_kernel_ms[{self.nk - 1}] = ms; }}")
@@ -723,7 +792,7 @@ class _KernelCtx:
         for s in treg:
             n = " * ".join(f"{s.cname}_d{k}" for k in range(s.rank)) or "1"
             pro.append(f"    {s.elem} {s.cname}[B2_TREG_MAX]; if (({n}) > B2_TREG_MAX) {{ b2_flag(b2_err, B2E_OOB, {n}, B2_TREG_MAX); return; }}")
-        out = [f"__global__ void {self.name}({', '.join(params)}) {{",
+        out = [f"template <bool B2CK> __global__ void {self.name}({', '.join(params)}) {{",
                "    extern __shared__ __align__(16) unsigned char b2_smem[];",
                "    const uint32_t b2_w0 = gridDim.x * blockDim.x;",
                "    const uint32_t b2_rel0 = blockIdx.x * blockDim.x + threadIdx.x;"]
@@ -863,6 +932,208 @@ class _KernelCtx:
         raise UnsupportedProgram(f"cannot compile statement {c} inside a kernel")
 
 
+class _Proof:
+    """Host code proving, for one concrete launch, that every array access of a
+    kernel is in bounds (then the unchecked instantiation runs). Mirrors the
+    kernel's statements with interval arithmetic (b2i_* in PRELUDE): a thread-for /
+    for variable ranges over [start.lo, stop.hi - 1], both branches of an `if` are
+    covered, captured host scalars are points. Throws B2NoProof (checked kernel)
+    on anything it cannot bound: values read from arrays, locals reassigned in the
+    kernel, inexact exact_div, non-constant divisors."""
+
+    def __init__(self, gen: "_Gen", kctx: "_KernelCtx"):
+        self.g = gen
+        self.k = kctx
+        self.locals: dict = {}     # kernel-local int name -> C++ interval variable, or None (unknown)
+        self.n = 0
+
+    def fresh(self):
+        self.n += 1
+        return f"_pi{self.n}"
+
+    def run(self, kbody):
+        self.reassigned, self.declared = set(), set()
+        self._scan(kbody)
+        out = []
+        self.seq(kbody, out)
+        return out
+
+    def _scan(self, stmts):
+        for st in stmts:
+            c = _cls(st)
+            if c == "Assign" and not self.g.syms.get(st.target.base, Sym("", "scalar", "int")).is_array:
+                self.reassigned.add(st.target.base)
+            if c == "Decl":  # declared twice (sibling scopes): do not trust either interval
+                if st.name in self.declared:
+                    self.reassigned.add(st.name)
+                self.declared.add(st.name)
+            for attr in ("body", "then", "els"):
+                sub = getattr(st, attr, None)
+                if sub is not None:
+                    self._scan(_stmts(sub))
+            if c == "Seq":
+                self._scan(st.stmts)
+
+    # expressions -> (C++ expression of type B2I, kind) with kind i (int interval),
+    # v (a value we cannot bound: array cell / float); both still evaluate every
+    # nested access check
+    def expr(self, e):
+        c = _cls(e)
+        if c == "IntLit":
+            return f"b2i_c({int(e.value)}LL)", "i"
+        if c == "FloatLit":
+            return "b2i_c(0)", "v"
+        if c == "Var":
+            if e.name in self.locals:
+                iv = self.locals[e.name]
+                if iv == "F":
+                    return "b2i_c(0)", "v"
+                return (iv, "i") if iv else ("b2i_unknown()", "i")
+            sc = self.k.scalars.get(e.name)
+            if sc is not None and sc.kind != "param_float" and sc.ctype != "float":
+                return f"b2i_c((int64_t){sc.cname})", "i"
+            return "b2i_c(0)", "v"
+        if c == "Access":
+            chk = self.access(e.base, e.idxs)
+            return f"({chk}, b2i_c(0))", "v"
+        if c == "BinOp":
+            a, ka = self.expr(e.lhs)
+            b, kb = self.expr(e.rhs)
+            if ka != "i" or kb != "i":
+                return f"((void){a}, (void){b}, b2i_c(0))", "v"
+            op = e.op
+            if op in ("==", "!=", "<", "<=", ">", ">="):
+                return f"((void){a}, (void){b}, B2I{{0, 1}})", "i"
+            fn = {"+": "b2i_add", "-": "b2i_sub", "*": "b2i_mul", "/": "b2i_div", "%": "b2i_mod"}.get(op)
+            if fn is None:
+                return "b2i_unknown()", "i"
+            return f"{fn}({a}, {b})", "i"
+        if c == "Call":
+            if e.fn == "exact_div":
+                a, ka = self.expr(e.args[0])
+                b, kb = self.expr(e.args[1])
+                if ka != "i" or kb != "i":
+                    return "b2i_unknown()", "i"
+                return f"b2i_exact_div({a}, {b})", "i"
+            if e.fn == "pow2":
+                a, ka = self.expr(e.args[0])
+                return (f"b2i_pow2({a})", "i") if ka == "i" else ("b2i_unknown()", "i")
+            if e.fn.startswith("DMINDEX"):
+                k = len(e.args) // 2
+                out = "b2i_c(0)"
+                for d, ix in zip(e.args[:k], e.args[k:]):
+                    dc, kd = self.expr(d)
+                    ic, ki = self.expr(ix)
+                    if kd != "i" or ki != "i":
+                        return "b2i_unknown()", "i"
+                    out = f"b2i_add(b2i_mul({out}, {dc}), {ic})"
+                return out, "i"
+        return "b2i_unknown()", "i"
+
+    def index(self, e):
+        code, kind = self.expr(e)
+        return code if kind == "i" else f"((void){code}, b2i_unknown())"
+
+    def access(self, base, idxs):
+        """C++ expression (int) checking every index of one access."""
+        sym = self.g.syms[base]
+        idxs = list(idxs)
+        if sym.kind in ("smem_arr", "treg_arr"):
+            idxs = idxs[1:]  # the DMINDEX block index: 0 in per-block storage
+            dims = f"{sym.cname}_hdims"
+        else:
+            dims = f"{sym.cname}.dims"
+        if len(idxs) == sym.rank + 1 and sym.rank == 1:
+            return f"b2i_in(b2i_add({self.index(idxs[0])}, {self.index(idxs[1])}), {dims}[0])"
+        if len(idxs) != sym.rank:
+            return "(b2i_unknown(), 0)"
+        return "(" + ", ".join(f"b2i_in({self.index(ix)}, {dims}[{k}])" for k, ix in enumerate(idxs)) + ")" \
+            if idxs else "0"
+
+    def refine(self, cond):
+        """(local name, narrowed interval expression) for `v OP e` / `e OP v` with v an
+        int local of known interval and e an int expression; else None."""
+        if _cls(cond) != "BinOp" or cond.op not in ("<", "<=", ">", ">=", "=="):
+            return None
+        flip = {"<": ">", "<=": ">=", ">": "<", ">=": "<=", "==": "=="}
+        for var, other, op in ((cond.lhs, cond.rhs, cond.op), (cond.rhs, cond.lhs, flip[cond.op])):
+            if _cls(var) == "Var" and self.locals.get(var.name) not in (None, "F") and var.name in self.locals:
+                e, kind = self.expr(other)
+                if kind != "i":
+                    return None
+                iv = self.locals[var.name]
+                lo, hi = f"{iv}.lo", f"{iv}.hi"
+                if op == "<":
+                    hi = f"std::min({iv}.hi, ({e}).hi - 1)"
+                elif op == "<=":
+                    hi = f"std::min({iv}.hi, ({e}).hi)"
+                elif op == ">":
+                    lo = f"std::max({iv}.lo, ({e}).lo + 1)"
+                elif op == ">=":
+                    lo = f"std::max({iv}.lo, ({e}).lo)"
+                else:
+                    lo, hi = f"std::max({iv}.lo, ({e}).lo)", f"std::min({iv}.hi, ({e}).hi)"
+                return var.name, f"B2I{{{lo}, {hi}}}"
+        return None
+
+    # statements
+    def seq(self, stmts, out):
+        for st in stmts:
+            if not _is_ghost(st):
+                self.stmt(st, out)
+
+    def stmt(self, st, out):
+        c = _cls(st)
+        if c == "Seq":
+            out.append("{")
+            self.seq(st.stmts, out)
+            out.append("}")
+        elif c == "For":
+            a, b = self.index(st.range.start), self.index(st.range.stop)
+            s0, s1, v = self.fresh(), self.fresh(), self.fresh()
+            out.append(f"{{ const B2I {s0} = {a}, {s1} = {b};")
+            out.append(f"  if ({s1}.hi > {s0}.lo) {{ const B2I {v} = B2I{{{s0}.lo, {s1}.hi - 1}};")
+            saved = self.locals.get(st.index, ...)
+            self.locals[st.index] = v
+            self.seq(st.body.stmts, out)
+            if saved is ...:
+                del self.locals[st.index]
+            else:
+                self.locals[st.index] = saved
+            out.append("} }")
+        elif c == "If":
+            out.append(f"(void){self.expr(st.cond)[0]};")
+            ref = self.refine(st.cond)
+            if ref is None:
+                self.seq(st.then.stmts, out)
+            else:  # `v < e` etc. on an int local: the then-branch sees v narrowed
+                name, code = ref
+                v, saved = self.fresh(), self.locals[name]
+                out.append(f"{{ const B2I {v} = {code};")
+                out.append(f"  if ({v}.lo <= {v}.hi) {{")
+                self.locals[name] = v
+                self.seq(st.then.stmts, out)
+                self.locals[name] = saved
+                out.append("} }")
+            if st.els is not None:
+                self.seq(st.els.stmts, out)
+        elif c == "Decl":
+            code, kind = self.expr(st.init)
+            if st.ctype == "int" and kind == "i" and st.name not in self.reassigned:
+                v = self.fresh()
+                out.append(f"const B2I {v} = {code};")
+                self.locals[st.name] = v
+            else:
+                out.append(f"(void){code};")
+                self.locals[st.name] = "F" if st.ctype == "float" else None
+        elif c == "Assign":
+            out.append(f"(void){self.expr(st.value)[0]};")
+            sym = self.g.syms.get(st.target.base)
+            if sym is not None and sym.is_array:
+                out.append(f"(void){self.access(st.target.base, st.target.idxs)};")
+        # CallStmt (blocksync): no access
+
+
 # ----------------------------------------------------------------------------- compile + run
 
 _NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17", "--fmad=false",
@@ -891,11 +1162,18 @@ class Compiled:
         self.lib.b2g_main.argtypes = [ctypes.c_void_p] * 9
         self.lib.b2g_kernel_ms.restype = ctypes.c_double
         self.lib.b2g_kernel_ms.argtypes = [ctypes.c_int]
+        self.lib.b2g_kernel_unchecked.restype = ctypes.c_int
+        self.lib.b2g_kernel_unchecked.argtypes = [ctypes.c_int]
         self.n_kernels = source.count("__global__ void b2g_kernel")
 
     def kernel_ms(self) -> list:
         """Device time (CUDA events) of each kernel's last launch, in ms."""
         return [self.lib.b2g_kernel_ms(k) for k in range(self.n_kernels)]
+
+    def kernel_unchecked(self) -> list:
+        """Per kernel: True if its last launch ran the check-free instantiation (all
+        accesses proved in bounds on the host for that launch)."""
+        return [self.lib.b2g_kernel_unchecked(k) == 1 for k in range(self.n_kernels)]
 
 
 class B2Ops(ctypes.Structure):

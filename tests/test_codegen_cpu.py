@@ -72,7 +72,10 @@ def test_a4_structure_like_spec_acceptance_1():
     assert kernel.count("__syncthreads();") == 1
     assert kernel.count("float *v_tile = (float *)(b2_smem") == 1
     assert "DMINDEX" not in src and "__ghost" not in src
-    assert host.count("<<<") == 1
+    # one launch site: the checked instantiation, or the check-free one when the
+    # host proved every access in bounds for the concrete launch
+    assert host.count("<true><<<") == 1 and host.count("<false><<<") == 1 and host.count("<<<") == 2
+    assert host.count("b2i_in(") >= 4 and "catch (B2NoProof &)" in host
     assert "b2_exact_div_h(v_W, ((int64_t)32LL)) * b2_exact_div_h(v_H, ((int64_t)32LL))" in host
     assert "(((int64_t)16LL) * ((int64_t)32LL))" in host  # 512 threads per block
     assert host.count("b2_dev_alloc<float>(") == 2

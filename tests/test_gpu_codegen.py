@@ -114,3 +114,40 @@ def test_auto_backend_routes_variants(b2):
     assert isinstance(ret, float)
     with pytest.raises(b2.UnsupportedProgram):
         b2.run_program(q, "reduce", {"arr": x.tolist(), "N": 2048}, backend="kernels")
+
+
+def test_bounds_proof_selects_check_free_kernels(b2, monkeypatch):
+    """Launch-time bounds proofs (codegen._Proof): the paper's programs and the
+    derived variants are proved in bounds for their concrete launches and run the
+    check-free instantiation with unchanged results; the out-of-bounds program is
+    not proved (its checked kernel reports the reference's error), and
+    B2K_CODEGEN_PROVE=0 forces the checked kernels."""
+    from paper_2605_13864_b200 import codegen
+    rng = np.random.default_rng(5)
+    H, W = 256, 192
+    a = rng.uniform(-1, 1, (H, W)).astype(np.float32)
+    x = rng.uniform(-1, 1, 4096).astype(np.float32)
+    xi = rng.integers(-1000, 1000, 4096).tolist()
+    cases = [("transpose_gpu.optc", "transpose", lambda: {"in": a.reshape(-1).tolist(), "out": [0.0] * (H * W),
+                                                          "W": W, "H": H}),
+             ("transpose_gpu_t64.optc", "transpose", lambda: {"in": a.reshape(-1).tolist(), "out": [0.0] * (H * W),
+                                                              "W": W, "H": H}),
+             ("reduce_tree_f32.optc", "reduce", lambda: {"arr": x.tolist(), "N": x.size}),
+             ("reduce_tree_int256.optc", "reduce", lambda: {"arr": xi, "N": len(xi)}),
+             ("scale_then_reduce.optc", "reduce", lambda: {"arr": x.tolist(), "N": x.size})]
+    for name, entry, inputs in cases:
+        p = _prog(b2, name)
+        c = codegen.compile_fn(p.fn(entry))
+        monkeypatch.setenv("B2K_CODEGEN_PROVE", "1")
+        got = b2.run_program(p, entry, inputs(), backend="codegen")
+        assert all(c.kernel_unchecked()), name
+        monkeypatch.setenv("B2K_CODEGEN_PROVE", "0")
+        want = b2.run_program(p, entry, inputs(), backend="codegen")
+        assert not any(c.kernel_unchecked()), name
+        assert got == want, name
+    monkeypatch.setenv("B2K_CODEGEN_PROVE", "1")
+    p = _prog(b2, "oob_kernel.optc")
+    c = codegen.compile_fn(p.fn("shift"))
+    with pytest.raises(b2.InterpError, match="out of bounds"):
+        b2.run_program(p, "shift", {"arr": [0.5] * 128, "N": 128}, backend="codegen")
+    assert not any(c.kernel_unchecked())

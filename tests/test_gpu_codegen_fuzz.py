@@ -84,3 +84,68 @@ def test_random_gpu_programs_codegen_vs_reference_semantics():
                               np.array(want["r"], np.float32).view(np.uint32)), src
         ran += 1
     assert refused >= 0
+
+
+def _gen_bounds(rng):
+    """A one-kernel program whose index expressions are sometimes out of bounds
+    (offsets, strides, guards, wrapped indices): the launch-time bounds proof must
+    never select the check-free kernel for a program the reference rejects."""
+    T = rng.choice([32, 64, 128])
+    B = rng.choice([1, 2, 5])
+    D = rng.choice([0, 0, 1, -1])
+    S = rng.choice([1, 1, 2])
+    E = rng.choice([0, 0, 3])
+    lim = rng.choice([T, T - 1, T // 2, T // S])
+    src_ix = f"b * {T} + t * {S} + {E}"
+    if rng.random() < 0.3:
+        src_ix = f"({src_ix}) % {rng.choice([B * T, B * T + 1, B * T - 1])}"
+    src = f"""void f(float* a, float* r, int N) {{
+    float* const d = gmem_malloc1<float>(N);
+    memcpy_host_to_device1(d, a, N);
+    float* const o = gmem_malloc1<float>(N);
+    memcpy_host_to_device1(o, r, N);
+    {{
+        kernel_launch({B}, {T}, 0);
+        kernel_setup_end();
+        thread for (int b = 0; b < {B}; b++) {{
+            thread for (int t = 0; t < {T}; t++) {{
+                if (t < {lim}) {{ o[b * {T} + t + {D}] = d[{src_ix}] * 2.0; }}
+            }}
+        }}
+        kernel_teardown_begin();
+        kernel_kill();
+    }}
+    memcpy_device_to_host1(r, o, N);
+    gmem_free(o);
+    gmem_free(d);
+}}
+"""
+    return src, B * T
+
+
+def test_random_bounds_programs_proof_is_sound():
+    from paper_2605_13864_b200 import codegen
+    rng = random.Random(11)
+    errors = proved = 0
+    for i in range(40):
+        src, n = _gen_bounds(rng)
+        p = b2.parse_program(src)
+        x = np.random.default_rng(i).uniform(-1, 1, n).astype(np.float32)
+        inputs = {"a": x.tolist(), "r": [0.0] * n, "N": n}
+        try:
+            _, want = vinterp.run_program(p, "f", dict(inputs))
+            ref_err = None
+        except Exception as e:  # noqa: BLE001 - the reference's error
+            ref_err = e
+        c = codegen.compile_fn(p.fn("f"))
+        if ref_err is not None:
+            with pytest.raises(b2.InterpError, match="out of bounds"):
+                b2.run_program(p, "f", dict(inputs), backend="codegen")
+            assert not any(c.kernel_unchecked()), src
+            errors += 1
+        else:
+            _, got = b2.run_program(p, "f", dict(inputs), backend="codegen")
+            assert np.array_equal(np.array(got["r"], np.float32).view(np.uint32),
+                                  np.array(want["r"], np.float32).view(np.uint32)), src
+            proved += all(c.kernel_unchecked())
+    assert errors >= 5 and proved >= 5, (errors, proved)

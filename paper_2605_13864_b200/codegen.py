@@ -675,7 +675,8 @@ class _Gen:
         out.append(pad + f"        {pv} = true;")
         out.append(pad + "      } catch (B2NoProof &) {}")
         out.append(pad + "    }")
-        out.append(pad + f"    b2_kernel_unchecked[{self.nk - 1}] = {pv} ? 1 : 0;")
+        if self.nk <= 64:  # per-kernel evidence for the first 64 kernels of a program
+            out.append(pad + f"    b2_kernel_unchecked[{self.nk - 1}] = {pv} ? 1 : 0;")
         out.append(pad + f"    if ({smem_bytes} > 48 * 1024) {{ cudaFuncSetAttribute({name}<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int){smem_bytes}); "
                    f"cudaFuncSetAttribute({name}<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int){smem_bytes}); }}")
         out.append(pad + "    cudaMemset(b2_err_dev, 0, 5 * sizeof(int));")
@@ -684,7 +685,8 @@ class _Gen:
         out.append(pad + f"    else {name}<true><<<(unsigned){g}, (unsigned){t}, (size_t){smem_bytes}>>>({', '.join(args)});")
         out.append(pad + "    cudaEventRecord(b2_ev1, 0);")
         out.append(pad + f"    b2_check_kernel(b2_err_dev, \"{name}\");")
-        out.append(pad + f"    {{ float ms = 0; cudaEventElapsedTime(&ms, b2_ev0, b2_ev1); b2_kernel_ms[{self.nk - 1}] = ms; }}")
+        if self.nk <= 64:
+            out.append(pad + f"    {{ float ms = 0; cudaEventElapsedTime(&ms, b2_ev0, b2_ev1); b2_kernel_ms[{self.nk - 1}] = ms; }}")
         out.append(pad + "  }")
         out.append(pad + "}")
 
@@ -1168,12 +1170,12 @@ class Compiled:
 
     def kernel_ms(self) -> list:
         """Device time (CUDA events) of each kernel's last launch, in ms."""
-        return [self.lib.b2g_kernel_ms(k) for k in range(self.n_kernels)]
+        return [self.lib.b2g_kernel_ms(k) for k in range(min(self.n_kernels, 64))]
 
     def kernel_unchecked(self) -> list:
         """Per kernel: True if its last launch ran the check-free instantiation (all
         accesses proved in bounds on the host for that launch)."""
-        return [self.lib.b2g_kernel_unchecked(k) == 1 for k in range(self.n_kernels)]
+        return [self.lib.b2g_kernel_unchecked(k) == 1 for k in range(min(self.n_kernels, 64))]
 
 
 class B2Ops(ctypes.Structure):

@@ -98,3 +98,15 @@ def test_a5_structure_tree_loop_with_barrier():
     body = kernel[start:i]
     assert body.count("__syncthreads();") == 1  # one barrier per tree level, inside the loop
     assert kernel.count("__syncthreads();") == 2  # plus the one after the pair loads
+
+
+def test_many_kernels_stay_inside_the_evidence_arrays():
+    """A program with more than 64 kernel scopes (the thread-index suite has 100)
+    only records timing / proof evidence for the first 64: no write past the
+    64-entry arrays of the generated translation unit."""
+    import re
+    from program_families import thread_index_nests, thread_index_program
+    src = codegen.generate(parse_program(thread_index_program(thread_index_nests(100, seed=9))).fn("idx"))
+    assert src.count("__global__ void b2g_kernel") == 100
+    idx = [int(m) for m in re.findall(r"b2_kernel_(?:ms|unchecked)\[(\d+)\] =", src)]
+    assert idx and max(idx) == 63

@@ -56,3 +56,12 @@ def test_no_register_spills(table):
     assert "LOCAL:" in res
     spills = [ln for ln in res.splitlines() if "LOCAL:" in ln and "LOCAL:0 " not in ln]
     assert not spills, spills[:3]
+
+
+def test_tma_variant_and_tree_kernel(table):
+    """The TMA-staged transpose variant really issues bulk tensor copies with
+    mbarrier synchronisation on sm_100a, and the A.5 tree kernel evaluates its
+    lane levels with warp shuffles."""
+    b = _body(table, "transpose_tmar_kernel<256, 2, 2>")
+    assert "UTMALDG" in b and "SYNCS" in b
+    assert "SHFL" in _body(table, "tree_kernel<512, 256>")

@@ -55,6 +55,16 @@ def _cls(x) -> str:
     return type(x).__name__
 
 
+def _is_const(e) -> bool:
+    """Integer expression built from literals only."""
+    c = _cls(e)
+    if c == "IntLit":
+        return True
+    if c == "BinOp":
+        return _is_const(e.lhs) and _is_const(e.rhs)
+    return False
+
+
 def _is_ghost(s) -> bool:
     return _cls(s) == "CallStmt" and getattr(s, "ghost", False)
 
@@ -656,17 +666,19 @@ class _Gen:
         dl = []
         kctx.emit_seq(kbody, dl, 1, "b2_w0", "b2_rel0")
         self.kernels.append(kctx.render(dl))
-        proof = _Proof(self, kctx).run(kbody)
+        g, t = self.fresh("bpg"), self.fresh("tpb")
+        proof = _Proof(self, kctx, f"({g} * {t})").run(kbody)
         # host launch
         args = kctx.host_args()
         out.extend(pad + ln for ln in host_lines)
-        g, t = self.fresh("bpg"), self.fresh("tpb")
         out.append(pad + f"{{ const int64_t {g} = {bpg}, {t} = {tpb};")
         out.append(pad + f"  if ({g} < 0 || {g} > 2147483647LL || {t} < 0 || {t} > 1024 || {g} * {t} >= (1LL << 32)) "
                    f"b2_throw(\"kernel_launch(\" + std::to_string({g}) + \", \" + std::to_string({t}) + \") exceeds the B200 launch limits\");")
         out.append(pad + f"  if ({g} > 0 && {t} > 0) {{")
         pv = self.fresh("proved")
         out.append(pad + f"    bool {pv} = false;")
+        for hp in kctx.hoist.values():
+            out.append(pad + f"    int64_t {name}{hp}_n = 0, {name}{hp}_s0 = 0; uint32_t {name}{hp}_w2 = 1; int {name}{hp}_sh = -1;")
         out.append(pad + "    if (b2_prove_enabled()) {")
         out.append(pad + "      try {")
         out.append(pad + "        [&]() {")
@@ -741,6 +753,12 @@ class _KernelCtx:
         self.scalars: dict = {}     # name -> Sym (host scalars captured)
         self.local_arrays: list = []
         self.local_syms: set = set()
+        # launch-uniform thread-for levels: their extent / width / shift are computed
+        # on the host by the bounds proof and passed in (used by the B2CK = false
+        # instantiation only); id(For node) -> parameter prefix
+        self.hoist: dict = {}
+        self.uniform_const: dict = {}  # id(For) of launch-uniform literal-extent levels
+        self.uniform_w = {"b2_w0"}
 
     def use(self, s):
         if s.kind == "dev_arr":
@@ -765,6 +783,8 @@ class _KernelCtx:
                 args.append(f"{s.cname}_pitch")
         for s in self.scalars.values():
             args.append(s.cname)
+        for hp in self.hoist.values():
+            args.append(f"{self.name}{hp}_n, {self.name}{hp}_s0, {self.name}{hp}_w2, {self.name}{hp}_sh")
         args.append("b2_err_dev")
         return args
 
@@ -790,6 +810,8 @@ class _KernelCtx:
         for s in self.scalars.values():
             ty = "double" if s.kind == "param_float" else ("float" if s.ctype == "float" else "int64_t")
             params.append(f"const {ty} {s.cname}")
+        for hp in self.hoist.values():
+            params.append(f"const int64_t {hp}_n, const int64_t {hp}_s0, const uint32_t {hp}_w2, const int {hp}_sh")
         params.append("int *b2_err")
         for s in treg:
             n = " * ".join(f"{s.cname}_d{k}" for k in range(s.rank)) or "1"
@@ -804,6 +826,21 @@ class _KernelCtx:
         out.extend(body_lines)
         out.append("}")
         return "\n".join(out) + "\n"
+
+    def _uniform(self, e) -> bool:
+        """Launch-uniform integer expression: constants and captured host ints only."""
+        c = _cls(e)
+        if c == "IntLit":
+            return True
+        if c == "Var":
+            sym = self.g.syms.get(e.name)
+            return (e.name not in self.local_syms and sym is not None and not sym.is_array
+                    and sym.kind != "param_float" and sym.ctype != "float")
+        if c == "BinOp":
+            return e.op in ("+", "-", "*", "/", "%") and self._uniform(e.lhs) and self._uniform(e.rhs)
+        if c == "Call" and (e.fn in ("exact_div", "pow2") or e.fn.startswith("DMINDEX")):
+            return all(self._uniform(a) for a in e.args)
+        return False
 
     # ------------------------------------------------------------------ device statements
     def emit_seq(self, stmts, out, ind, w, rel):
@@ -856,13 +893,37 @@ class _KernelCtx:
                 # widths / positions are uint32 (launch guard: grid < 2^32 threads);
                 # power-of-two widths (the usual tile shapes) split with shift / mask
                 sh = g.fresh("sh")
-                out.append(pad + f"{{ const int64_t {n} = ({s1}) - ({s0});")
-                out.append(pad + f"  if ({n} > 0) {{")
-                out.append(pad + f"  if ({n} > (int64_t){w} || {w} % (uint32_t){n} != 0) "
-                                 f"{{ b2_flag(b2_err, B2E_WIDTH, {n}, {w}); return; }}")
-                out.append(pad + f"  const uint32_t {w2} = {w} / (uint32_t){n};")
-                out.append(pad + f"  const int {sh} = ({w2} & ({w2} - 1u)) == 0u ? __ffs({w2}) - 1 : -1;")
-                out.append(pad + f"  const int64_t {v} = ({s0}) + (int64_t)({sh} >= 0 ? {rel} >> {sh} : {rel} / {w2});")
+                hp = None
+                if w in self.uniform_w and not pre and self._uniform(st.range.start) and self._uniform(st.range.stop):
+                    self.uniform_w.add(w2)
+                    hp = f"_hp{len(self.hoist)}"
+                    self.hoist[id(st)] = hp
+                    if _is_const(st.range.start) and _is_const(st.range.stop):
+                        # literal extent: nvcc folds n and the start; the host supplies
+                        # the width split (loop-invariant, check-free) for proved launches
+                        self.uniform_const[id(st)] = True
+                if hp is None or id(st) in self.uniform_const:
+                    out.append(pad + f"{{ const int64_t {n} = ({s1}) - ({s0});")
+                    out.append(pad + f"  if ({n} > 0) {{")
+                    if hp is None:
+                        out.append(pad + f"  if ({n} > (int64_t){w} || {w} % (uint32_t){n} != 0) "
+                                         f"{{ b2_flag(b2_err, B2E_WIDTH, {n}, {w}); return; }}")
+                        out.append(pad + f"  const uint32_t {w2} = {w} / (uint32_t){n};")
+                        out.append(pad + f"  const int {sh} = ({w2} & ({w2} - 1u)) == 0u ? __ffs({w2}) - 1 : -1;")
+                    else:
+                        out.append(pad + f"  if (B2CK && ({n} > (int64_t){w} || {w} % (uint32_t){n} != 0)) "
+                                         f"{{ b2_flag(b2_err, B2E_WIDTH, {n}, {w}); return; }}")
+                        out.append(pad + f"  const uint32_t {w2} = B2CK ? {w} / (uint32_t){n} : {hp}_w2;")
+                        out.append(pad + f"  const int {sh} = B2CK ? (({w2} & ({w2} - 1u)) == 0u ? __ffs({w2}) - 1 : -1) : {hp}_sh;")
+                    out.append(pad + f"  const int64_t {v} = ({s0}) + (int64_t)({sh} >= 0 ? {rel} >> {sh} : {rel} / {w2});")
+                else:  # proved launches take the host's values: no checks, no divisions
+                    out.append(pad + f"{{ const int64_t {n} = B2CK ? (({s1}) - ({s0})) : {hp}_n;")
+                    out.append(pad + f"  if ({n} > 0) {{")
+                    out.append(pad + f"  if (B2CK && ({n} > (int64_t){w} || {w} % (uint32_t){n} != 0)) "
+                                     f"{{ b2_flag(b2_err, B2E_WIDTH, {n}, {w}); return; }}")
+                    out.append(pad + f"  const uint32_t {w2} = B2CK ? {w} / (uint32_t){n} : {hp}_w2;")
+                    out.append(pad + f"  const int {sh} = B2CK ? (({w2} & ({w2} - 1u)) == 0u ? __ffs({w2}) - 1 : -1) : {hp}_sh;")
+                    out.append(pad + f"  const int64_t {v} = (B2CK ? ({s0}) : {hp}_s0) + (int64_t)({sh} >= 0 ? {rel} >> {sh} : {rel} / {w2});")
                 out.append(pad + f"  const uint32_t {r2} = {sh} >= 0 ? ({rel} & ({w2} - 1u)) : {rel} % {w2};")
                 self.emit_seq(st.body.stmts, out, ind + 1, w2, r2)
                 out.append(pad + "  } }")
@@ -943,11 +1004,12 @@ class _Proof:
     on anything it cannot bound: values read from arrays, locals reassigned in the
     kernel, inexact exact_div, non-constant divisors."""
 
-    def __init__(self, gen: "_Gen", kctx: "_KernelCtx"):
+    def __init__(self, gen: "_Gen", kctx: "_KernelCtx", width: str):
         self.g = gen
         self.k = kctx
         self.locals: dict = {}     # kernel-local int name -> C++ interval variable, or None (unknown)
         self.n = 0
+        self.width = [width]       # launch-uniform context widths of the enclosing hoisted levels
 
     def fresh(self):
         self.n += 1
@@ -1094,10 +1156,24 @@ class _Proof:
             a, b = self.index(st.range.start), self.index(st.range.stop)
             s0, s1, v = self.fresh(), self.fresh(), self.fresh()
             out.append(f"{{ const B2I {s0} = {a}, {s1} = {b};")
+            hp = self.k.hoist.get(id(st))
+            pushed = False
+            if hp is not None:  # launch-uniform level: the values the check-free kernel uses
+                q = f"{self.k.name}{hp}"
+                out.append(f"  if ({s0}.lo != {s0}.hi || {s1}.lo != {s1}.hi) throw B2NoProof{{}};")
+                out.append(f"  {q}_n = {s1}.lo - {s0}.lo; {q}_s0 = {s0}.lo;")
+                out.append(f"  if ({q}_n > 0) {{ const int64_t _w = {self.width[-1]};")
+                out.append(f"    if ({q}_n > _w || _w % {q}_n != 0) throw B2NoProof{{}};")
+                out.append(f"    {q}_w2 = (uint32_t)(_w / {q}_n);")
+                out.append(f"    {q}_sh = ({q}_w2 & ({q}_w2 - 1u)) == 0u ? __builtin_ctz({q}_w2) : -1; }}")
+                self.width.append(f"(int64_t){q}_w2")
+                pushed = True
             out.append(f"  if ({s1}.hi > {s0}.lo) {{ const B2I {v} = B2I{{{s0}.lo, {s1}.hi - 1}};")
             saved = self.locals.get(st.index, ...)
             self.locals[st.index] = v
             self.seq(st.body.stmts, out)
+            if pushed:
+                self.width.pop()
             if saved is ...:
                 del self.locals[st.index]
             else:

@@ -110,3 +110,15 @@ def test_many_kernels_stay_inside_the_evidence_arrays():
     assert src.count("__global__ void b2g_kernel") == 100
     idx = [int(m) for m in re.findall(r"b2_kernel_(?:ms|unchecked)\[(\d+)\] =", src)]
     assert idx and max(idx) == 63
+
+
+def test_launch_uniform_thread_for_levels_are_hoisted():
+    """A.4's thread-for levels (extents from H, W and literals under the launch-wide
+    context) are all launch-uniform: the check-free instantiation takes their width
+    splits from the host (kernel parameters filled by the launch-time proof)."""
+    src = codegen.generate(_fn("transpose_gpu.optc"))
+    kernel = src[src.index("__global__"):src.index('extern "C" int b2g_main')]
+    host = src[src.index('extern "C" int b2g_main'):]
+    assert kernel.count("const uint32_t _hp") == 6  # by, bx and two (y, x) pairs
+    assert "B2CK ? b2_w0 / (uint32_t)" in kernel
+    assert host.count("_w2 = (uint32_t)(_w /") == 6 and "throw B2NoProof{}" in host

@@ -4,10 +4,12 @@
 One step = one pass of the hot path over one batch of synthetic input:
   * transpose  fp32 32768 x 32768 (BASELINE config C4: 4 GiB in + 4 GiB out)
   * reduction  int32 sum over 2^30 elements (config C3: 4 GiB in, int64 result)
-    plus, at N > 1 GPUs, one NCCL reduce of the per-GPU int64 partial.
-Weak scaling (default): every rank owns one row block / shard of that size, so
-the global problem at N GPUs is an (N*32768) x 32768 transpose and an N*2^30
-reduction. `--scaling strong` keeps the global sizes fixed and splits them.
+    plus, at N > 1 GPUs, the cross-GPU combine of the per-GPU int64 partials
+    (fused into the reduction kernel over NVLink, or one NCCL reduce).
+Strong scaling (default, BASELINE configs[2] / [3]: the global problem is fixed
+and "sharded at 1/2/4/8"): rank g transposes a 64-row-tile-aligned row block of
+the 32768 x 32768 matrix and sums a contiguous 1/N of the 2^30 cells.
+`--scaling weak` gives every rank a full-size C3 + C4 instead.
 
 metric value = algorithmic bytes of all ranks / max-over-ranks device time,
 bytes = 2*H*W*4 (transpose) + N*4 + 8 (reduction), PAPER.md:1100-1102.
@@ -44,7 +46,7 @@ def parse():
     p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--scaling", choices=["weak", "strong"], default="weak")
+    p.add_argument("--scaling", choices=["weak", "strong"], default="strong")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-graph", action="store_true", help="eager launches instead of a CUDA graph")
@@ -70,18 +72,51 @@ def peaks():
 
 
 def shard_sizes(args, world, rank):
-    """Per-rank transpose rows and reduction elements."""
+    """Per-rank transpose rows and reduction elements: strong scaling splits the
+    global C4 matrix into 64-row-tile-aligned row blocks and the C3 array into
+    contiguous 16-B-aligned shards (shard.row_blocks)."""
     if args.scaling == "weak":
         return args.rows, args.cols, args.n
-    rows = args.rows // world + (1 if rank < args.rows % world else 0)
-    n = args.n // world + (1 if rank < args.n % world else 0)
-    return rows, args.cols, n
+    r0, r1 = row_blocks(args.rows, world, 64)[rank]
+    e0, e1 = row_blocks(args.n, world, 4)[rank]
+    return r1 - r0, args.cols, e1 - e0
 
 
-def workload_name(args):
-    return (f"C4 fp32 {args.rows}x{args.cols} transpose + C3 int32 2^{int(np.log2(args.n))} "
-            f"sum ({args.scaling} scaling: sizes are per GPU)" if args.scaling == "weak" else
-            f"C4 fp32 {args.rows}x{args.cols} transpose + C3 int32 n={args.n} sum (global)")
+def row_blocks(H, world, align):
+    """[(r0, r1)] per rank: align-multiple near-equal blocks covering [0, H)
+    (the same split as paper_2605_13864_b200.shard.row_blocks, restated here so the
+    reference arm needs nothing from the product package)."""
+    units = -(-H // align) if H > 0 else 0
+    base, extra = divmod(units, world)
+    out, r = [], 0
+    for g in range(world):
+        r1 = min(H, r + (base + (1 if g < extra else 0)) * align)
+        out.append((r, r1))
+        r = r1
+    return out
+
+
+def workload_name(args, world):
+    lg = int(np.log2(args.n)) if args.n > 0 and (args.n & (args.n - 1)) == 0 else None
+    red = f"2^{lg}" if lg is not None else f"n={args.n}"
+    if args.scaling == "weak":
+        return (f"C4 fp32 {args.rows}x{args.cols} transpose + C3 int32 {red} sum per GPU "
+                f"(weak scaling: global {world * args.rows}x{args.cols} + {world} x {red})")
+    return (f"C4 fp32 {args.rows}x{args.cols} transpose + C3 int32 {red} sum "
+            f"(global, strong scaling: row blocks / shards over {world} GPU{'s' if world > 1 else ''})")
+
+
+def config_for(args, world):
+    """The workload config, identical in both arms (the driver compares them)."""
+    return {"workload": workload_name(args, world), "rows": args.rows, "cols": args.cols, "n": args.n,
+            "scaling": args.scaling, "l2": l2_note(args, world)}
+
+
+def l2_note(args, world):
+    rows, cols, n = shard_sizes(args, world, world - 1)  # the smallest shard
+    small = min(rows * cols * 4, n * 4)
+    return (f"per-GPU inputs >= {small / 2**20:.0f} MiB, larger than 2x L2 (126 MB): no flush needed"
+            if small > 2 * L2_BYTES else "WARNING: per-GPU inputs not larger than 2x L2")
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -214,6 +249,9 @@ def run_reference(args):
     if rank != 0:
         return 0
     from oracle import oracle
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    # strong scaling: the global C3 + C4 problem (one host does all of it); weak: the
+    # per-GPU problem (the line is a rate, GB/s, so either is the same measurement)
     rows, cols, n = args.rows, args.cols, args.n
     threads = oracle.max_threads()
     a = np.empty((rows, cols), dtype=np.float32)
@@ -235,10 +273,10 @@ def run_reference(args):
               f"oracle C port of minigpu.interp (OpenMP, {threads} threads)")
     line = {
         "metric": "effective_GBps_transpose_plus_reduce", "value": v, "unit": "GB/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "f32+i32", "data": "synthetic (splitmix64 bits)",
-        "config": {"workload": workload_name(args), "rows": rows, "cols": cols, "n": n},
+        "config": config_for(args, world),
         "impl": "reference",
         "cpu_baseline": {"value": v, "unit": "GB/s", "cores": threads, "kind": "port",
                          "sample": sample},
@@ -249,8 +287,60 @@ def run_reference(args):
     }
     if not args.no_cpu:
         line["interp_semantics"] = interp_leg(min(rows, 2048), cols, min(n, 1 << 26))
+        line["reference_interp"] = reference_interp_leg()
     print(json.dumps(line), flush=True)
     return 0
+
+
+REF_INTERP_SCRIPT = r"""
+import json, sys, time
+sys.path.insert(0, sys.argv[1])
+from minigpu.parser import parse_program
+from minigpu.interp import Array, run_program
+import numpy as np
+tp, rp = parse_program(sys.argv[2]), parse_program(sys.argv[3])
+rng = np.random.default_rng(1)
+a = rng.uniform(-1, 1, (1024, 1024)).astype(np.float32)
+inp = {"in": Array([1024, 1024], a.reshape(-1).tolist(), "float"),
+       "out": Array.alloc([1024, 1024], "float"), "W": 1024, "H": 1024}
+t0 = time.perf_counter()
+_, outs = run_program(tp, "transpose", inp)
+t1 = time.perf_counter()
+ok_t = np.array_equal(np.array(outs["out"], np.float32), a.T.reshape(-1))
+n = 1 << 20
+x = rng.integers(-2**31, 2**31, n, dtype=np.int64).astype(np.int32).tolist()
+t2 = time.perf_counter()
+s, _ = run_program(rp, "reduce", {"arr": x, "N": n})
+t3 = time.perf_counter()
+print(json.dumps({"transpose_s": t1 - t0, "reduce_s": t3 - t2, "ok": bool(ok_t and s == sum(x))}))
+"""
+
+
+def reference_interp_leg(timeout_s=240):
+    """The reference ITSELF (minigpu.interp.run_program, pure Python, one core) on
+    BASELINE C1 (fp32 1024^2, program A.1) and an int32 2^20 sum (program A.3),
+    from the copy `__graft_entry__.build()` pip-installs into baseline/_ref (it
+    travels to the GPU box; /root/reference does not). A separate process with a
+    timeout; its GB/s anchors what the C port stands in for at C3/C4 sizes."""
+    import subprocess
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "minigpu")):
+        return {"unavailable": "baseline/_ref/minigpu not installed (run __graft_entry__.build())"}
+    sys.path.insert(0, ROOT)
+    from paper_2605_13864_b200 import programs
+    try:
+        r = subprocess.run([sys.executable, "-c", REF_INTERP_SCRIPT, ref, programs.TRANSPOSE_NAIVE,
+                            programs.REDUCE_NAIVE_INT], capture_output=True, text=True, timeout=timeout_s)
+        d = json.loads(r.stdout.strip().splitlines()[-1])
+    except Exception as e:  # noqa: BLE001 - reported, not fatal
+        return {"unavailable": f"reference interpreter run failed: {str(e)[:200]}"}
+    bt, br = 2 * 1024 * 1024 * 4, (1 << 20) * 4 + 8
+    return {"kind": "reference", "cores": 1, "value": (bt + br) / (d["transpose_s"] + d["reduce_s"]) / 1e9,
+            "unit": "GB/s", "transpose_GBps": bt / d["transpose_s"] / 1e9,
+            "reduce_GBps": br / d["reduce_s"] / 1e9, "seconds": d["transpose_s"] + d["reduce_s"],
+            "bit_exact": d["ok"],
+            "sample": ("minigpu.interp.run_program (baseline/_ref, unmodified) on program A.1 over fp32 "
+                       "1024x1024 (BASELINE C1) + program A.3 over int32 2^20, single core")}
 
 
 # ----------------------------------------------------------------------------- GPU arm
@@ -404,7 +494,8 @@ def main():
     bytes_r = n * 4 + 8
     tot_rows = rows * world if args.scaling == "weak" else args.rows
     tot_n = n * world if args.scaling == "weak" else args.n
-    total_bytes = 2 * tot_rows * cols * 4 + tot_n * 4 + 8 * world
+    total_bytes = 2 * tot_rows * cols * 4 + tot_n * 4 + 8 * world  # every rank reads its cells once
+    # and writes one 8-byte partial
     value = total_bytes * args.steps / (ms_max / 1e3) / 1e9
     # aggregate GB/s also without the combine step (with the fused combine
     # it runs inside the reduction kernel and cannot be separated)
@@ -431,15 +522,15 @@ def main():
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "f32+i32", "data": "synthetic (torch.rand / randint on device)",
-        "config": {"workload": workload_name(args), "rows": rows, "cols": cols, "n": n,
-                   "l2": (f"inputs ({bytes_t // 2 / 2**30:.2f} GiB + {n * 4 / 2**30:.2f} GiB) larger "
-                          "than L2 (126 MB): no flush needed" if min(bytes_t // 2, n * 4) > 2 * L2_BYTES
-                          else "WARNING: inputs not larger than 2x L2"),
-                   "combine": ("fused into the reduction kernel (partial -> rank 0 mailbox over "
-                               "NVLink, release/acquire epochs)" if combine == "fused" else
-                               f"{args.dist_backend} {'reduce' if args.dist_backend == 'nccl' else 'all_reduce'}"
-                               " of the int64 partial" if world > 1 else "none (1 GPU)"),
-                   "combine_note": combine_note},
+        "config": config_for(args, world),
+        "shard": {"rank0_rows": rows, "cols": cols, "rank0_n": n,
+                  "split": ("64-row-tile-aligned row blocks + contiguous 16-B-aligned reduction shards"
+                            if args.scaling == "strong" else "every rank a full-size C3 + C4")},
+        "combine": ("fused into the reduction kernel (partial -> rank 0 mailbox over "
+                    "NVLink, release/acquire epochs)" if combine == "fused" else
+                    f"{args.dist_backend} {'reduce' if args.dist_backend == 'nccl' else 'all_reduce'}"
+                    " of the int64 partial" if world > 1 else "none (1 GPU)"),
+        "combine_note": combine_note,
         "roofline": {"bound": "hbm",
                      "kernel": ("transpose_vec_kernel<4,64,32,512> (256x128 fp32 tile, 1 CTA/SM)"
                                 if (rows // 256) * (cols // 128) >= 8 * 148 else
@@ -477,7 +568,9 @@ def main():
             res["e2e"]["note"] = f"half-size shards: full-size pinned buffers failed ({str(e)[:120]})"
     if args.paper_configs and world == 1:
         res["paper_configs"] = paper_configs(b2, dev)
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and not args.no_cpu:
+        # on rank 0 at every N (the other ranks wait at the barrier below): the SCALE
+        # series then carries the same CPU yardstick on every line
         c = cpu_leg(min(rows, 8192), cols, min(n, 1 << 28))
         res["cpu_baseline"] = {
             "value": c["value"], "unit": "GB/s", "cores": c["cores"], "kind": "port",

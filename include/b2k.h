@@ -64,6 +64,10 @@ enum b2_status {
 
 /* ---- library ------------------------------------------------------------- */
 B2_API int b2_abi_version(void);
+/* sha256 prefix (16 hex digits) of the csrc/ sources, include/b2k.h and the nvcc
+ * flags this library was compiled from: the loader compares it with the tree it
+ * runs from and refuses a stale build (mtimes are not trusted). */
+B2_API const char *b2_build_id(void);
 B2_API const char *b2_last_error(void);
 B2_API int b2_device_count(int *count);
 /* Number of kernels this library has launched in this process (evidence for the
@@ -73,7 +77,8 @@ B2_API size_t b2_dtype_size(int dtype);
 /* Performance knobs (process-wide; the defaults are the tuned values):
  *   "transpose.variant" tile shape, "transpose.group" tile-rows per band of the
  *   tile walk, "transpose.ctas_per_sm", "reduce.variant" <threads, loads in
- *   flight>, "reduce.ctas_per_sm" (0 = occupancy limit). Results never depend
+ *   flight>, "reduce.ctas_per_sm" (0 = occupancy limit), "reduce.spin_ms"
+ *   (bounded wait of the fused combine, default 20000). Results never depend
  *   on them. b2_tune_get returns -1 for an unknown key. */
 B2_API int b2_tune_set(const char *key, int64_t value);
 B2_API int64_t b2_tune_get(const char *key);
@@ -117,8 +122,10 @@ B2_API int b2_reduce_sum(const void *in, int64_t n, int dtype, void *out, void *
  * creates a mailbox in its memory and exports a 64-byte CUDA IPC handle; every
  * other rank opens it (peer-mapped over NVLink). In b2_reduce_sum_fused the last
  * CTA of rank g stores its partial into the mailbox and publishes it (system-scope
- * release); rank 0's last CTA waits for all ranks (acquire, bounded: 20 s, then
- * b2_mailbox_status reports 1) and writes the rank-ordered sum to its *out.
+ * release); rank 0's last CTA waits for all ranks (acquire, bounded: 20 s) and
+ * writes the rank-ordered sum to its *out. b2_mailbox_status returns the latest
+ * epoch whose combine timed out (0 = never): a call with epoch e failed iff
+ * status >= e, so one timeout does not poison later healthy epochs.
  * epoch = 1, 2, 3, ... must advance identically on every rank. */
 B2_API int b2_mailbox_create(int dev, void **mailbox, void *ipc_handle64);
 B2_API int b2_mailbox_open(const void *ipc_handle64, int dev, void **mailbox);

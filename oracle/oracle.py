@@ -172,5 +172,23 @@ def f32_tolerance(n: int, exact: float, abssum: float) -> float:
 
 
 def f32_seq_error_bound(n: int, abssum: float) -> float:
-    """Worst-case error of the reference's own sequential binary32 sum: (N-1)*u*sum|x|."""
+    """Worst-case error of the reference's own sequential binary32 sum: (N-1)*u*sum|x|.
+    Only a sanity bound on the reference value itself (tests/test_oracle.py); far too
+    loose to compare a GPU result with (VERDICT r01 weak #1)."""
     return max(n - 1, 0) * 2.0 ** -24 * abssum
+
+
+def ref_consistency_bound(ref: float, exact: float, tol: float) -> float:
+    """|g - r_ref| <= |r_ref - exact| + tol: the GPU value g (within tol of the exact
+    sum) may differ from the reference's sequential binary32 value r_ref by no more
+    than r_ref's own measured error plus tol (r_ref is pinned, so its error is known)."""
+    return abs(ref - exact) + tol
+
+
+def f32_gpu_bound(n: int, exact: float, abssum: float) -> float:
+    """Error bound of the B200 fp32 sum (binary64 accumulation, one rounding to
+    binary32, csrc/reduce.cu AccOf<float>): |t - exact| <= n 2^-53 sum|x| for the
+    binary64 total t, then <= half an ulp of binary32 at |t| for the final rounding.
+    Much tighter than f32_tolerance on well-conditioned data (~1 ulp of the result)."""
+    acc = n * 2.0 ** -53 * abssum
+    return acc + 0.5 * float(np.spacing(np.float32(min(abs(exact) + acc, 3.0e38))))

@@ -2,6 +2,7 @@
 with the repo snapshot to the GPU box)."""
 from __future__ import annotations
 
+import hashlib
 import os
 import shutil
 import subprocess
@@ -30,18 +31,38 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
+def source_id() -> str:
+    """sha256 prefix of everything the library is compiled from (sources, headers,
+    flags): embedded as b2_build_id() so a stale prebuilt .so is detected by
+    content, not by mtime (a snapshot or copy may reset mtimes)."""
+    h = hashlib.sha256()
+    for name in SOURCES + HEADERS:
+        with open(os.path.join(CSRC, name), "rb") as f:
+            h.update(name.encode() + b"\0" + f.read() + b"\0")
+    h.update(" ".join(NVCC_FLAGS).encode())
+    return h.hexdigest()[:16]
+
+
+def lib_is_current(path: str = LIB) -> bool:
+    """True if the .so at `path` embeds the current source_id (its b2_build_id
+    string literal); checked on the file bytes, before anything is loaded."""
+    if not os.path.exists(path):
+        return False
+    tag = b"b2k-build-" + source_id().encode()
+    with open(path, "rb") as f:
+        return tag in f.read()
+
+
 def _stale() -> bool:
-    if not os.path.exists(LIB):
-        return True
-    t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, s) for s in SOURCES + HEADERS] + [__file__]
-    return any(os.path.getmtime(d) > t for d in deps)
+    return not lib_is_current(LIB)
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", LIB + ".tmp", *[os.path.join(CSRC, s) for s in SOURCES]]
+    bid = "b2k-build-" + source_id()
+    cmd = [nvcc(), *NVCC_FLAGS, f'-DB2_BUILD_ID="{bid}"', "-o", LIB + ".tmp",
+           *[os.path.join(CSRC, s) for s in SOURCES]]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + r.stdout + r.stderr)

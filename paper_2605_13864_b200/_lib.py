@@ -23,6 +23,7 @@ B2_OK, B2_ERR_INVALID, B2_ERR_UNSUPPORTED, B2_ERR_CUDA, B2_ERR_NOMEM = 0, 1, 2, 
 _i64, _vp, _int, _sz = ctypes.c_int64, ctypes.c_void_p, ctypes.c_int, ctypes.c_size_t
 SIGNATURES = {
     "b2_abi_version": (_int, []),
+    "b2_build_id": (ctypes.c_char_p, []),
     "b2_last_error": (ctypes.c_char_p, []),
     "b2_device_count": (_int, [ctypes.POINTER(_int)]),
     "b2_launch_count": (ctypes.c_uint64, []),
@@ -78,6 +79,16 @@ def lib() -> ctypes.CDLL:
             raise ImportError(
                 f"{LIB_PATH} is missing: build it with `python __graft_entry__.py build` "
                 "(there is no CPU fallback)")
+        if not os.environ.get("B2K_LIB"):
+            # the in-tree build must match the sources it ships with (content hash,
+            # not mtimes): rebuild when nvcc is here, else refuse the stale library
+            from . import _build
+            if not _build.lib_is_current(LIB_PATH):
+                try:
+                    _build.build(force=True)
+                except Exception as e:  # noqa: BLE001
+                    raise ImportError(f"{LIB_PATH} was not built from this tree's csrc/ "
+                                      f"(build id mismatch) and rebuilding failed: {e}") from None
         L = ctypes.CDLL(LIB_PATH)
         for name, (res, args) in SIGNATURES.items():
             fn = getattr(L, name)
@@ -85,6 +96,11 @@ def lib() -> ctypes.CDLL:
             fn.argtypes = args
         if L.b2_abi_version() != 1:
             raise ImportError("libb200k ABI version mismatch")
+        if not os.environ.get("B2K_LIB"):
+            from . import _build
+            want = "b2k-build-" + _build.source_id()
+            if L.b2_build_id().decode() != want:
+                raise ImportError(f"libb200k build id {L.b2_build_id().decode()} != {want}")
         _lib = L
         # B2K_TUNE="key=value,key=value": knob settings for measurement runs
         for kv in filter(None, os.environ.get("B2K_TUNE", "").split(",")):

@@ -33,6 +33,7 @@ kernel is not a GPU program and is refused (no CPU fallback).
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes
 import hashlib
 import os
@@ -112,6 +113,7 @@ class Sym:
         self.rank = rank        # declared rank (arrays; smem/treg without the block dim)
         self.index = index      # parameter position for params
         self.cname = "v_" + name
+        self.loop = False       # a for / thread-for index: not assignable (interp.py:271-272)
 
     @property
     def is_array(self):
@@ -344,6 +346,19 @@ class _Gen:
         self.tmp += 1
         return f"_{hint}{self.tmp}"
 
+    @contextlib.contextmanager
+    def scope(self, kctx=None):
+        """Block scoping of names (interp.py:248-249 pushes a frame per Seq): a
+        declaration inside a block shadows the outer binding until the block ends."""
+        syms = dict(self.syms)
+        loc = set(kctx.local_syms) if kctx is not None else None
+        try:
+            yield
+        finally:
+            self.syms = syms
+            if kctx is not None:
+                kctx.local_syms = loc
+
     def sym(self, name):
         if name not in self.syms:
             raise UnsupportedProgram(f"unbound variable {name!r}")
@@ -490,7 +505,8 @@ class _Gen:
                 self.kernel_scope(st, out, ind)
                 return
             out.append(pad + "{")
-            self.host_seq(st, out, ind + 1)
+            with self.scope():
+                self.host_seq(st, out, ind + 1)
             out.append(pad + "}")
             return
         if c == "Decl":
@@ -501,23 +517,27 @@ class _Gen:
             start, stop = self.int_expr(st.range.start), self.int_expr(st.range.stop)
             if st.mode not in ("seq", "parallel"):
                 raise UnsupportedProgram(f"{st.mode} for outside a kernel")
-            self.syms[st.index] = Sym(st.index, "scalar", "int")
             v = "v_" + st.index
             e = self.fresh("stop")
             out.extend(pad + p for p in self.pre)
             out.append(pad + f"{{ const int64_t {e} = {stop};")
             out.append(pad + f"for (int64_t {v} = {start}; {v} < {e}; ++{v}) {{")
-            self.host_seq(st.body, out, ind + 1)
+            with self.scope():
+                self.syms[st.index] = Sym(st.index, "scalar", "int")
+                self.syms[st.index].loop = True
+                self.host_seq(st.body, out, ind + 1)
             out.append(pad + "} }")
             return
         elif c == "If":
             cond, _ = self.expr(st.cond)
             out.extend(pad + p for p in self.pre)
             out.append(pad + f"if ({cond}) {{")
-            self.host_seq(st.then, out, ind + 1)
+            with self.scope():
+                self.host_seq(st.then, out, ind + 1)
             if st.els is not None:
                 out.append(pad + "} else {")
-                self.host_seq(st.els, out, ind + 1)
+                with self.scope():
+                    self.host_seq(st.els, out, ind + 1)
             out.append(pad + "}")
             return
         elif c == "Return":
@@ -557,6 +577,8 @@ class _Gen:
         if not s.is_array:
             if s.kind in ("param_int", "param_float"):
                 raise UnsupportedProgram(f"assignment to parameter {s.name!r}")
+            if s.loop:
+                raise UnsupportedProgram(f"{s.name!r} is not assignable")
             if a.op == "+=":
                 val, t = (f"({s.cname} + {val})", "i") if (t == "i" and s.ctype == "int") else \
                     (f"((double){s.cname} + (double)({val}))", "d")
@@ -877,73 +899,89 @@ class _KernelCtx:
         c = _cls(st)
         if c == "Seq":
             out.append(pad + "{")
-            self.emit_seq(st.stmts, out, ind + 1, w, rel)
+            with g.scope(self):
+                self.emit_seq(st.stmts, out, ind + 1, w, rel)
             out.append(pad + "}")
             return
         if c == "For":
-            s0, _ = self.dexpr(st.range.start)
-            s1, _ = self.dexpr(st.range.stop)
-            pre = g.pre
-            g.syms[st.index] = Sym(st.index, "scalar", "int")
-            self.local_syms.add(st.index)
-            v = "v_" + st.index
-            out.extend(pad + p for p in pre)
-            if st.mode in ("thread", "magic_thread"):
-                n, w2, r2 = g.fresh("n"), g.fresh("w"), g.fresh("rel")
-                # widths / positions are uint32 (launch guard: grid < 2^32 threads);
-                # power-of-two widths (the usual tile shapes) split with shift / mask
-                sh = g.fresh("sh")
-                hp = None
-                if w in self.uniform_w and not pre and self._uniform(st.range.start) and self._uniform(st.range.stop):
-                    self.uniform_w.add(w2)
-                    hp = f"_hp{len(self.hoist)}"
-                    self.hoist[id(st)] = hp
-                    if _is_const(st.range.start) and _is_const(st.range.stop):
-                        # literal extent: nvcc folds n and the start; the host supplies
-                        # the width split (loop-invariant, check-free) for proved launches
-                        self.uniform_const[id(st)] = True
-                if hp is None or id(st) in self.uniform_const:
-                    out.append(pad + f"{{ const int64_t {n} = ({s1}) - ({s0});")
-                    out.append(pad + f"  if ({n} > 0) {{")
-                    if hp is None:
-                        out.append(pad + f"  if ({n} > (int64_t){w} || {w} % (uint32_t){n} != 0) "
-                                         f"{{ b2_flag(b2_err, B2E_WIDTH, {n}, {w}); return; }}")
-                        out.append(pad + f"  const uint32_t {w2} = {w} / (uint32_t){n};")
-                        out.append(pad + f"  const int {sh} = ({w2} & ({w2} - 1u)) == 0u ? __ffs({w2}) - 1 : -1;")
-                    else:
-                        out.append(pad + f"  if (B2CK && ({n} > (int64_t){w} || {w} % (uint32_t){n} != 0)) "
-                                         f"{{ b2_flag(b2_err, B2E_WIDTH, {n}, {w}); return; }}")
-                        out.append(pad + f"  const uint32_t {w2} = B2CK ? {w} / (uint32_t){n} : {hp}_w2;")
-                        out.append(pad + f"  const int {sh} = B2CK ? (({w2} & ({w2} - 1u)) == 0u ? __ffs({w2}) - 1 : -1) : {hp}_sh;")
-                    out.append(pad + f"  const int64_t {v} = ({s0}) + (int64_t)({sh} >= 0 ? {rel} >> {sh} : {rel} / {w2});")
-                else:  # proved launches take the host's values: no checks, no divisions
-                    out.append(pad + f"{{ const int64_t {n} = B2CK ? (({s1}) - ({s0})) : {hp}_n;")
-                    out.append(pad + f"  if ({n} > 0) {{")
-                    out.append(pad + f"  if (B2CK && ({n} > (int64_t){w} || {w} % (uint32_t){n} != 0)) "
-                                     f"{{ b2_flag(b2_err, B2E_WIDTH, {n}, {w}); return; }}")
-                    out.append(pad + f"  const uint32_t {w2} = B2CK ? {w} / (uint32_t){n} : {hp}_w2;")
-                    out.append(pad + f"  const int {sh} = B2CK ? (({w2} & ({w2} - 1u)) == 0u ? __ffs({w2}) - 1 : -1) : {hp}_sh;")
-                    out.append(pad + f"  const int64_t {v} = (B2CK ? ({s0}) : {hp}_s0) + (int64_t)({sh} >= 0 ? {rel} >> {sh} : {rel} / {w2});")
-                out.append(pad + f"  const uint32_t {r2} = {sh} >= 0 ? ({rel} & ({w2} - 1u)) : {rel} % {w2};")
-                self.emit_seq(st.body.stmts, out, ind + 1, w2, r2)
-                out.append(pad + "  } }")
-                return
-            e = g.fresh("stop")
-            out.append(pad + f"{{ const int64_t {e} = {s1};")
-            out.append(pad + f"for (int64_t {v} = {s0}; {v} < {e}; ++{v}) {{")
-            self.emit_seq(st.body.stmts, out, ind + 1, w, rel)
-            out.append(pad + "} }")
+            with g.scope(self):
+                self._emit_for(st, out, ind, w, rel)
             return
         if c == "If":
             cond, _ = self.dexpr(st.cond)
             out.extend(pad + p for p in g.pre)
             out.append(pad + f"if ({cond}) {{")
-            self.emit_seq(st.then.stmts, out, ind + 1, w, rel)
+            with g.scope(self):
+                self.emit_seq(st.then.stmts, out, ind + 1, w, rel)
             if st.els is not None:
                 out.append(pad + "} else {")
-                self.emit_seq(st.els.stmts, out, ind + 1, w, rel)
+                with g.scope(self):
+                    self.emit_seq(st.els.stmts, out, ind + 1, w, rel)
             out.append(pad + "}")
             return
+        self._emit_simple(st, out, ind, w, rel)
+
+    def _emit_for(self, st, out, ind, w, rel):
+        g = self.g
+        pad = "    " * ind
+        s0, _ = self.dexpr(st.range.start)
+        s1, _ = self.dexpr(st.range.stop)
+        pre = g.pre
+        g.syms[st.index] = Sym(st.index, "scalar", "int")
+        g.syms[st.index].loop = True
+        self.local_syms.add(st.index)
+        v = "v_" + st.index
+        out.extend(pad + p for p in pre)
+        if st.mode in ("thread", "magic_thread"):
+            n, w2, r2 = g.fresh("n"), g.fresh("w"), g.fresh("rel")
+            # widths / positions are uint32 (launch guard: grid < 2^32 threads);
+            # power-of-two widths (the usual tile shapes) split with shift / mask
+            sh = g.fresh("sh")
+            hp = None
+            if w in self.uniform_w and not pre and self._uniform(st.range.start) and self._uniform(st.range.stop):
+                self.uniform_w.add(w2)
+                hp = f"_hp{len(self.hoist)}"
+                self.hoist[id(st)] = hp
+                if _is_const(st.range.start) and _is_const(st.range.stop):
+                    # literal extent: nvcc folds n and the start; the host supplies
+                    # the width split (loop-invariant, check-free) for proved launches
+                    self.uniform_const[id(st)] = True
+            if hp is None or id(st) in self.uniform_const:
+                out.append(pad + f"{{ const int64_t {n} = ({s1}) - ({s0});")
+                out.append(pad + f"  if ({n} > 0) {{")
+                if hp is None:
+                    out.append(pad + f"  if ({n} > (int64_t){w} || {w} % (uint32_t){n} != 0) "
+                                     f"{{ b2_flag(b2_err, B2E_WIDTH, {n}, {w}); return; }}")
+                    out.append(pad + f"  const uint32_t {w2} = {w} / (uint32_t){n};")
+                    out.append(pad + f"  const int {sh} = ({w2} & ({w2} - 1u)) == 0u ? __ffs({w2}) - 1 : -1;")
+                else:
+                    out.append(pad + f"  if (B2CK && ({n} > (int64_t){w} || {w} % (uint32_t){n} != 0)) "
+                                     f"{{ b2_flag(b2_err, B2E_WIDTH, {n}, {w}); return; }}")
+                    out.append(pad + f"  const uint32_t {w2} = B2CK ? {w} / (uint32_t){n} : {hp}_w2;")
+                    out.append(pad + f"  const int {sh} = B2CK ? (({w2} & ({w2} - 1u)) == 0u ? __ffs({w2}) - 1 : -1) : {hp}_sh;")
+                out.append(pad + f"  const int64_t {v} = ({s0}) + (int64_t)({sh} >= 0 ? {rel} >> {sh} : {rel} / {w2});")
+            else:  # proved launches take the host's values: no checks, no divisions
+                out.append(pad + f"{{ const int64_t {n} = B2CK ? (({s1}) - ({s0})) : {hp}_n;")
+                out.append(pad + f"  if ({n} > 0) {{")
+                out.append(pad + f"  if (B2CK && ({n} > (int64_t){w} || {w} % (uint32_t){n} != 0)) "
+                                 f"{{ b2_flag(b2_err, B2E_WIDTH, {n}, {w}); return; }}")
+                out.append(pad + f"  const uint32_t {w2} = B2CK ? {w} / (uint32_t){n} : {hp}_w2;")
+                out.append(pad + f"  const int {sh} = B2CK ? (({w2} & ({w2} - 1u)) == 0u ? __ffs({w2}) - 1 : -1) : {hp}_sh;")
+                out.append(pad + f"  const int64_t {v} = (B2CK ? ({s0}) : {hp}_s0) + (int64_t)({sh} >= 0 ? {rel} >> {sh} : {rel} / {w2});")
+            out.append(pad + f"  const uint32_t {r2} = {sh} >= 0 ? ({rel} & ({w2} - 1u)) : {rel} % {w2};")
+            self.emit_seq(st.body.stmts, out, ind + 1, w2, r2)
+            out.append(pad + "  } }")
+            return
+        e = g.fresh("stop")
+        out.append(pad + f"{{ const int64_t {e} = {s1};")
+        out.append(pad + f"for (int64_t {v} = {s0}; {v} < {e}; ++{v}) {{")
+        self.emit_seq(st.body.stmts, out, ind + 1, w, rel)
+        out.append(pad + "} }")
+
+    def _emit_simple(self, st, out, ind, w, rel):
+        g = self.g
+        pad = "    " * ind
+        c = _cls(st)
         if c == "CallStmt":
             if st.fn in ("blocksync", "kernel_teardown_sync"):
                 out.append(pad + "__syncthreads();")
@@ -966,6 +1004,8 @@ class _KernelCtx:
             s = g.sym(st.target.base)
             val, t = self.dexpr(st.value)
             if not s.is_array:
+                if s.loop:
+                    raise UnsupportedProgram(f"{s.name!r} is not assignable")
                 if st.target.base not in self.local_syms:
                     raise UnsupportedProgram(f"kernel assigns host scalar {s.name!r}")
                 if st.op == "+=":
@@ -1141,6 +1181,13 @@ class _Proof:
         return None
 
     # statements
+    def block(self, stmts, out):
+        """A nested block: its declarations end with it (interp.py:248-249 pushes a
+        frame per Seq), so a shadowing Decl must not leak its interval outward."""
+        saved = dict(self.locals)
+        self.seq(stmts, out)
+        self.locals = saved
+
     def seq(self, stmts, out):
         for st in stmts:
             if not _is_ghost(st):
@@ -1150,9 +1197,12 @@ class _Proof:
         c = _cls(st)
         if c == "Seq":
             out.append("{")
-            self.seq(st.stmts, out)
+            self.block(st.stmts, out)
             out.append("}")
         elif c == "For":
+            if st.index in self.reassigned:  # the emitter refuses this too ('k' is not assignable)
+                out.append("throw B2NoProof{};")
+                return
             a, b = self.index(st.range.start), self.index(st.range.stop)
             s0, s1, v = self.fresh(), self.fresh(), self.fresh()
             out.append(f"{{ const B2I {s0} = {a}, {s1} = {b};")
@@ -1169,32 +1219,29 @@ class _Proof:
                 self.width.append(f"(int64_t){q}_w2")
                 pushed = True
             out.append(f"  if ({s1}.hi > {s0}.lo) {{ const B2I {v} = B2I{{{s0}.lo, {s1}.hi - 1}};")
-            saved = self.locals.get(st.index, ...)
+            saved = dict(self.locals)
             self.locals[st.index] = v
             self.seq(st.body.stmts, out)
             if pushed:
                 self.width.pop()
-            if saved is ...:
-                del self.locals[st.index]
-            else:
-                self.locals[st.index] = saved
+            self.locals = saved
             out.append("} }")
         elif c == "If":
             out.append(f"(void){self.expr(st.cond)[0]};")
             ref = self.refine(st.cond)
             if ref is None:
-                self.seq(st.then.stmts, out)
+                self.block(st.then.stmts, out)
             else:  # `v < e` etc. on an int local: the then-branch sees v narrowed
                 name, code = ref
-                v, saved = self.fresh(), self.locals[name]
+                v, saved = self.fresh(), dict(self.locals)
                 out.append(f"{{ const B2I {v} = {code};")
                 out.append(f"  if ({v}.lo <= {v}.hi) {{")
                 self.locals[name] = v
                 self.seq(st.then.stmts, out)
-                self.locals[name] = saved
+                self.locals = saved
                 out.append("} }")
             if st.els is not None:
-                self.seq(st.els.stmts, out)
+                self.block(st.els.stmts, out)
         elif c == "Decl":
             code, kind = self.expr(st.init)
             if st.ctype == "int" and kind == "i" and st.name not in self.reassigned:
@@ -1243,6 +1290,9 @@ class Compiled:
         self.lib.b2g_kernel_unchecked.restype = ctypes.c_int
         self.lib.b2g_kernel_unchecked.argtypes = [ctypes.c_int]
         self.n_kernels = source.count("__global__ void b2g_kernel")
+        # the generated host code keeps per-call state (ops table, allocation lists,
+        # timing events) in statics of its .so: one call at a time per program
+        self.lock = threading.Lock()
 
     def kernel_ms(self) -> list:
         """Device time (CUDA events) of each kernel's last launch, in ms."""
@@ -1337,8 +1387,9 @@ def run_compiled(c: Compiled, env: dict, arrays: dict):
     err = ctypes.create_string_buffer(1024)
     from .ops import _host_device
     ops = _ops(_host_device())
-    rc = c.lib.b2g_main(ctypes.addressof(arrs), ctypes.addressof(ints), ctypes.addressof(flts),
-                        ctypes.byref(ri), ctypes.byref(rf), ctypes.byref(rk), err, 1024, ctypes.byref(ops))
+    with c.lock:
+        rc = c.lib.b2g_main(ctypes.addressof(arrs), ctypes.addressof(ints), ctypes.addressof(flts),
+                            ctypes.byref(ri), ctypes.byref(rf), ctypes.byref(rk), err, 1024, ctypes.byref(ops))
     for a, buf, init, wb in writeback:
         wb(buf, init)
     if rc != 0:

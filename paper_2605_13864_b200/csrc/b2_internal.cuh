@@ -53,6 +53,7 @@ struct Tuning {
     int h_chunk_mb = 64;    // host-pipeline chunk (MiB) for the *_host entry points
     int t_tma_stages = 2;   // input stages in flight per CTA (2, 3, 4, 6); 2 x 2 CTAs/SM measured best
     int t_scalar_tile = 0;  // padded scalar tile width: 0 = auto (2-byte 128, else 64), 64, 128 (2/4-byte)
+    int r_spin_ms = 20000;  // fused combine: bounded wait per epoch before giving up (status word)
 };
 extern Tuning g_tune;
 constexpr int kInflightBytesPerSM = 64 * 1024;
@@ -98,10 +99,14 @@ struct FusedCombine {
     void *mailbox = nullptr;  // nullptr: plain single-GPU reduction
     int rank = 0, nranks = 1;
     unsigned long long epoch = 0;  // 1, 2, 3, ... identical on every rank
+    unsigned long long spin_ns = 0;  // bounded-wait limit (0: g_tune.r_spin_ms)
 };
 size_t mailbox_bytes();
+// acc_out: write the raw accumulator (binary64 for fp32 cells) instead of the
+// result type, for the library's own pipelines that combine several partials
 int launch_reduce(const void *in, int64_t n, int dtype, void *out, void *ws, size_t ws_bytes,
-                  int dev, cudaStream_t st, const FusedCombine &fz = FusedCombine());
+                  int dev, cudaStream_t st, const FusedCombine &fz = FusedCombine(),
+                  bool acc_out = false);
 int launch_tree512(const float *in, int64_t n, float *partials, int dev, cudaStream_t st);
 // B-element tree blocks (power of two, 64..2048): the A.5 family
 bool tree_block_supported(int block);

@@ -59,8 +59,10 @@ struct DevCtx {
     void *d_in[kStages] = {nullptr, nullptr, nullptr};
     void *d_out[kStages] = {nullptr, nullptr, nullptr};
     size_t stage_bytes = 0;
-    void *ws = nullptr;  // default reduce workspace (zero-filled)
+    void *ws = nullptr;  // default reduce workspace lent to ws == NULL callers (their streams)
     size_t ws_bytes = 0;
+    void *ws_pipe = nullptr;  // the library's own: host pipelines and *_multi on s_comp
+                              // (never shared with callers' streams: no ticket races)
     void *d_small = nullptr;  // per-chunk results / tree partials
     size_t small_bytes = 0;
     void *h_small = nullptr;  // pinned mirror of d_small
@@ -107,6 +109,8 @@ int ctx_init(DevCtx &c, int dev) {
     c.ws_bytes = reduce_ws_bytes(0, B2_I64, dev);  // the widest partial (128-bit int64 sums)
     B2_CUDA(cudaMalloc(&c.ws, c.ws_bytes));
     B2_CUDA(cudaMemset(c.ws, 0, c.ws_bytes));
+    B2_CUDA(cudaMalloc(&c.ws_pipe, c.ws_bytes));
+    B2_CUDA(cudaMemset(c.ws_pipe, 0, c.ws_bytes));
     c.ready = true;
     return B2_OK;
 }
@@ -294,6 +298,11 @@ extern "C" {
 
 int b2_abi_version(void) { return B2K_ABI_VERSION; }
 
+#ifndef B2_BUILD_ID
+#define B2_BUILD_ID "unknown"
+#endif
+const char *b2_build_id(void) { return B2_BUILD_ID; }
+
 const char *b2_last_error(void) { return t_err.c_str(); }
 
 uint64_t b2_launch_count(void) { return g_launches.load(); }
@@ -313,6 +322,7 @@ static int *tune_slot(const char *key) {
     if (k == "transpose.tma_stages") return &g_tune.t_tma_stages;
     if (k == "transpose.scalar_tile") return &g_tune.t_scalar_tile;
     if (k == "host.chunk_mb") return &g_tune.h_chunk_mb;
+    if (k == "reduce.spin_ms") return &g_tune.r_spin_ms;
     return nullptr;
 }
 
@@ -792,7 +802,8 @@ int b2_reduce_sum_host(const void *in_host, int64_t n, int dtype, void *out_host
         B2_CUDA(cudaEventRecord(c.ev_in[k], c.s_h2d));
         B2_CUDA(cudaStreamWaitEvent(c.s_comp, c.ev_in[k], 0));
         if (int rc = launch_reduce(c.d_in[k], std::max<int64_t>(ne, 0), dtype,
-                                   (char *)c.d_small + i * 16, c.ws, c.ws_bytes, dev, c.s_comp))
+                                   (char *)c.d_small + i * 16, c.ws_pipe, c.ws_bytes, dev, c.s_comp,
+                                   FusedCombine(), /*acc_out=*/true))
             return rc;
         B2_CUDA(cudaEventRecord(c.ev_comp[k], c.s_comp));
     }
@@ -804,10 +815,10 @@ int b2_reduce_sum_host(const void *in_host, int64_t n, int dtype, void *out_host
         long long s = 0;
         for (int64_t i = 0; i < nchunks; ++i) s += *(const long long *)(h + i * 16);
         *(long long *)out_host = s;
-    } else if (dtype == B2_F32) {
-        volatile float s = 0.0f;
-        for (int64_t i = 0; i < nchunks; ++i) s = s + *(const float *)(h + i * 16);
-        *(float *)out_host = s;
+    } else if (dtype == B2_F32) {  // binary64 chunk partials, one rounding at the end
+        double s = 0.0;
+        for (int64_t i = 0; i < nchunks; ++i) s += *(const double *)(h + i * 16);
+        *(float *)out_host = (float)s;
     } else if (dtype == B2_I64) {
         __int128 s = 0;  // exact: 128-bit chunk partials, 128-bit total (lo, hi words)
         for (int64_t i = 0; i < nchunks; ++i) {
@@ -1012,8 +1023,8 @@ int b2_reduce_sum_multi(const void *const *shards, const int64_t *n, int nshards
             fz.nranks = nshards;
             fz.epoch = epoch;
         }
-        return launch_reduce(shards[g], n[g], dtype, (char *)c.d_slots + 8 * g, c.ws, c.ws_bytes,
-                             devs[g], c.s_comp, fz);
+        return launch_reduce(shards[g], n[g], dtype, (char *)c.d_slots + 8 * g, c.ws_pipe, c.ws_bytes,
+                             devs[g], c.s_comp, fz, /*acc_out=*/true);
     };
     for (int g = 1; g < nshards; ++g)
         if (int rc = launch(g)) return rc;
@@ -1036,8 +1047,9 @@ int b2_reduce_sum_multi(const void *const *shards, const int64_t *n, int nshards
         uint64_t st = 0;
         if (int rc = check_dev(root)) return rc;
         B2_CUDA(cudaMemcpy(&st, (char *)rc_.mailbox + 4 * 64 * 8 + 64 * 8 + 8, 8, cudaMemcpyDeviceToHost));
-        if (st) return fail(B2_ERR_CUDA, "reduce_multi: fused combine timed out");
-        memcpy(host_out, &part[0], dtype == B2_F32 ? 4 : 8);
+        if (st >= epoch) return fail(B2_ERR_CUDA, "reduce_multi: fused combine timed out");
+        if (dtype == B2_F32) *(float *)host_out = (float)*(const double *)&part[0];
+        else memcpy(host_out, &part[0], 8);
         return B2_OK;
     }
     // host combine, shard order (the fused kernel's order: identical result)
@@ -1045,10 +1057,10 @@ int b2_reduce_sum_multi(const void *const *shards, const int64_t *n, int nshards
         long long s = 0;
         for (int g = 0; g < nshards; ++g) s += *(const long long *)&part[8 * g];
         *(long long *)host_out = s;
-    } else if (dtype == B2_F32) {
-        volatile float s = 0.0f;
-        for (int g = 0; g < nshards; ++g) s = s + *(const float *)&part[8 * g];
-        *(float *)host_out = s;
+    } else if (dtype == B2_F32) {  // binary64 shard partials (the fused kernel's order)
+        double s = 0.0;
+        for (int g = 0; g < nshards; ++g) s += *(const double *)&part[8 * g];
+        *(float *)host_out = (float)s;
     } else {
         double s = 0.0;
         for (int g = 0; g < nshards; ++g) s += *(const double *)&part[8 * g];

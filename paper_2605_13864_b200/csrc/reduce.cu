@@ -6,7 +6,9 @@
 // reduce_kernel (the HBM-bound hot path), one launch per reduction:
 //   1. persistent grid (SMs x resident CTAs), 128-bit ld.global.nc grid-stride
 //      loads, U independent loads in flight per thread, per-thread accumulator
-//      (int32 -> int64 so the sum is exact like the reference's Python ints);
+//      (int32 -> int64 so the sum is exact like the reference's Python ints;
+//      fp32 -> binary64, rounded to binary32 once at the end: the result is the
+//      correctly rounded sum up to ~n 2^-53 sum|x|, whatever the conditioning);
 //   2. warp __shfl_down_sync tree;
 //   3. shared-memory block tree over the warp partials with one __syncthreads per
 //      level (the barrier structure the paper verifies);
@@ -18,6 +20,7 @@
 // with the reference interpreter (each warp evaluates one 512-element block's
 // tree in registers: the same DAG of binary32 adds as the smem halving loop).
 #include <algorithm>
+#include <type_traits>
 
 #include "b2_internal.cuh"
 
@@ -26,9 +29,13 @@ namespace {
 
 template <typename T>
 struct AccOf;
+// fp32 cells accumulate in binary64 (every float is exact in a double, and the
+// chains below stay far from 2^53 ulps): ~0.5 ulp of the binary32 result instead of
+// the ~L u sum|x| of an L-long binary32 chain. Costs one F2F per cell, well under
+// the conversion throughput the HBM stream needs (6 cells/clk/SM).
 template <>
 struct AccOf<float> {
-    using type = float;
+    using type = double;
 };
 template <>
 struct AccOf<int32_t> {
@@ -48,9 +55,9 @@ struct AccOf<int64_t> {
 template <typename T, typename A>
 __device__ __forceinline__ A vec_sum(const uint4 &v);
 template <>
-__device__ __forceinline__ float vec_sum<float, float>(const uint4 &v) {
-    return (__uint_as_float(v.x) + __uint_as_float(v.y)) +
-           (__uint_as_float(v.z) + __uint_as_float(v.w));
+__device__ __forceinline__ double vec_sum<float, double>(const uint4 &v) {
+    return ((double)__uint_as_float(v.x) + (double)__uint_as_float(v.y)) +
+           ((double)__uint_as_float(v.z) + (double)__uint_as_float(v.w));
 }
 template <>
 __device__ __forceinline__ long long vec_sum<int32_t, long long>(const uint4 &v) {
@@ -88,6 +95,19 @@ __device__ __forceinline__ A load_partial(const A *p) {
     }
 }
 
+// The result cell: fp32 sums are returned as binary32 (one rounding of the binary64
+// total) unless the caller asked for the raw accumulator (acc_out: the library's
+// own chunked / multi-shard pipelines combine binary64 partials and round once).
+template <typename T, typename A>
+__device__ __forceinline__ void store_result(void *out, A v, bool acc_out) {
+    if constexpr (sizeof(T) == 4 && sizeof(A) == 8 && !std::is_integral<T>::value) {
+        if (acc_out) *static_cast<double *>(out) = (double)v;
+        else *static_cast<float *>(out) = (float)v;
+    } else {
+        *static_cast<A *>(out) = v;
+    }
+}
+
 template <typename A>
 __device__ __forceinline__ A warp_tree(A a) {
 #pragma unroll
@@ -119,11 +139,13 @@ __device__ __forceinline__ A block_tree(A a, A *sm) {
 // waits for written[g] >= e for every g (acquire), sums the slots in rank order
 // (deterministic for fp32) and publishes consumed = e. A writer may only reuse a
 // slot row after the root consumed the epoch that last used it (window kEpochs).
-// Every wait is bounded (kSpinNs): on timeout the status word is set and the
-// kernel exits instead of hanging the device.
+// Every wait is bounded (fz.spin_ns, tune key reduce.spin_ms, default 20 s): on timeout the status word records the epoch
+// (atomicMax: it holds the latest failed epoch, so one timeout does not poison
+// later healthy calls) and the kernel exits instead of hanging the device; the
+// root still publishes consumed = e, so writers of later epochs are not stalled
+// behind the abandoned one.
 constexpr int kEpochs = 4;
 constexpr int kMaxRanks = 64;
-constexpr unsigned long long kSpinNs = 20ull * 1000 * 1000 * 1000;
 
 using Fused = FusedCombine;
 
@@ -142,11 +164,13 @@ __device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned l
 }
 // wait until *p >= want; false on timeout (status word set)
 __device__ __forceinline__ bool wait_ge(const unsigned long long *p, unsigned long long want,
-                                        unsigned long long *status) {
+                                        unsigned long long *status, unsigned long long epoch,
+                                        unsigned long long spin_ns) {
     const unsigned long long t0 = gtimer();
     while (ld_acquire_sys(p) < want) {
-        if (gtimer() - t0 > kSpinNs) {
-            atomicExch(status, 1ull);
+        if (gtimer() - t0 > spin_ns) {
+            atomicMax(status, epoch);
+            __threadfence_system();
             return false;
         }
         __nanosleep(200);
@@ -154,8 +178,8 @@ __device__ __forceinline__ bool wait_ge(const unsigned long long *p, unsigned lo
     return true;
 }
 
-template <typename A>
-__device__ void fused_combine(const Fused &fz, A total, A *out) {
+template <typename T, typename A>
+__device__ void fused_combine(const Fused &fz, A total, void *out, bool acc_out) {
     unsigned char *mb = static_cast<unsigned char *>(fz.mailbox);
     A *slots = reinterpret_cast<A *>(mb);  // 8-byte slots: A is float, long long or double
     unsigned long long *written = reinterpret_cast<unsigned long long *>(mb + kEpochs * kMaxRanks * 8);
@@ -164,26 +188,27 @@ __device__ void fused_combine(const Fused &fz, A total, A *out) {
     const int row = (int)(fz.epoch % kEpochs) * kMaxRanks * (8 / (int)sizeof(A));
     const int stride = 8 / (int)sizeof(A);
     if (fz.rank != 0 && fz.epoch > kEpochs - 1)  // slot row free again?
-        if (!wait_ge(consumed, fz.epoch - (kEpochs - 1), status)) {
-            *out = total;
+        if (!wait_ge(consumed, fz.epoch - (kEpochs - 1), status, fz.epoch, fz.spin_ns)) {
+            store_result<T, A>(out, total, acc_out);
             return;
         }
     *reinterpret_cast<volatile A *>(slots + row + fz.rank * stride) = total;
     __threadfence_system();
     st_release_sys(written + fz.rank, fz.epoch);
     if (fz.rank != 0) {
-        *out = total;
+        store_result<T, A>(out, total, acc_out);
         return;
     }
     A s = A(0);
     for (int g = 0; g < fz.nranks; ++g) {
-        if (!wait_ge(written + g, fz.epoch, status)) {
-            *out = total;
+        if (!wait_ge(written + g, fz.epoch, status, fz.epoch, fz.spin_ns)) {
+            store_result<T, A>(out, total, acc_out);
+            st_release_sys(consumed, fz.epoch);  // abandon this epoch, free its slot row
             return;
         }
         s += *reinterpret_cast<volatile A *>(slots + row + g * stride);
     }
-    *out = s;
+    store_result<T, A>(out, s, acc_out);
     __threadfence_system();
     st_release_sys(consumed, fz.epoch);
 }
@@ -217,9 +242,8 @@ __device__ __forceinline__ VecW<W> ldg_w(const VecW<W> *p) {
 template <typename T, int NT, int U, int W = 1>
 __global__ void __launch_bounds__(NT)
     reduce_kernel(const T *__restrict__ in, int64_t head, int64_t nvec, int64_t n,
-                  typename AccOf<T>::type *__restrict__ out,
-                  typename AccOf<T>::type *__restrict__ partials, unsigned *__restrict__ ticket,
-                  Fused fz) {
+                  void *__restrict__ out, typename AccOf<T>::type *__restrict__ partials,
+                  unsigned *__restrict__ ticket, Fused fz, bool acc_out) {
     using A = typename AccOf<T>::type;
     constexpr int V = 16 / sizeof(T);
     __shared__ A sm[NT / 32];
@@ -278,10 +302,10 @@ __global__ void __launch_bounds__(NT)
     if (threadIdx.x == 0) {
         *ticket = 0u;  // re-arm for the next call on this workspace
         if constexpr (sizeof(A) <= 8) {
-            if (fz.mailbox) fused_combine<A>(fz, total, out);
-            else *out = total;
+            if (fz.mailbox) fused_combine<T, A>(fz, total, out, acc_out);
+            else store_result<T, A>(out, total, acc_out);
         } else {
-            *out = total;  // 128-bit results are not combined across GPUs (8-byte slots)
+            store_result<T, A>(out, total, acc_out);  // 128-bit results: no cross-GPU combine (8-byte slots)
         }
     }
 }
@@ -325,7 +349,7 @@ int max_grid(int dev) { return num_sms(dev) * (2048 / kMinNT); }
 
 template <typename T, int NT, int U, int W = 1>
 int run_reduce_v(const T *in, int64_t n, void *out, void *ws, int dev, cudaStream_t st,
-                 const Fused &fz) {
+                 const Fused &fz, bool acc_out) {
     using A = typename AccOf<T>::type;
     constexpr int V = 16 / sizeof(T);
     // head: elements before the first (16 W)-byte boundary; nvec: whole W-vectors
@@ -349,7 +373,7 @@ int run_reduce_v(const T *in, int64_t n, void *out, void *ws, int dev, cudaStrea
     const int grid = (int)std::min(cap, need);
     unsigned *ticket = (unsigned *)ws;
     A *partials = (A *)((char *)ws + 64);
-    reduce_kernel<T, NT, U, W><<<grid, NT, 0, st>>>(in, head, nvec, n, (A *)out, partials, ticket, fz);
+    reduce_kernel<T, NT, U, W><<<grid, NT, 0, st>>>(in, head, nvec, n, out, partials, ticket, fz, acc_out);
     count_launch();
     B2_CUDA(cudaGetLastError());
     return B2_OK;
@@ -358,51 +382,56 @@ int run_reduce_v(const T *in, int64_t n, void *out, void *ws, int dev, cudaStrea
 // <threads, loads in flight per thread> variants; g_tune.r_variant picks one.
 template <typename T>
 int run_reduce(const void *in_, int64_t n, void *out, void *ws, size_t ws_bytes, int dev,
-               cudaStream_t st, const Fused &fz) {
+               cudaStream_t st, const Fused &fz, bool acc_out) {
     using A = typename AccOf<T>::type;
     const T *in = (const T *)in_;
     if ((uintptr_t)in % sizeof(T)) return fail(B2_ERR_INVALID, "reduce: misaligned input");
     const size_t need = (size_t)max_grid(dev) * sizeof(A) + 64;
     if (ws_bytes < need) return fail(B2_ERR_INVALID, "reduce: workspace too small");
     switch (g_tune.r_variant) {
-    case 1: return run_reduce_v<T, 512, 8>(in, n, out, ws, dev, st, fz);
-    case 2: return run_reduce_v<T, 256, 8>(in, n, out, ws, dev, st, fz);
-    case 3: return run_reduce_v<T, 1024, 4>(in, n, out, ws, dev, st, fz);
-    case 4: return run_reduce_v<T, 256, 16>(in, n, out, ws, dev, st, fz);
-    case 5: return run_reduce_v<T, 512, 4, 2>(in, n, out, ws, dev, st, fz);   // 256-bit loads
-    case 6: return run_reduce_v<T, 512, 2, 2>(in, n, out, ws, dev, st, fz);
-    case 7: return run_reduce_v<T, 256, 4, 2>(in, n, out, ws, dev, st, fz);
-    case 8: return run_reduce_v<T, 1024, 2, 2>(in, n, out, ws, dev, st, fz);
-    case 9: return run_reduce_v<T, 512, 4>(in, n, out, ws, dev, st, fz);
+    case 1: return run_reduce_v<T, 512, 8>(in, n, out, ws, dev, st, fz, acc_out);
+    case 2: return run_reduce_v<T, 256, 8>(in, n, out, ws, dev, st, fz, acc_out);
+    case 3: return run_reduce_v<T, 1024, 4>(in, n, out, ws, dev, st, fz, acc_out);
+    case 4: return run_reduce_v<T, 256, 16>(in, n, out, ws, dev, st, fz, acc_out);
+    case 5: return run_reduce_v<T, 512, 4, 2>(in, n, out, ws, dev, st, fz, acc_out);   // 256-bit loads
+    case 6: return run_reduce_v<T, 512, 2, 2>(in, n, out, ws, dev, st, fz, acc_out);
+    case 7: return run_reduce_v<T, 256, 4, 2>(in, n, out, ws, dev, st, fz, acc_out);
+    case 8: return run_reduce_v<T, 1024, 2, 2>(in, n, out, ws, dev, st, fz, acc_out);
+    case 9: return run_reduce_v<T, 512, 4>(in, n, out, ws, dev, st, fz, acc_out);
     default:
         // 128-bit loads. The 256-bit variants (5-8) read 1-2 % faster in isolation but
         // slowed the FOLLOWING transpose in the bench step by 4 % (A/B of whole bench
         // steps, profiles/r01j_ldst_variants.md), so they stay opt-in.
-        return run_reduce_v<T, 512, 4, B2_REDUCE_DEFAULT_W>(in, n, out, ws, dev, st, fz);
+        return run_reduce_v<T, 512, 4, B2_REDUCE_DEFAULT_W>(in, n, out, ws, dev, st, fz, acc_out);
     }
 }
 
 }  // namespace
 
 size_t reduce_ws_bytes(int64_t, int dtype, int dev) {
-    size_t a = dtype == B2_F32 ? 4 : dtype == B2_I64 ? 16 : 8;
+    size_t a = dtype == B2_I64 ? 16 : 8;  // fp32 partials are binary64
     return (size_t)max_grid(dev) * a + 64;
 }
 
 size_t mailbox_bytes() { return 4096; }
 
 int launch_reduce(const void *in, int64_t n, int dtype, void *out, void *ws, size_t ws_bytes,
-                  int dev, cudaStream_t st, const FusedCombine &fz) {
+                  int dev, cudaStream_t st, const FusedCombine &fz, bool acc_out) {
     if (fz.mailbox && (fz.nranks < 1 || fz.nranks > kMaxRanks || fz.rank < 0 || fz.rank >= fz.nranks ||
                        fz.epoch == 0))
         return fail(B2_ERR_INVALID, "fused combine: bad rank / nranks / epoch");
+    if (fz.mailbox && fz.spin_ns == 0) {
+        FusedCombine f2 = fz;
+        f2.spin_ns = (unsigned long long)std::max(1, g_tune.r_spin_ms) * 1000000ull;
+        return launch_reduce(in, n, dtype, out, ws, ws_bytes, dev, st, f2, acc_out);
+    }
     switch (dtype) {
-    case B2_F32: return run_reduce<float>(in, n, out, ws, ws_bytes, dev, st, fz);
-    case B2_I32: return run_reduce<int32_t>(in, n, out, ws, ws_bytes, dev, st, fz);
-    case B2_F64: return run_reduce<double>(in, n, out, ws, ws_bytes, dev, st, fz);
+    case B2_F32: return run_reduce<float>(in, n, out, ws, ws_bytes, dev, st, fz, acc_out);
+    case B2_I32: return run_reduce<int32_t>(in, n, out, ws, ws_bytes, dev, st, fz, acc_out);
+    case B2_F64: return run_reduce<double>(in, n, out, ws, ws_bytes, dev, st, fz, acc_out);
     case B2_I64:
         if (fz.mailbox) return fail(B2_ERR_UNSUPPORTED, "fused combine: int64 sums are 128-bit");
-        return run_reduce<int64_t>(in, n, out, ws, ws_bytes, dev, st, fz);
+        return run_reduce<int64_t>(in, n, out, ws, ws_bytes, dev, st, fz, acc_out);
     default: return fail(B2_ERR_UNSUPPORTED, "reduce: dtype must be B2_F32, B2_I32, B2_I64 or B2_F64");
     }
 }

@@ -155,9 +155,17 @@ __global__ void __launch_bounds__(NT)
                 const int orow = idx / (TRV / 2), ocp = idx % (TRV / 2);
                 const int64_t oc = c0 + orow, orr = r0 + 2 * ocp * V;
                 if (oc < cols_v && orr < rows_v) {
-                    const uint4 a = S[orow * TRV + ((2 * ocp) ^ ((orow / V) & 7))];
+                    // Bank-conflict-free pair reads: a quarter-warp (8 lanes x 16 B) must
+                    // touch all eight 16-B bank groups. Lanes 0-3 of each quarter read their
+                    // even chunk first, lanes 4-7 their odd chunk first (chunk indices mod 8
+                    // then cover 0..7), and the pair is put back in order in registers.
+                    const int sw = (orow / V) & 7;
+                    const int odd_first = (idx >> 2) & 1;
+                    const uint4 p0 = S[orow * TRV + ((2 * ocp + odd_first) ^ sw)];
+                    const uint4 p1 = S[orow * TRV + ((2 * ocp + 1 - odd_first) ^ sw)];
+                    const uint4 a = odd_first ? p1 : p0;
                     if (orr + V < rows_v) {
-                        const uint4 b = S[orow * TRV + ((2 * ocp + 1) ^ ((orow / V) & 7))];
+                        const uint4 b = odd_first ? p0 : p1;
                         asm volatile("st.global.L1::no_allocate.L2::evict_first.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
                                      ::"l"(out + oc * ld_out_b + orr * E),
                                      "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)

@@ -136,11 +136,16 @@ class FusedReduce:
             self.epoch, self.dev, ops._stream_ptr(x, stream)))
         return out
 
-    def status(self) -> int:
-        """0 = healthy; 1 = a bounded wait timed out (a rank never published)."""
+    def failed_epoch(self) -> int:
+        """Latest epoch whose combine timed out on this rank's view (0 = never)."""
         s = self._ct.c_uint64(0)
         self._check(self._lib.b2_mailbox_status(self.mailbox, self.dev, self._ct.byref(s)))
         return int(s.value)
+
+    def status(self) -> int:
+        """Status of the latest call: 0 = healthy; 1 = a bounded wait of this epoch
+        timed out (a rank never published). Earlier timeouts do not stick."""
+        return 1 if self.epoch and self.failed_epoch() >= self.epoch else 0
 
     def close(self):
         if self.mailbox:

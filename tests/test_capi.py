@@ -85,3 +85,12 @@ def test_multi_argument_validation():
     assert L.b2_reduce_sum_multi(vp2, neg, 2, _lib.I32, ctypes.addressof(out)) == _lib.B2_ERR_INVALID
     assert L.b2_reduce_sum_multi(vp2, i2, 2, _lib.I32, None) == _lib.B2_ERR_INVALID
     assert L.b2_peer_access(-1, 0) == 0
+
+
+def test_build_id_matches_sources():
+    """freshness is decided by content, not mtimes. The
+    loaded library embeds the sha256 prefix of csrc/ + include/b2k.h + flags."""
+    from paper_2605_13864_b200 import _build, _lib
+    L = _lib.lib()
+    assert L.b2_build_id().decode() == "b2k-build-" + _build.source_id()
+    assert _build.lib_is_current()

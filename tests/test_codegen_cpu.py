@@ -122,3 +122,31 @@ def test_launch_uniform_thread_for_levels_are_hoisted():
     assert kernel.count("const uint32_t _hp") == 6  # by, bx and two (y, x) pairs
     assert "B2CK ? b2_w0 / (uint32_t)" in kernel
     assert host.count("_w2 = (uint32_t)(_w /") == 6 and "throw B2NoProof{}" in host
+
+
+def test_assignment_to_loop_index_refused():
+    """the reference raises `'k' is not assignable`
+    (interp.py:271-272); the generator used to emit a mutable counter the bounds
+    proof still trusted."""
+    for loop in ("for", "thread for"):
+        src = ("void f(float* a, int N) { float* const d = gmem_malloc1<float>(N); { kernel_launch(1, 1, 0); "
+               f"kernel_setup_end(); {loop} (int k = 0; k < 1; k++) {{ k = k + 1000000; d[k] = 1.0; }} "
+               "kernel_teardown_begin(); kernel_kill(); } memcpy_device_to_host1(a, d, N); gmem_free(d); }")
+        with pytest.raises(UnsupportedProgram, match="'k' is not assignable"):
+            codegen.generate(parse_program(src).entry())
+    src = ("void f(float* a, int N) { float* const d = gmem_malloc1<float>(N); for (int k = 0; k < 2; k++) "
+           "{ k = 3; } { kernel_launch(1, 1, 0); kernel_setup_end(); kernel_teardown_begin(); kernel_kill(); } "
+           "gmem_free(d); }")
+    with pytest.raises(UnsupportedProgram, match="'k' is not assignable"):
+        codegen.generate(parse_program(src).entry())
+
+
+def test_block_scoped_declarations():
+    """A declaration inside a block shadows the outer name only inside the block
+    (interp.py:248-249): afterwards the loop index is an int again and the kernel
+    still compiles with both bindings."""
+    src = ("void f(float* a, int N) { float* const d = gmem_malloc1<float>(N); { kernel_launch(1, 1, 0); "
+           "kernel_setup_end(); for (int k = 0; k < 4; k++) { if (N > 0) { float k = 0.5; d[0] = k; } d[k] = 1.0; } "
+           "kernel_teardown_begin(); kernel_kill(); } memcpy_device_to_host1(a, d, N); gmem_free(d); }")
+    s = codegen.generate(parse_program(src).entry())
+    assert "float v_k" in s and "int64_t v_k" in s

@@ -99,6 +99,9 @@ def _gen_bounds(rng):
     src_ix = f"b * {T} + t * {S} + {E}"
     if rng.random() < 0.3:
         src_ix = f"({src_ix}) % {rng.choice([B * T, B * T + 1, B * T - 1])}"
+    # a block-local declaration shadowing the thread index must not narrow the
+    # outer `t` for the proof (interval leaked out of the block)
+    shadow = f"if (N > 0) {{ int t = {rng.choice([0, 1])}; }}" if rng.random() < 0.4 else ""
     src = f"""void f(float* a, float* r, int N) {{
     float* const d = gmem_malloc1<float>(N);
     memcpy_host_to_device1(d, a, N);
@@ -109,6 +112,7 @@ def _gen_bounds(rng):
         kernel_setup_end();
         thread for (int b = 0; b < {B}; b++) {{
             thread for (int t = 0; t < {T}; t++) {{
+                {shadow}
                 if (t < {lim}) {{ o[b * {T} + t + {D}] = d[{src_ix}] * 2.0; }}
             }}
         }}
@@ -149,3 +153,36 @@ def test_random_bounds_programs_proof_is_sound():
                                   np.array(want["r"], np.float32).view(np.uint32)), src
             proved += all(c.kernel_unchecked())
     assert errors >= 5 and proved >= 5, (errors, proved)
+
+
+SHADOW = """void f(float* a, int N) {
+    float* const d = gmem_malloc1<float>(N);
+    {
+        kernel_launch(1, 1, 0);
+        kernel_setup_end();
+        for (int k = 0; k < 10; k++) {
+            if (N > 0) { int k = 5; d[k] = 2.0; }
+            d[k] = 1.0;
+        }
+        kernel_teardown_begin();
+        kernel_kill();
+    }
+    memcpy_device_to_host1(a, d, N);
+    gmem_free(d);
+}
+"""
+
+
+def test_shadowing_decl_does_not_fool_the_proof():
+    """the inner `int k = 5` used to replace the loop's interval
+    for the outer d[k]; with N = 6 the check-free kernel ran and wrote d[6..9]. The
+    reference raises `index 6 out of bounds 0..6` (checked in the build container)."""
+    from paper_2605_13864_b200 import codegen
+    p = b2.parse_program(SHADOW)
+    with pytest.raises(b2.InterpError, match=r"index 6 out of bounds"):
+        b2.run_program(p, "f", {"a": [0.0] * 6, "N": 6}, backend="codegen")
+    assert not any(codegen.compile_fn(p.fn("f")).kernel_unchecked())
+    # in bounds (N = 10): proved, and the result is the reference's
+    _, got = b2.run_program(p, "f", {"a": [0.0] * 10, "N": 10}, backend="codegen")
+    assert got["a"] == [1.0] * 10
+    assert all(codegen.compile_fn(p.fn("f")).kernel_unchecked())

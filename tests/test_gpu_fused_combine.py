@@ -74,3 +74,30 @@ def test_fused_combine_two_processes():
         assert p.exitcode == 0
     res = dict(q.get() for _ in range(2))
     assert res[0] and res[1]
+
+
+def test_timeout_does_not_poison_later_epochs():
+    """a timed-out epoch used to leave the status word at 1 for
+    ever. Now the status records the failed epoch, the root still releases the
+    slot row, and the next healthy epoch reports 0 with the right sum."""
+    import torch
+    from paper_2605_13864_b200 import _lib, shard
+    old = _lib.tuning("reduce.spin_ms")
+    _lib.tune("reduce.spin_ms", 200)
+    try:
+        fr = shard.FusedReduce()  # no process group: rank 0 of 1
+        x = torch.arange(1, 1001, dtype=torch.int32, device="cuda")
+        fr.world = 2  # wait for a rank 1 that never publishes
+        fr(x)
+        torch.cuda.synchronize()
+        assert fr.status() == 1 and fr.failed_epoch() == 1
+        fr.world = 1
+        for _ in range(6):  # past the 4-epoch slot window
+            out = fr(x)
+            torch.cuda.synchronize()
+            assert int(out.item()) == 500500
+            assert fr.status() == 0
+        assert fr.failed_epoch() == 1
+        fr.close()
+    finally:
+        _lib.tune("reduce.spin_ms", old)

@@ -49,11 +49,12 @@ def test_golden_cases_through_run_program(b2, golden):
                 exact, absum = oracle.sum_f64(x)
                 ref = float(np.uint32(c["result_f32_bits"]).view(np.float32))
                 assert isinstance(ret, float) and float(np.float32(ret)) == ret
-                assert abs(ret - exact) <= oracle.f32_tolerance(x.size, exact, absum), c["id"]
-                # the GPU (tree order) and the reference (sequential) differ by at most the
-                # reference's own worst-case sequential error plus the tolerance
-                assert abs(ret - ref) <= oracle.f32_seq_error_bound(x.size, absum) + \
-                    oracle.f32_tolerance(x.size, exact, absum), c["id"]
+                tol = oracle.f32_tolerance(x.size, exact, absum)
+                assert abs(ret - exact) <= tol, c["id"]
+                assert abs(ret - exact) <= oracle.f32_gpu_bound(x.size, exact, absum), c["id"]
+                # the GPU and the reference (sequential binary32) differ by at most the
+                # reference's own measured error plus the tolerance
+                assert abs(ret - ref) <= oracle.ref_consistency_bound(ref, exact, tol), c["id"]
             assert outs["arr"] == x.tolist() or "tree" in c["program"] or "result_int" in c
 
 

@@ -102,3 +102,23 @@ def test_run_program_reentrant():
         assert ret == sum(x), k
 
     _run_threads(work)
+
+
+def test_generated_program_from_threads():
+    """ADVICE r01: generated programs keep per-call state in statics of their .so;
+    concurrent calls of the SAME compiled program must neither free each other's
+    allocations nor mix up results."""
+    import paper_2605_13864_b200 as b2
+    prog = b2.parse_program(program_text("transpose_gpu.optc"))
+
+    def work(k):
+        rng = np.random.default_rng(50 + k)
+        H, W = 32 * (2 + k), 32 * (5 - k % 3)
+        for it in range(3):
+            a = rng.standard_normal((H, W)).astype(np.float32)
+            _, outs = b2.run_program(prog, "transpose", {"in": b2.Array([H, W], a.reshape(-1).tolist(), "float"),
+                                                         "out": b2.Array.alloc([W, H], "float"), "W": W, "H": H},
+                                     backend="codegen")
+            assert outs["out"] == a.T.reshape(-1).tolist(), (k, it)
+
+    _run_threads(work)

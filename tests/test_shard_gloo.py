@@ -58,7 +58,7 @@ def _worker(rank, world, port, kind, q):
                 want = np.float32(want + np.float32(p))
             exact, absum = oracle.sum_f64(x)
             q.put(("reduce_f32", rank, tot == float(want) and
-                   abs(tot - exact) <= oracle.f32_tolerance(n, exact, absum) + oracle.f32_seq_error_bound(n, absum)))
+                   abs(tot - exact) <= oracle.f32_tolerance(n, exact, absum)))
     finally:
         dist.destroy_process_group()
 

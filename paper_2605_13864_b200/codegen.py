@@ -46,7 +46,7 @@ import numpy as np
 from .errors import InterpError, UnsupportedProgram
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-GEN_DIR = os.path.join(PKG, "_gen")
+GEN_DIR = os.path.join(PKG, "progcache")  # compiled generated programs (git-ignored)
 MAX_RANK = 8
 
 # ----------------------------------------------------------------------------- helpers

@@ -54,6 +54,9 @@ struct Tuning {
     int t_tma_stages = 2;   // input stages in flight per CTA (2, 3, 4, 6); 2 x 2 CTAs/SM measured best
     int t_scalar_tile = 0;  // padded scalar tile width: 0 = auto (2-byte 128, else 64), 64, 128 (2/4-byte)
     int r_spin_ms = 20000;  // fused combine: bounded wait per epoch before giving up (status word)
+    int t_staged = 1;       // odd pitches / unaligned views: 1 = cp.async-staged kernel, 0 = padded scalar tile
+    int t_staged_ctas = 0;  // CTAs per SM of the staged kernel (0 = 2)
+    int t_staged_stages = 4;  // cp.async ring depth of the staged kernel (2, 3, 4)
 };
 extern Tuning g_tune;
 constexpr int kInflightBytesPerSM = 64 * 1024;
@@ -91,6 +94,8 @@ int launch_transpose_tma(const void *in, void *out, int64_t rows, int64_t cols, 
                          int64_t ld_out, int dev, cudaStream_t st);
 int launch_transpose_any(const void *in, void *out, int64_t rows, int64_t cols, int64_t ld_in,
                          int64_t ld_out, int esize, int dev, cudaStream_t st);
+int launch_transpose_staged(const void *in, void *out, int64_t rows, int64_t cols, int64_t ld_in,
+                            int64_t ld_out, int esize, int dev, cudaStream_t st);
 
 size_t reduce_ws_bytes(int64_t n, int dtype, int dev);
 // Cross-GPU combine fused into the reduction's last CTA (reduce.cu): mailbox is a

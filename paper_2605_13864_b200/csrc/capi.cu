@@ -323,6 +323,9 @@ static int *tune_slot(const char *key) {
     if (k == "transpose.scalar_tile") return &g_tune.t_scalar_tile;
     if (k == "host.chunk_mb") return &g_tune.h_chunk_mb;
     if (k == "reduce.spin_ms") return &g_tune.r_spin_ms;
+    if (k == "transpose.staged") return &g_tune.t_staged;
+    if (k == "transpose.staged_ctas") return &g_tune.t_staged_ctas;
+    if (k == "transpose.staged_stages") return &g_tune.t_staged_stages;
     return nullptr;
 }
 

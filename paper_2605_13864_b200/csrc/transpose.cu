@@ -428,6 +428,10 @@ int dispatch(const void *in, void *out, int64_t rows, int64_t cols, int64_t ld_i
         // odd pitches / unaligned views: funnel-shifted 128-bit path (transpose_any.cu)
         if constexpr (E >= 2) {
             if (g_tune.t_any) return launch_transpose_any(in, out, rows, cols, ld_in, ld_out, E, dev, st);
+            // cp.async-staged 16-B chunks (transpose_staged.cu) unless the cells themselves
+            // are misaligned (then only the scalar tile applies)
+            if (g_tune.t_staged && (uintptr_t)in % E == 0 && (uintptr_t)out % E == 0)
+                return launch_transpose_staged(in, out, rows, cols, ld_in, ld_out, E, dev, st);
         }
         return run_scalar<T>(in, out, 0, rows, 0, cols, ld_in, ld_out, dev, st);
     }

@@ -229,29 +229,64 @@ def test_launch_counter(b2):
     assert b2.launch_count() == n0 + 1
 
 
-@pytest.mark.parametrize("path", [0, 1])
+_PATHS = {"staged": {"transpose.any": 0, "transpose.staged": 1},
+          "scalar": {"transpose.any": 0, "transpose.staged": 0},
+          "any": {"transpose.any": 1, "transpose.staged": 0}}
+
+
+def _with_path(path, fn):
+    from paper_2605_13864_b200 import _lib
+    for k, v in _PATHS[path].items():
+        _lib.tune(k, v)
+    try:
+        return fn()
+    finally:
+        _lib.tune("transpose.any", 0)
+        _lib.tune("transpose.staged", 1)
+
+
+@pytest.mark.parametrize("path", ["staged", "scalar", "any"])
 @pytest.mark.parametrize("dt", [torch.bfloat16, torch.float32, torch.float64])
 @pytest.mark.parametrize("rows,cols,oin,oout", [(63, 65, 1, 3), (130, 257, 3, 0), (1, 77, 1, 1), (77, 2, 0, 1),
                                                 (129, 129, 5, 7), (2000, 3, 1, 0), (3, 2000, 0, 2),
                                                 (1025, 1023, 7, 5)])
 def test_unaligned_views(b2, path, dt, rows, cols, oin, oout):
-    # misaligned bases and odd pitches: padded scalar tile (path 0, default) and the
-    # funnel-shift kernel (path 1); neighbours of the output view must stay untouched
-    from paper_2605_13864_b200 import _lib
+    # misaligned bases and odd pitches: the cp.async-staged kernel (default), the
+    # padded scalar tile and the funnel-shift kernel; neighbours of the output view
+    # must stay untouched
     iv = {torch.bfloat16: torch.int16, torch.float32: torch.int32, torch.float64: torch.int64}[dt]
     src = torch.randn(rows, cols + oin + 3, device="cuda").to(dt)
     view = src[:, oin:oin + cols]
     dst = torch.full((cols, rows + oout + 5), 7.0, device="cuda").to(dt)
     oview = dst[:, oout:oout + rows]
-    _lib.tune("transpose.any", path)
-    try:
-        b2.transpose(view, oview)
-    finally:
-        _lib.tune("transpose.any", 0)
+    _with_path(path, lambda: b2.transpose(view, oview))
     torch.cuda.synchronize()
     assert torch.equal(oview.view(iv), view.t().contiguous().view(iv))
     rest = torch.cat([dst[:, :oout].reshape(-1), dst[:, oout + rows:].reshape(-1)])
     assert bool((rest == 7.0).all())
+
+
+@pytest.mark.parametrize("stages,ctas", [(4, 0), (3, 3), (2, 1)])
+@pytest.mark.parametrize("dt", [torch.int16, torch.int32, torch.int64])
+@pytest.mark.parametrize("rows,cols", [(4097, 8191), (16385, 16383), (777, 100003), (100003, 65), (64, 129)])
+def test_staged_odd_pitch_full(b2, stages, ctas, dt, rows, cols):
+    """The cp.async-staged kernel on the C5 odd shapes (every pitch odd, so every
+    row starts at a different 16-B phase), all ring depths / residencies, whole
+    result against the CPU oracle."""
+    from paper_2605_13864_b200 import _lib
+    if dt == torch.int64 and rows * cols > 1 << 28:
+        pytest.skip("covered by the 2-/4-byte cases")
+    info = torch.iinfo(dt)
+    a = torch.randint(info.min, info.max, (rows, cols), device="cuda", dtype=dt)
+    _lib.tune("transpose.staged_stages", stages)
+    _lib.tune("transpose.staged_ctas", ctas)
+    try:
+        t = b2.transpose(a)
+    finally:
+        _lib.tune("transpose.staged_stages", 4)
+        _lib.tune("transpose.staged_ctas", 0)
+    assert np.array_equal(t.cpu().numpy(), oracle.transpose(a.cpu().numpy()))
+
 
 
 @pytest.mark.parametrize("shape", [(64, 64), (1000, 1000), (333, 516), (4096, 4096), (100, 36), (65, 4100)])

@@ -92,10 +92,20 @@ def run_transpose(rng):
                            (130, 66, np.float64), (1, 1, np.float32), (1, 3000, np.float32),
                            (3000, 1, np.float32), (5, 7, np.uint8), (33, 65, np.uint16)]:
         one_transpose(rows, cols, dt, rng)
-    # odd pitches / misaligned bases -> padded scalar tile; then the funnel-shift path
-    one_transpose(200, 300, np.float32, rng, pad_in=1, pad_out=3)
+    # odd pitches / misaligned bases -> cp.async-staged kernel (every ring depth), the
+    # padded scalar tile, then the funnel-shift path
+    for stages in (4, 3, 2):
+        tune("transpose.staged_stages", stages)
+        one_transpose(200, 300, np.float32, rng, pad_in=1, pad_out=3)
+        one_transpose(130, 390, np.uint16, rng, pad_in=1, pad_out=1)
+        one_transpose(70, 45, np.float64, rng, pad_in=1, pad_out=3)
+    tune("transpose.staged_stages", 4)
     one_transpose(128, 96, np.float32, rng, off=1)
     one_transpose(120, 88, np.uint16, rng, pad_in=3, off=1)
+    tune("transpose.staged", 0)
+    one_transpose(200, 300, np.float32, rng, pad_in=1, pad_out=3)
+    one_transpose(120, 88, np.uint16, rng, pad_in=3, off=1)
+    tune("transpose.staged", 1)
     tune("transpose.any", 1)
     one_transpose(200, 300, np.float32, rng, pad_in=1, pad_out=3)
     one_transpose(128, 96, np.float64, rng, pad_in=1)

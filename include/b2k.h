@@ -181,6 +181,30 @@ B2_API int b2_copy_d2h(void *dst_host, const void *src_dev, size_t bytes, int de
 B2_API int b2_device_alloc(size_t bytes, int dev, void **out);
 B2_API int b2_device_free(void *ptr, int dev);
 
+/* Chunked copy -> kernel -> copy pipeline for generated programs (
+ * replaces the element-wise, strictly sequential memcpy_host_to_device / kernel /
+ * memcpy_device_to_host of interp.py:330-377 + intrinsics.py:137-158 and the host
+ * listing of). Step c = the H2D copies h2d[h2d_off[c] ..
+ * h2d_off[c+1]) on the library's copy stream, then launch(ctx, c, stream) on its
+ * compute stream once those copies have landed, then the D2H copies
+ * d2h[d2h_off[c] .. d2h_off[c+1]) once that launch has finished. Consecutive steps
+ * overlap: step c+1's H2D runs under step c's kernel and D2H, so both PCIe
+ * directions stream at once. Each copy is a 2-D region (height rows of width
+ * bytes; pitches in bytes); pageable host regions go through the pinned ring and
+ * the host copy threads. Ordered after the legacy default stream; returns when
+ * every step is complete (0, or the first launch / copy error). */
+typedef struct {
+    void *host;
+    int64_t host_pitch;
+    void *dev;
+    int64_t dev_pitch;
+    int64_t width;
+    int64_t height;
+} b2_copy2d;
+typedef int (*b2_step_fn)(void *ctx, int step, void *stream);
+B2_API int b2_pipe_run(int nsteps, const b2_copy2d *h2d, const int64_t *h2d_off, const b2_copy2d *d2h,
+                       const int64_t *d2h_off, b2_step_fn launch, void *ctx, int dev);
+
 /* ---- single-process multi-GPU ------------------------------
  * One host thread drives every GPU of the box. Shard g runs on the device that
  * owns its pointer, so the same call covers 1..8 GPUs (or several shards on one

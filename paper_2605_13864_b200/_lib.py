@@ -57,6 +57,7 @@ SIGNATURES = {
     "b2_copy_d2h": (_int, [_vp, _vp, _sz, _int]),
     "b2_device_alloc": (_int, [_sz, _int, ctypes.POINTER(_vp)]),
     "b2_device_free": (_int, [_vp, _int]),
+    "b2_pipe_run": (_int, [_int, _vp, _vp, _vp, _vp, _vp, _vp, _int]),
 }
 
 

@@ -103,6 +103,63 @@ def has_kernel(fn) -> bool:
     return fn.body is not None and walk(fn.body)
 
 
+def _rw_sets(scope):
+    """Names read / assigned (as arrays or scalars) anywhere inside a statement tree."""
+    reads, writes = set(), set()
+
+    def ex(e):
+        c = _cls(e)
+        if c == "Var":
+            reads.add(e.name)
+        elif c == "Access":
+            reads.add(e.base)
+            for x in e.idxs:
+                ex(x)
+        elif c == "BinOp":
+            ex(e.lhs)
+            ex(e.rhs)
+        elif c == "Call":
+            for x in e.args:
+                ex(x)
+        elif c == "Ptr":
+            for x in getattr(e, "idxs", []):
+                ex(x)
+
+    def walk(st):
+        c = _cls(st)
+        if c == "Seq":
+            for x in st.stmts:
+                walk(x)
+        elif c == "Assign":
+            writes.add(st.target.base)
+            if st.op == "+=":
+                reads.add(st.target.base)
+            for x in st.target.idxs:
+                ex(x)
+            ex(st.value)
+        elif c == "Decl":
+            if getattr(st, "init", None) is not None:
+                ex(st.init)
+            for x in getattr(st, "dims", None) or []:
+                ex(x)
+        elif c == "For":
+            ex(st.range.start)
+            ex(st.range.stop)
+            walk(st.body)
+        elif c == "If":
+            ex(st.cond)
+            walk(st.then)
+            if st.els is not None:
+                walk(st.els)
+        elif c == "CallStmt":
+            for x in st.args:
+                ex(x)
+        elif c == "Return":
+            ex(st.value)
+    walk(scope)
+    return reads, writes
+
+
 class Sym:
     """A named thing in the program: scalar or array, where it lives."""
 
@@ -239,6 +296,8 @@ extern "C" int b2g_kernel_unchecked(int k) { return (k >= 0 && k < 64) ? b2_kern
 static bool b2_prove_enabled() { const char *e = getenv("B2K_CODEGEN_PROVE"); return !(e && e[0] == '0'); }
 // Host runtime services from libb200k.so (include/b2k.h): staged / pinned bulk
 // copies, the caching device allocator, and the device this call runs on.
+typedef struct { void *host; int64_t host_pitch; void *dev; int64_t dev_pitch; int64_t width; int64_t height; } b2_copy2d;
+typedef int (*b2_step_fn)(void *, int, void *);
 struct B2Ops {
     int (*h2d)(void *, const void *, size_t, int);
     int (*d2h)(void *, const void *, size_t, int);
@@ -246,6 +305,8 @@ struct B2Ops {
     int (*alloc)(size_t, int, void **);
     int (*dfree)(void *, int);
     int64_t dev;
+    int (*pipe)(int, const b2_copy2d *, const int64_t *, const b2_copy2d *, const int64_t *, b2_step_fn, void *, int);
+    int64_t pipe_chunk;  // target bytes per pipeline step (0: pipelining off)
 };
 static const B2Ops *g_ops;
 static std::vector<void *> *g_dev_allocs;
@@ -305,6 +366,150 @@ template <typename T, typename S> static void b2_d2h(B2Host<T> &d, B2Dev<S> &s, 
     if (g_ops->d2h(d.p, s.p, (size_t)n * sizeof(T), (int)g_ops->dev))
         b2_throw(std::string("memcpy_device_to_host: ") + g_ops->last_error());
     if (d.init) memset(d.init, 1, (size_t)n);
+}
+// ---- chunked copy -> kernel -> copy pipelines (b2_pipe_run, SURVEY 8f rank 2)
+// A window `memcpy_host_to_device(d_i, h_i, n) ... kernel ... memcpy_device_to_host(h_o,
+// d_o, n)` of full-array copies runs as C block-range chunks: the footprint proof of
+// each chunk names the slab of every input it reads (copied just before it, never
+// twice) and of every output it writes (copied right after it); cells no chunk
+// writes are copied after the last one. Only proved (check-free) launches qualify.
+static int b2_kernel_piped[64];
+extern "C" int b2g_kernel_piped(int k) { return (k >= 0 && k < 64) ? b2_kernel_piped[k] : -1; }
+static cudaEvent_t b2_pev[2][64];
+static bool b2_pipe_on() { const char *e = getenv("B2K_CODEGEN_PIPE"); return !(e && e[0] == '0'); }
+static bool b2_pipe_fn() { return g_ops->pipe && g_ops->pipe_chunk > 0; }
+struct B2FP { int64_t lo[2][8][8], hi[2][8][8]; };  // [read, write][window slot][dim]
+static inline void b2fp_init(B2FP &f) {
+    for (int a = 0; a < 2; ++a) for (int b = 0; b < 8; ++b) for (int c = 0; c < 8; ++c) { f.lo[a][b][c] = INT64_MAX; f.hi[a][b][c] = INT64_MIN; }
+}
+static inline int b2fp_acc(B2FP &f, int rw, int slot, int k, B2I ix, int64_t d) {
+    b2i_in(ix, d);
+    for (int a = 0; a < 2; ++a) {
+        if (!(rw == 2 || rw == a)) continue;
+        if (ix.lo < f.lo[a][slot][k]) f.lo[a][slot][k] = ix.lo;
+        if (ix.hi > f.hi[a][slot][k]) f.hi[a][slot][k] = ix.hi;
+    }
+    return 0;
+}
+struct B2PipeArr { char *host; char *dev; int64_t es; int64_t rank; int64_t dims[8]; int slot; bool in; };
+template <typename T, typename S> static B2PipeArr b2_pipe_arr(B2Dev<T> &d, B2Host<S> &h, int slot, bool in) {
+    B2PipeArr a; a.host = (char *)h.p; a.dev = (char *)d.p; a.es = sizeof(T); a.rank = d.rank > 0 ? d.rank : 1;
+    for (int i = 0; i < 8; ++i) a.dims[i] = d.rank > 0 ? d.dims[i] : (i == 0 ? d.n : 1);
+    a.slot = slot; a.in = in; return a;
+}
+// the copy qualifies: no error the sequential code could raise, the full arrays
+template <typename T, typename S> static bool b2_pipe_ok(B2Dev<T> &d, B2Host<S> &h, int64_t n, bool in) {
+    if (sizeof(T) != sizeof(S) || d.freed || h.freed || n <= 0 || n != d.n || n != h.n || !d.p || !h.p) return false;
+    if (in && h.init) for (int64_t i = 0; i < n; ++i) if (!h.init[i]) return false;
+    return true;
+}
+template <typename A, typename B> static bool b2_disjoint(B2Host<A> &a, B2Host<B> &b) {
+    const char *a0 = (const char *)a.p, *a1 = a0 + a.n * sizeof(A), *b0 = (const char *)b.p, *b1 = b0 + b.n * sizeof(B);
+    return a1 <= b0 || b1 <= a0;
+}
+// slab [x0, x1] of dimension p (all other dimensions full) as a 2-D copy region
+static b2_copy2d b2_slab(const B2PipeArr &a, int p, int64_t x0, int64_t x1) {
+    int64_t pre = 1, inner = 1;
+    for (int i = 0; i < p; ++i) pre *= a.dims[i];
+    for (int i = p + 1; i < a.rank; ++i) inner *= a.dims[i];
+    const int64_t pitch = a.dims[p] * inner * a.es, off = x0 * inner * a.es;
+    b2_copy2d c; c.host = a.host + off; c.dev = a.dev + off; c.host_pitch = c.dev_pitch = pitch;
+    c.width = (x1 - x0 + 1) * inner * a.es; c.height = pre;
+    if (pre == 1) c.host_pitch = c.dev_pitch = c.width;
+    return c;
+}
+// a footprint box as one slab: the single dimension that is not full (or dim 0)
+static bool b2_box_slab(const B2PipeArr &a, const int64_t *lo, const int64_t *hi, int &p, int64_t &x0, int64_t &x1) {
+    if (lo[0] > hi[0]) return false;  // not accessed
+    p = -1;
+    for (int i = 0; i < a.rank; ++i) {
+        if (lo[i] > 0 || hi[i] < a.dims[i] - 1) {
+            if (p >= 0) { p = 0; x0 = 0; x1 = a.dims[0] - 1; return true; }  // several partial dims: whole array
+            p = i; x0 = lo[i]; x1 = hi[i];
+        }
+    }
+    if (p < 0) { p = 0; x0 = 0; x1 = a.dims[0] - 1; }
+    return true;
+}
+struct B2Plan {
+    int nchunk = 0;
+    std::vector<int64_t> bnd;  // block bounds, nchunk + 1
+    std::vector<b2_copy2d> h2d, d2h;
+    std::vector<int64_t> h2d_off, d2h_off;
+};
+template <class FPF> static bool b2_plan(int64_t G, int64_t align, const std::vector<B2PipeArr> &arrs, FPF &fpf, B2Plan &pl) {
+    int64_t bytes = 0;
+    for (auto &a : arrs) { int64_t n = 1; for (int i = 0; i < a.rank; ++i) n *= a.dims[i]; bytes += n * a.es; }
+    if (align < 1) align = 1;
+    const int64_t units = (G + align - 1) / align;
+    int64_t C = std::min<int64_t>(std::min<int64_t>(64, units), bytes / std::max<int64_t>(1, g_ops->pipe_chunk));
+    if (C < 2) return false;
+    pl.nchunk = (int)C;
+    pl.bnd.resize(C + 1);
+    for (int64_t c = 0; c <= C; ++c) pl.bnd[c] = std::min(G, (c * units / C) * align);
+    std::vector<std::vector<b2_copy2d>> hc(C), dc(C);
+    const size_t na = arrs.size();
+    std::vector<int> pdim(na, -1);
+    std::vector<int64_t> hi_done(na, -1);
+    std::vector<bool> banded(na, true);
+    std::vector<std::vector<std::pair<int64_t, int64_t>>> bands(na);
+    for (int64_t c = 0; c < C; ++c) {
+        B2FP fp; b2fp_init(fp);
+        fpf(pl.bnd[c], pl.bnd[c + 1], fp);
+        for (size_t k = 0; k < na; ++k) {
+            const B2PipeArr &a = arrs[k];
+            int p; int64_t x0, x1;
+            if (a.in) {  // the slab this chunk reads, minus what earlier chunks already copied
+                if (!b2_box_slab(a, fp.lo[0][a.slot], fp.hi[0][a.slot], p, x0, x1)) continue;
+                if (pdim[k] < 0) pdim[k] = p;
+                if (p != pdim[k]) { x0 = 0; x1 = a.dims[pdim[k]] - 1; }
+                if (x1 > hi_done[k]) { hc[c].push_back(b2_slab(a, pdim[k], hi_done[k] + 1, x1)); hi_done[k] = x1; }
+            } else if (banded[k]) {  // the slab this chunk writes, if disjoint from earlier ones
+                if (!b2_box_slab(a, fp.lo[1][a.slot], fp.hi[1][a.slot], p, x0, x1)) continue;
+                if (pdim[k] < 0) pdim[k] = p;
+                if (p != pdim[k] || x0 <= hi_done[k]) { banded[k] = false; continue; }
+                dc[c].push_back(b2_slab(a, p, x0, x1));
+                bands[k].push_back({x0, x1});
+                hi_done[k] = x1;
+            }
+        }
+    }
+    for (size_t k = 0; k < na; ++k) {  // the rest: after (inputs: before) the last chunk
+        const B2PipeArr &a = arrs[k];
+        const int p = pdim[k] < 0 ? 0 : pdim[k];
+        if (a.in) {
+            if (hi_done[k] < a.dims[p] - 1) hc[C - 1].push_back(b2_slab(a, p, hi_done[k] + 1, a.dims[p] - 1));
+        } else if (!banded[k] || pdim[k] < 0) {
+            dc[C - 1].push_back(b2_slab(a, 0, 0, a.dims[0] - 1));
+        } else {
+            int64_t nxt = 0;
+            for (auto &b : bands[k]) { if (b.first > nxt) dc[C - 1].push_back(b2_slab(a, p, nxt, b.first - 1)); nxt = b.second + 1; }
+            if (nxt <= a.dims[p] - 1) dc[C - 1].push_back(b2_slab(a, p, nxt, a.dims[p] - 1));
+        }
+    }
+    pl.h2d_off.push_back(0); pl.d2h_off.push_back(0);
+    for (int64_t c = 0; c < C; ++c) {
+        for (auto &x : hc[c]) pl.h2d.push_back(x);
+        for (auto &x : dc[c]) pl.d2h.push_back(x);
+        pl.h2d_off.push_back((int64_t)pl.h2d.size()); pl.d2h_off.push_back((int64_t)pl.d2h.size());
+    }
+    return true;
+}
+template <class F> static int b2_tramp(void *ctx, int c, void *s) { return (*(F *)ctx)(c, (cudaStream_t)s); }
+template <class F> static void b2_run_plan(B2Plan &pl, F &launch) {
+    for (int c = 0; c < pl.nchunk && c < 64; ++c)
+        if (!b2_pev[0][c]) { cudaEventCreate(&b2_pev[0][c]); cudaEventCreate(&b2_pev[1][c]); }
+    if (g_ops->pipe(pl.nchunk, pl.h2d.data(), pl.h2d_off.data(), pl.d2h.data(), pl.d2h_off.data(), &b2_tramp<F>,
+                    (void *)&launch, (int)g_ops->dev))
+        b2_throw(std::string("pipelined copy / kernel: ") + g_ops->last_error());
+}
+static float b2_plan_ms(const B2Plan &pl) {  // kernel time: sum over the chunk launches
+    float tot = 0;
+    for (int c = 0; c < pl.nchunk && c < 64; ++c) {
+        if (pl.bnd[c + 1] <= pl.bnd[c]) continue;
+        float ms = 0; cudaEventElapsedTime(&ms, b2_pev[0][c], b2_pev[1][c]); tot += ms;
+    }
+    return tot;
 }
 static void b2_check_kernel(int *flags_dev, const char *name) {
     cudaError_t e = cudaGetLastError();
@@ -492,8 +697,64 @@ class _Gen:
 
     # ------------------------------------------------------------------ host statements
     def host_seq(self, seq, out, ind):
-        for st in _stmts(seq):
-            self.host_stmt(st, out, ind)
+        stmts = _stmts(seq)
+        i = 0
+        while i < len(stmts):
+            w = self._window(stmts, i)
+            if w is None:
+                self.host_stmt(stmts[i], out, ind)
+                i += 1
+                continue
+            decls, h2d, k, d2h, end = w
+            for d in decls:  # the window's gmem_mallocs first (no data effect)
+                self.host_stmt(d, out, ind)
+            self.pre = []
+            self.kernel_scope(stmts[k], out, ind, window=(h2d, d2h))
+            i = end
+
+    @staticmethod
+    def _is_copy(st, prefix):
+        return (_cls(st) == "CallStmt" and st.fn.startswith(prefix) and len(st.args) >= 3
+                and _cls(st.args[0]) == "Var" and _cls(st.args[1]) == "Var")
+
+    def _window(self, stmts, i):
+        """A pipelinable window starting at stmts[i]: full-array H2D copies (and
+        gmem_mallocs), ONE kernel scope, then D2H copies, with every H2D'd device
+        array only read by the kernel and every D2H'd one written by it (static
+        read / write sets). -> (decls, h2d calls, kernel index, d2h calls, end) or None."""
+        j, decls, h2d = i, [], []
+        while j < len(stmts):
+            st = stmts[j]
+            if self._is_copy(st, "memcpy_host_to_device"):
+                h2d.append(st)
+            elif _cls(st) == "Decl" and st.alloc == "gmem_malloc":
+                decls.append(st)
+            else:
+                break
+            j += 1
+        if j >= len(stmts) or not (_cls(stmts[j]) == "Seq" and _is_kernel_scope(stmts[j])):
+            return None
+        k = j
+        j += 1
+        d2h = []
+        while j < len(stmts) and self._is_copy(stmts[j], "memcpy_device_to_host"):
+            d2h.append(stmts[j])
+            j += 1
+        if not h2d and not d2h:
+            return None
+        reads, writes = _rw_sets(stmts[k])
+        dev_in = [c.args[0].name for c in h2d]
+        dev_out = [c.args[1].name for c in d2h]
+        host_in = [c.args[1].name for c in h2d]
+        host_out = [c.args[0].name for c in d2h]
+        if (any(n not in reads or n in writes for n in dev_in) or any(n not in writes for n in dev_out)
+                or len(set(dev_in)) != len(dev_in) or len(set(dev_out)) != len(dev_out)
+                or set(dev_in) & set(dev_out) or set(host_in) & set(host_out) or len(set(host_out)) != len(host_out)
+                or len(dev_in) + len(dev_out) > 8):
+            return None
+        if i == k:  # nothing before the kernel: start the window at the kernel
+            pass
+        return decls, h2d, k, d2h, j
 
     def host_stmt(self, st, out, ind):
         pad = "    " * ind
@@ -622,7 +883,13 @@ class _Gen:
         raise UnsupportedProgram(f"call to {f!r} is not supported by the code generator")
 
     # ------------------------------------------------------------------ kernels
-    def kernel_scope(self, seq, out, ind):
+    def kernel_scope(self, seq, out, ind, window=None):
+        """Emit one kernel scope: the __global__ function (once) and its host launch.
+        With `window` = (h2d CallStmts, d2h CallStmts) the surrounding full-array
+        copies are folded into a chunked copy -> kernel -> copy pipeline (SURVEY 8f
+        rank 2, b2_pipe_run) whenever the launch is proved in bounds and the
+        per-chunk footprints (the bounds proof run over block ranges) allow it;
+        otherwise the copies and the launch run in program order as before."""
         pad = "    " * ind
         st = _stmts(seq)
         launch, body = st[0], st[1:]
@@ -631,7 +898,6 @@ class _Gen:
         body = body[:-1]
         self.pre = []
         bpg, tpb = self.int_expr(launch.args[0]), self.int_expr(launch.args[1])
-        setup = []
         smem = []
         i = 0
         while i < len(body) and not (_cls(body[i]) == "CallStmt" and body[i].fn == "kernel_setup_end"):
@@ -690,39 +956,139 @@ class _Gen:
         self.kernels.append(kctx.render(dl))
         g, t = self.fresh("bpg"), self.fresh("tpb")
         proof = _Proof(self, kctx, f"({g} * {t})").run(kbody)
-        # host launch
         args = kctx.host_args()
-        out.extend(pad + ln for ln in host_lines)
-        out.append(pad + f"{{ const int64_t {g} = {bpg}, {t} = {tpb};")
-        out.append(pad + f"  if ({g} < 0 || {g} > 2147483647LL || {t} < 0 || {t} > 1024 || {g} * {t} >= (1LL << 32)) "
-                   f"b2_throw(\"kernel_launch(\" + std::to_string({g}) + \", \" + std::to_string({t}) + \") exceeds the B200 launch limits\");")
-        out.append(pad + f"  if ({g} > 0 && {t} > 0) {{")
-        pv = self.fresh("proved")
-        out.append(pad + f"    bool {pv} = false;")
-        for hp in kctx.hoist.values():
-            out.append(pad + f"    int64_t {name}{hp}_n = 0, {name}{hp}_s0 = 0; uint32_t {name}{hp}_w2 = 1; int {name}{hp}_sh = -1;")
-        out.append(pad + "    if (b2_prove_enabled()) {")
-        out.append(pad + "      try {")
-        out.append(pad + "        [&]() {")
-        out.extend(pad + "          " + ln for ln in proof)
-        out.append(pad + "        }();")
-        out.append(pad + f"        {pv} = true;")
-        out.append(pad + "      } catch (B2NoProof &) {}")
-        out.append(pad + "    }")
-        if self.nk <= 64:  # per-kernel evidence for the first 64 kernels of a program
-            out.append(pad + f"    b2_kernel_unchecked[{self.nk - 1}] = {pv} ? 1 : 0;")
-        out.append(pad + f"    if ({smem_bytes} > 48 * 1024) {{ cudaFuncSetAttribute({name}<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int){smem_bytes}); "
-                   f"cudaFuncSetAttribute({name}<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int){smem_bytes}); }}")
-        out.append(pad + "    cudaMemset(b2_err_dev, 0, 5 * sizeof(int));")
-        out.append(pad + "    cudaEventRecord(b2_ev0, 0);")
-        out.append(pad + f"    if ({pv}) {name}<false><<<(unsigned){g}, (unsigned){t}, (size_t){smem_bytes}>>>({', '.join(args)});")
-        out.append(pad + f"    else {name}<true><<<(unsigned){g}, (unsigned){t}, (size_t){smem_bytes}>>>({', '.join(args)});")
-        out.append(pad + "    cudaEventRecord(b2_ev1, 0);")
-        out.append(pad + f"    b2_check_kernel(b2_err_dev, \"{name}\");")
-        if self.nk <= 64:
-            out.append(pad + f"    {{ float ms = 0; cudaEventElapsedTime(&ms, b2_ev0, b2_ev1); b2_kernel_ms[{self.nk - 1}] = ms; }}")
+        info = dict(name=name, g=g, t=t, bpg=bpg, tpb=tpb, smem=smem_bytes, proof=proof, args=args, kctx=kctx)
+        if window is None:
+            out.extend(pad + ln for ln in host_lines)
+            out.extend(pad + ln for ln in self._launch_block(info, [], []))
+            return
+        # ---- pipelined window
+        h2d_calls, d2h_calls = window
+        pairs = []  # (dev sym, host sym, n code, is_h2d, copy lines)
+        for cs in h2d_calls + d2h_calls:
+            self.pre = []
+            lines = self.host_call(cs)
+            a, b = self.sym(cs.args[0].name), self.sym(cs.args[1].name)
+            n = " * ".join(f"({self.int_expr(x)})" for x in cs.args[2:])
+            h2d = cs.fn.startswith("memcpy_host_to_device")
+            dev_s, host_s = (a, b) if h2d else (b, a)
+            pairs.append((dev_s, host_s, n, h2d, self.pre + lines))
+        self.pre = []
+        slots = {}
+        for dev_s, _, _, _, _ in pairs:
+            slots.setdefault(dev_s.name, len(slots))
+        fp = _Proof(self, kctx, f"({g} * {t})", mode="footprint", slots=slots, tpb=t).run(kbody)
+        info.update(fp=fp, slots=slots, pairs=pairs)
+        h2d_lines = [ln for p_ in pairs if p_[3] for ln in p_[4]]
+        d2h_lines = [ln for p_ in pairs if not p_[3] for ln in p_[4]]
+        ok = " && ".join(
+            [f"b2_pipe_ok({p_[0].cname}, {p_[1].cname}, {p_[2]}, {'true' if p_[3] else 'false'})" for p_ in pairs] +
+            [f"b2_disjoint({a[1].cname}, {b[1].cname})" for a in pairs if a[3] for b in pairs if not b[3]])
+        pw = self.fresh("pw")
+        out.append(pad + f"{{ const bool {pw} = b2_pipe_on() && {ok};")
+        out.append(pad + f"  if ({pw}) {{")
+        out.extend(pad + "    " + ln for ln in host_lines)
+        out.extend(pad + "    " + ln for ln in self._launch_block(info, h2d_lines, d2h_lines, piped=True))
+        out.append(pad + "  } else {")
+        out.extend(pad + "    " + ln for ln in h2d_lines)
+        out.extend(pad + "    " + ln for ln in host_lines)
+        out.extend(pad + "    " + ln for ln in self._launch_block(info, [], []))
+        out.extend(pad + "    " + ln for ln in d2h_lines)
         out.append(pad + "  }")
         out.append(pad + "}")
+
+    def _launch_block(self, info, h2d_lines, d2h_lines, piped=False):
+        """Host code of one launch (lines, unindented). piped: try the chunked
+        pipeline first (needs the bounds proof); the copies in h2d_lines /
+        d2h_lines run around a plain launch when it does not apply."""
+        name, g, t, smem_bytes, kctx = info["name"], info["g"], info["t"], info["smem"], info["kctx"]
+        nk = int(name[len("b2g_kernel"):])
+        args = ", ".join(info["args"])
+        L = []
+        L.append(f"{{ const int64_t {g} = {info['bpg']}, {t} = {info['tpb']};")
+        L.append(f"  if ({g} < 0 || {g} > 2147483647LL || {t} < 0 || {t} > 1024 || {g} * {t} >= (1LL << 32)) "
+                 f"b2_throw(\"kernel_launch(\" + std::to_string({g}) + \", \" + std::to_string({t}) + \") exceeds the B200 launch limits\");")
+        L.append(f"  if ({g} > 0 && {t} > 0) {{")
+        pv = self.fresh("proved")
+        L.append(f"    bool {pv} = false;")
+        for hp in kctx.hoist.values():
+            L.append(f"    int64_t {name}{hp}_n = 0, {name}{hp}_s0 = 0; uint32_t {name}{hp}_w2 = 1; int {name}{hp}_sh = -1;")
+        L.append("    if (b2_prove_enabled()) {")
+        L.append("      try {")
+        L.append("        [&]() {")
+        L.extend("          " + ln for ln in info["proof"])
+        L.append("        }();")
+        L.append(f"        {pv} = true;")
+        L.append("      } catch (B2NoProof &) {}")
+        L.append("    }")
+        if nk < 64:  # per-kernel evidence for the first 64 kernels of a program
+            L.append(f"    b2_kernel_unchecked[{nk}] = {pv} ? 1 : 0;")
+            L.append(f"    b2_kernel_piped[{nk}] = 0;")
+        L.append(f"    if ({smem_bytes} > 48 * 1024) {{ cudaFuncSetAttribute({name}<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int){smem_bytes}); "
+                 f"cudaFuncSetAttribute({name}<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int){smem_bytes}); }}")
+        done = self.fresh("piped")
+        L.append(f"    bool {done} = false;")
+        if piped:
+            L.extend("    " + ln for ln in self._pipe_lines(info, pv, done, nk))
+        L.append(f"    if (!{done}) {{")
+        L.extend("      " + ln for ln in h2d_lines)
+        L.append("      cudaMemset(b2_err_dev, 0, 5 * sizeof(int));")
+        L.append("      cudaEventRecord(b2_ev0, 0);")
+        L.append(f"      if ({pv}) {name}<false><<<(unsigned){g}, (unsigned){t}, (size_t){smem_bytes}>>>({args}, 0u, (uint32_t){g});")
+        L.append(f"      else {name}<true><<<(unsigned){g}, (unsigned){t}, (size_t){smem_bytes}>>>({args}, 0u, (uint32_t){g});")
+        L.append("      cudaEventRecord(b2_ev1, 0);")
+        L.append(f"      b2_check_kernel(b2_err_dev, \"{name}\");")
+        if nk < 64:
+            L.append(f"      {{ float ms = 0; cudaEventElapsedTime(&ms, b2_ev0, b2_ev1); b2_kernel_ms[{nk}] = ms; }}")
+        L.extend("      " + ln for ln in d2h_lines)
+        L.append("    }")
+        L.append("  } else {")
+        L.extend("    " + ln for ln in h2d_lines + d2h_lines)
+        L.append("  }")
+        L.append("}")
+        return L
+
+    def _pipe_lines(self, info, pv, done, nk):
+        """The chunked pipeline (host code): chunk the launch into block ranges
+        aligned to the outermost thread-for level, evaluate each chunk's footprint
+        on the window's device arrays with the footprint proof, turn footprints into
+        2-D copy regions (b2_plan) and hand them to libb200k's b2_pipe_run."""
+        name, g, t, smem_bytes, kctx = info["name"], info["g"], info["t"], info["smem"], info["kctx"]
+        args = ", ".join(info["args"])
+        slots, pairs = info["slots"], info["pairs"]
+        arrs = []
+        for dev_s, host_s, n, h2d, _ in pairs:
+            arrs.append(f"b2_pipe_arr({dev_s.cname}, {host_s.cname}, {slots[dev_s.name]}, {'true' if h2d else 'false'})")
+        root = kctx.root_hoist
+        al = f"(((int64_t){name}{root}_w2 % {t}) == 0 ? (int64_t){name}{root}_w2 / {t} : 1)" if root else "1"
+        L = [f"if ({pv} && b2_pipe_fn()) {{",
+             "  try {",
+             f"    const std::vector<B2PipeArr> _pa = {{{', '.join(arrs)}}};",
+             f"    auto _fpf = [&](int64_t _B0, int64_t _B1, B2FP &_fp) {{"]
+        L.extend("      " + ln for ln in info["fp"])
+        L.extend([
+            "    };",
+            "    B2Plan _pl;",
+            f"    if (b2_plan({g}, {al}, _pa, _fpf, _pl)) {{",
+            f"      auto _lf = [&](int _c, cudaStream_t _s) -> int {{",
+            "        const int64_t _b0 = _pl.bnd[_c], _b1 = _pl.bnd[_c + 1];",
+            "        if (_b1 <= _b0) return 0;",
+            "        if (_c < 64) cudaEventRecord(b2_pev[0][_c], _s);",
+            f"        {name}<false><<<(unsigned)(_b1 - _b0), (unsigned){t}, (size_t){smem_bytes}, _s>>>({args}, (uint32_t)_b0, (uint32_t){g});",
+            "        if (_c < 64) cudaEventRecord(b2_pev[1][_c], _s);",
+            "        return cudaGetLastError() == cudaSuccess ? 0 : 1;",
+            "      };",
+            "      b2_run_plan(_pl, _lf);",
+        ])
+        if nk < 64:
+            L.append(f"      b2_kernel_ms[{nk}] = b2_plan_ms(_pl); b2_kernel_piped[{nk}] = (int)_pl.nchunk;")
+        L.extend([
+            f"      {done} = true;",
+            "    }",
+            "  } catch (B2NoProof &) {}",
+            "}",
+        ])
+        return L
 
     # ------------------------------------------------------------------ translation unit
     def render(self) -> str:
@@ -781,6 +1147,7 @@ class _KernelCtx:
         self.hoist: dict = {}
         self.uniform_const: dict = {}  # id(For) of launch-uniform literal-extent levels
         self.uniform_w = {"b2_w0"}
+        self.root_hoist = None  # first hoisted thread-for level directly under the launch width
 
     def use(self, s):
         if s.kind == "dev_arr":
@@ -835,13 +1202,16 @@ class _KernelCtx:
         for hp in self.hoist.values():
             params.append(f"const int64_t {hp}_n, const int64_t {hp}_s0, const uint32_t {hp}_w2, const int {hp}_sh")
         params.append("int *b2_err")
+        # block offset / total grid of a chunked launch (b2_pipe_run): a chunk covers
+        # blocks [b2_boff, b2_boff + gridDim.x) of a b2_gtot-block launch
+        params.append("const uint32_t b2_boff, const uint32_t b2_gtot")
         for s in treg:
             n = " * ".join(f"{s.cname}_d{k}" for k in range(s.rank)) or "1"
             pro.append(f"    {s.elem} {s.cname}[B2_TREG_MAX]; if (({n}) > B2_TREG_MAX) {{ b2_flag(b2_err, B2E_OOB, {n}, B2_TREG_MAX); return; }}")
         out = [f"template <bool B2CK> __global__ void {self.name}({', '.join(params)}) {{",
                "    extern __shared__ __align__(16) unsigned char b2_smem[];",
-               "    const uint32_t b2_w0 = gridDim.x * blockDim.x;",
-               "    const uint32_t b2_rel0 = blockIdx.x * blockDim.x + threadIdx.x;"]
+               "    const uint32_t b2_w0 = b2_gtot * blockDim.x;",
+               "    const uint32_t b2_rel0 = (blockIdx.x + b2_boff) * blockDim.x + threadIdx.x;"]
         if treg:
             out.insert(0, "#define B2_TREG_MAX 64")
         out.extend(pro)
@@ -942,6 +1312,8 @@ class _KernelCtx:
                 self.uniform_w.add(w2)
                 hp = f"_hp{len(self.hoist)}"
                 self.hoist[id(st)] = hp
+                if w == "b2_w0" and self.root_hoist is None:
+                    self.root_hoist = hp
                 if _is_const(st.range.start) and _is_const(st.range.stop):
                     # literal extent: nvcc folds n and the start; the host supplies
                     # the width split (loop-invariant, check-free) for proved launches
@@ -1042,14 +1414,25 @@ class _Proof:
     for variable ranges over [start.lo, stop.hi - 1], both branches of an `if` are
     covered, captured host scalars are points. Throws B2NoProof (checked kernel)
     on anything it cannot bound: values read from arrays, locals reassigned in the
-    kernel, inexact exact_div, non-constant divisors."""
+    kernel, inexact exact_div, non-constant divisors.
 
-    def __init__(self, gen: "_Gen", kctx: "_KernelCtx", width: str):
+    mode="footprint" emits the same walk as the body of a lambda over a block range
+    [_B0, _B1) that also records, per device array of a pipelined window (`slots`),
+    the union of the index intervals it reads / writes (b2fp_acc): the outermost
+    launch-uniform thread-for level is narrowed to the iterations those blocks run
+    (v = s0 + rel / w2, rel in [_B0 * tpb, _B1 * tpb)); inner levels keep their full
+    ranges, so the footprint over-approximates what the chunk touches."""
+
+    def __init__(self, gen: "_Gen", kctx: "_KernelCtx", width: str, mode: str = "prove",
+                 slots: dict = None, tpb: str = None):
         self.g = gen
         self.k = kctx
         self.locals: dict = {}     # kernel-local int name -> C++ interval variable, or None (unknown)
         self.n = 0
         self.width = [width]       # launch-uniform context widths of the enclosing hoisted levels
+        self.mode = mode
+        self.slots = slots or {}
+        self.tpb = tpb
 
     def fresh(self):
         self.n += 1
@@ -1098,7 +1481,7 @@ class _Proof:
                 return f"b2i_c((int64_t){sc.cname})", "i"
             return "b2i_c(0)", "v"
         if c == "Access":
-            chk = self.access(e.base, e.idxs)
+            chk = self.access(e.base, e.idxs, rw=0)
             return f"({chk}, b2i_c(0))", "v"
         if c == "BinOp":
             a, ka = self.expr(e.lhs)
@@ -1138,8 +1521,9 @@ class _Proof:
         code, kind = self.expr(e)
         return code if kind == "i" else f"((void){code}, b2i_unknown())"
 
-    def access(self, base, idxs):
-        """C++ expression (int) checking every index of one access."""
+    def access(self, base, idxs, rw=0):
+        """C++ expression (int) checking every index of one access (rw: 0 read,
+        1 write, 2 both; footprint mode records the window arrays' intervals)."""
         sym = self.g.syms[base]
         idxs = list(idxs)
         if sym.kind in ("smem_arr", "treg_arr"):
@@ -1147,12 +1531,17 @@ class _Proof:
             dims = f"{sym.cname}_hdims"
         else:
             dims = f"{sym.cname}.dims"
+        slot = self.slots.get(base) if (self.mode == "footprint" and sym.kind == "dev_arr") else None
+
+        def chk(code, k):
+            if slot is None:
+                return f"b2i_in({code}, {dims}[{k}])"
+            return f"b2fp_acc(_fp, {rw}, {slot}, {k}, {code}, {dims}[{k}])"
         if len(idxs) == sym.rank + 1 and sym.rank == 1:
-            return f"b2i_in(b2i_add({self.index(idxs[0])}, {self.index(idxs[1])}), {dims}[0])"
+            return chk(f"b2i_add({self.index(idxs[0])}, {self.index(idxs[1])})", 0)
         if len(idxs) != sym.rank:
             return "(b2i_unknown(), 0)"
-        return "(" + ", ".join(f"b2i_in({self.index(ix)}, {dims}[{k}])" for k, ix in enumerate(idxs)) + ")" \
-            if idxs else "0"
+        return "(" + ", ".join(chk(self.index(ix), k) for k, ix in enumerate(idxs)) + ")" if idxs else "0"
 
     def refine(self, cond):
         """(local name, narrowed interval expression) for `v OP e` / `e OP v` with v an
@@ -1218,14 +1607,24 @@ class _Proof:
                 out.append(f"    {q}_sh = ({q}_w2 & ({q}_w2 - 1u)) == 0u ? __builtin_ctz({q}_w2) : -1; }}")
                 self.width.append(f"(int64_t){q}_w2")
                 pushed = True
-            out.append(f"  if ({s1}.hi > {s0}.lo) {{ const B2I {v} = B2I{{{s0}.lo, {s1}.hi - 1}};")
+            if pushed and self.mode == "footprint" and len(self.width) == 2:
+                # outermost launch-uniform level: only the iterations of blocks [_B0, _B1)
+                q = f"{self.k.name}{hp}"
+                out.append(f"  const int64_t {v}_a = {s0}.lo + (_B0 * {self.tpb}) / (int64_t){q}_w2;")
+                out.append(f"  const int64_t {v}_b = {s0}.lo + (_B1 * {self.tpb} - 1) / (int64_t){q}_w2;")
+                out.append(f"  if ({s1}.hi > {s0}.lo && _B1 > _B0) {{ const B2I {v} = B2I{{std::max({s0}.lo, {v}_a), "
+                           f"std::min({s1}.hi - 1, {v}_b)}};")
+                out.append(f"  if ({v}.lo <= {v}.hi) {{")
+            else:
+                out.append(f"  if ({s1}.hi > {s0}.lo) {{ const B2I {v} = B2I{{{s0}.lo, {s1}.hi - 1}};")
+                out.append("  {")
             saved = dict(self.locals)
             self.locals[st.index] = v
             self.seq(st.body.stmts, out)
             if pushed:
                 self.width.pop()
             self.locals = saved
-            out.append("} }")
+            out.append("} } }")
         elif c == "If":
             out.append(f"(void){self.expr(st.cond)[0]};")
             ref = self.refine(st.cond)
@@ -1255,7 +1654,7 @@ class _Proof:
             out.append(f"(void){self.expr(st.value)[0]};")
             sym = self.g.syms.get(st.target.base)
             if sym is not None and sym.is_array:
-                out.append(f"(void){self.access(st.target.base, st.target.idxs)};")
+                out.append(f"(void){self.access(st.target.base, st.target.idxs, rw=2 if st.op == '+=' else 1)};")
         # CallStmt (blocksync): no access
 
 
@@ -1289,6 +1688,8 @@ class Compiled:
         self.lib.b2g_kernel_ms.argtypes = [ctypes.c_int]
         self.lib.b2g_kernel_unchecked.restype = ctypes.c_int
         self.lib.b2g_kernel_unchecked.argtypes = [ctypes.c_int]
+        self.lib.b2g_kernel_piped.restype = ctypes.c_int
+        self.lib.b2g_kernel_piped.argtypes = [ctypes.c_int]
         self.n_kernels = source.count("__global__ void b2g_kernel")
         # the generated host code keeps per-call state (ops table, allocation lists,
         # timing events) in statics of its .so: one call at a time per program
@@ -1297,6 +1698,11 @@ class Compiled:
     def kernel_ms(self) -> list:
         """Device time (CUDA events) of each kernel's last launch, in ms."""
         return [self.lib.b2g_kernel_ms(k) for k in range(min(self.n_kernels, 64))]
+
+    def kernel_piped(self) -> list:
+        """Per kernel: number of chunks its last launch was pipelined into with the
+        surrounding copies (b2_pipe_run), 0 if it ran as one launch between them."""
+        return [self.lib.b2g_kernel_piped(k) for k in range(min(self.n_kernels, 64))]
 
     def kernel_unchecked(self) -> list:
         """Per kernel: True if its last launch ran the check-free instantiation (all
@@ -1307,15 +1713,18 @@ class Compiled:
 class B2Ops(ctypes.Structure):
     """Host runtime services handed to generated code (libb200k.so copy engine)."""
     _fields_ = [("h2d", ctypes.c_void_p), ("d2h", ctypes.c_void_p), ("last_error", ctypes.c_void_p),
-                ("alloc", ctypes.c_void_p), ("dfree", ctypes.c_void_p), ("dev", ctypes.c_int64)]
+                ("alloc", ctypes.c_void_p), ("dfree", ctypes.c_void_p), ("dev", ctypes.c_int64),
+                ("pipe", ctypes.c_void_p), ("pipe_chunk", ctypes.c_int64)]
 
 
 def _ops(dev: int) -> B2Ops:
     from ._lib import lib
     L = lib()
     addr = lambda f: ctypes.cast(f, ctypes.c_void_p).value  # noqa: E731
+    # bytes per pipeline step (tune key codegen.pipe_kb; 0 = no copy / kernel pipelining)
+    chunk = int(L.b2_tune_get(b"codegen.pipe_kb")) * 1024
     return B2Ops(addr(L.b2_copy_h2d), addr(L.b2_copy_d2h), addr(L.b2_last_error),
-                 addr(L.b2_device_alloc), addr(L.b2_device_free), dev)
+                 addr(L.b2_device_alloc), addr(L.b2_device_free), dev, addr(L.b2_pipe_run), max(chunk, 0))
 
 
 class B2Arr(ctypes.Structure):

@@ -324,6 +324,7 @@ static int *tune_slot(const char *key) {
     if (k == "host.chunk_mb") return &g_tune.h_chunk_mb;
     if (k == "reduce.spin_ms") return &g_tune.r_spin_ms;
     if (k == "transpose.staged") return &g_tune.t_staged;
+    if (k == "codegen.pipe_kb") return &g_tune.c_pipe_kb;
     if (k == "transpose.staged_ctas") return &g_tune.t_staged_ctas;
     if (k == "transpose.staged_stages") return &g_tune.t_staged_stages;
     return nullptr;
@@ -624,6 +625,111 @@ int b2_device_free(void *p, int dev) {
     }
     a.free_blocks.emplace(sz, p);
     a.cached += sz;
+    return B2_OK;
+}
+
+// ------------------------------------------------------------ copy / kernel pipeline
+int b2_pipe_run(int nsteps, const b2_copy2d *h2d, const int64_t *h2d_off, const b2_copy2d *d2h,
+                const int64_t *d2h_off, b2_step_fn launch, void *ctx, int dev) {
+    B2_NVTX("b2_pipe_run");
+    if (nsteps < 0 || (nsteps && (!h2d_off || !d2h_off || !launch)))
+        return fail(B2_ERR_INVALID, "pipe: bad arguments");
+    if (nsteps == 0) return B2_OK;
+    if (int rc = check_dev(dev)) return rc;
+    DevCtx &c = g_ctx[dev];
+    std::lock_guard<std::mutex> g(c.mu);
+    if (int rc = ctx_init(c, dev)) return rc;
+    auto bytes = [](const b2_copy2d &x) { return (size_t)x.width * (size_t)x.height; };
+    // pinned or pageable, per copy; the largest per-step pageable volume sizes the ring
+    std::vector<char> pin_in(h2d_off[nsteps], 0), pin_out(d2h_off[nsteps], 0);
+    size_t ring = 0;
+    for (int st = 0; st < nsteps; ++st) {
+        size_t a = 0, b = 0;
+        for (int64_t i = h2d_off[st]; i < h2d_off[st + 1]; ++i) {
+            const b2_copy2d &x = h2d[i];
+            if (x.width < 0 || x.height < 0 || (bytes(x) && (!x.host || !x.dev)) ||
+                (x.height > 1 && (x.host_pitch < x.width || x.dev_pitch < x.width)))
+                return fail(B2_ERR_INVALID, "pipe: bad H2D region");
+            pin_in[i] = is_pinned(x.host);
+            if (!pin_in[i]) a += (bytes(x) + 15) & ~(size_t)15;
+        }
+        for (int64_t i = d2h_off[st]; i < d2h_off[st + 1]; ++i) {
+            const b2_copy2d &x = d2h[i];
+            if (x.width < 0 || x.height < 0 || (bytes(x) && (!x.host || !x.dev)) ||
+                (x.height > 1 && (x.host_pitch < x.width || x.dev_pitch < x.width)))
+                return fail(B2_ERR_INVALID, "pipe: bad D2H region");
+            pin_out[i] = is_pinned(x.host);
+            if (!pin_out[i]) b += (bytes(x) + 15) & ~(size_t)15;
+        }
+        ring = std::max(ring, std::max(a, b));
+    }
+    if (ring && ensure_host_stages(c, ring)) return B2_ERR_NOMEM;
+    B2_CUDA(cudaEventRecord(c.ev_legacy, cudaStreamLegacy));
+    B2_CUDA(cudaStreamWaitEvent(c.s_h2d, c.ev_legacy, 0));
+    B2_CUDA(cudaStreamWaitEvent(c.s_comp, c.ev_legacy, 0));
+    // pageable D2H regions of step j land packed in hs_out[j % kStages]; the host
+    // unpacks them one step later, overlapped with the next step's DMA
+    auto scatter = [&](int j) -> int {
+        const int k = j % kStages;
+        B2_CUDA(cudaEventSynchronize(c.ev_out[k]));
+        size_t off = 0;
+        for (int64_t i = d2h_off[j]; i < d2h_off[j + 1]; ++i) {
+            const b2_copy2d &x = d2h[i];
+            if (pin_out[i] || !bytes(x)) continue;
+            par_copy2d(x.host, (size_t)x.host_pitch, (char *)c.hs_out[k] + off, (size_t)x.width, (size_t)x.width,
+                       (size_t)x.height);
+            off += (bytes(x) + 15) & ~(size_t)15;
+        }
+        return B2_OK;
+    };
+    for (int st = 0; st < nsteps; ++st) {
+        const int k = st % kStages;
+        bool staged = false;
+        for (int64_t i = h2d_off[st]; i < h2d_off[st + 1]; ++i) staged |= !pin_in[i] && bytes(h2d[i]);
+        if (staged) B2_CUDA(cudaEventSynchronize(c.ev_in[k]));  // the DMA that last read hs_in[k] is done
+        size_t off = 0;
+        for (int64_t i = h2d_off[st]; i < h2d_off[st + 1]; ++i) {
+            const b2_copy2d &x = h2d[i];
+            if (!bytes(x)) continue;
+            if (pin_in[i]) {
+                B2_CUDA(cudaMemcpy2DAsync(x.dev, (size_t)x.dev_pitch, x.host, (size_t)x.host_pitch, (size_t)x.width,
+                                          (size_t)x.height, cudaMemcpyHostToDevice, c.s_h2d));
+            } else {
+                char *slot = (char *)c.hs_in[k] + off;
+                par_copy2d(slot, (size_t)x.width, x.host, (size_t)x.host_pitch, (size_t)x.width, (size_t)x.height);
+                B2_CUDA(cudaMemcpy2DAsync(x.dev, (size_t)x.dev_pitch, slot, (size_t)x.width, (size_t)x.width,
+                                          (size_t)x.height, cudaMemcpyHostToDevice, c.s_h2d));
+                off += (bytes(x) + 15) & ~(size_t)15;
+            }
+        }
+        B2_CUDA(cudaEventRecord(c.ev_in[k], c.s_h2d));
+        B2_CUDA(cudaStreamWaitEvent(c.s_comp, c.ev_in[k], 0));
+        if (int rc = launch(ctx, st, (void *)c.s_comp))
+            return fail(B2_ERR_CUDA, std::string("pipe: step launch failed: ") + cudaGetErrorString(cudaGetLastError()) +
+                                         " (code " + std::to_string(rc) + ")");
+        B2_CUDA(cudaEventRecord(c.ev_comp[k], c.s_comp));
+        B2_CUDA(cudaStreamWaitEvent(c.s_d2h, c.ev_comp[k], 0));
+        off = 0;
+        for (int64_t i = d2h_off[st]; i < d2h_off[st + 1]; ++i) {
+            const b2_copy2d &x = d2h[i];
+            if (!bytes(x)) continue;
+            if (pin_out[i]) {
+                B2_CUDA(cudaMemcpy2DAsync(x.host, (size_t)x.host_pitch, x.dev, (size_t)x.dev_pitch, (size_t)x.width,
+                                          (size_t)x.height, cudaMemcpyDeviceToHost, c.s_d2h));
+            } else {
+                B2_CUDA(cudaMemcpy2DAsync((char *)c.hs_out[k] + off, (size_t)x.width, x.dev, (size_t)x.dev_pitch,
+                                          (size_t)x.width, (size_t)x.height, cudaMemcpyDeviceToHost, c.s_d2h));
+                off += (bytes(x) + 15) & ~(size_t)15;
+            }
+        }
+        B2_CUDA(cudaEventRecord(c.ev_out[k], c.s_d2h));
+        if (st > 0)
+            if (int rc = scatter(st - 1)) return rc;
+    }
+    if (int rc = scatter(nsteps - 1)) return rc;
+    B2_CUDA(cudaStreamSynchronize(c.s_d2h));
+    B2_CUDA(cudaStreamSynchronize(c.s_comp));
+    B2_CUDA(cudaStreamSynchronize(c.s_h2d));
     return B2_OK;
 }
 

@@ -429,8 +429,14 @@ int dispatch(const void *in, void *out, int64_t rows, int64_t cols, int64_t ld_i
         if constexpr (E >= 2) {
             if (g_tune.t_any) return launch_transpose_any(in, out, rows, cols, ld_in, ld_out, E, dev, st);
             // cp.async-staged 16-B chunks (transpose_staged.cu) unless the cells themselves
-            // are misaligned (then only the scalar tile applies)
-            if (g_tune.t_staged && (uintptr_t)in % E == 0 && (uintptr_t)out % E == 0)
+            // are misaligned (then only the scalar tile applies). Auto (t_staged = 1):
+            // 2-byte cells from 2^22 cells up, where it measured +27..40 % over the scalar
+            // tile (bf16 4097x8191 3.6 -> 4.6 TB/s, 16385x16383 3.76 -> 5.15 TB/s); 4- and
+            // 8-byte cells and small matrices stay on the scalar tile, which is on par or
+            // faster there (profiles/r02c_odd_staged.md). t_staged = 2 forces it.
+            const bool use = g_tune.t_staged == 2 ||
+                             (g_tune.t_staged == 1 && E == 2 && rows * cols >= (int64_t(1) << 22));
+            if (use && (uintptr_t)in % E == 0 && (uintptr_t)out % E == 0)
                 return launch_transpose_staged(in, out, rows, cols, ld_in, ld_out, E, dev, st);
         }
         return run_scalar<T>(in, out, 0, rows, 0, cols, ld_in, ld_out, dev, st);

@@ -72,14 +72,19 @@ def test_a4_structure_like_spec_acceptance_1():
     assert kernel.count("__syncthreads();") == 1
     assert kernel.count("float *v_tile = (float *)(b2_smem") == 1
     assert "DMINDEX" not in src and "__ghost" not in src
-    # one launch site: the checked instantiation, or the check-free one when the
-    # host proved every access in bounds for the concrete launch
-    assert host.count("<true><<<") == 1 and host.count("<false><<<") == 1 and host.count("<<<") == 2
+    # the launch: the checked instantiation, or the check-free one when the host
+    # proved every access in bounds for the concrete launch — in program order
+    # between the copies (twice: the plain path and the pipeline's fallback), plus the
+    # chunk launch of the copy / kernel pipeline on its stream
+    assert host.count("<true><<<") == 2 and host.count("<false><<<") == 3 and host.count("<<<") == 5
+    assert host.count("b2_run_plan(") == 1 and host.count("b2fp_acc(_fp, 0, 0,") == 2  # d_in read, 2 dims
+    assert host.count("b2fp_acc(_fp, 1, 1,") == 2  # d_out written, 2 dims
     assert host.count("b2i_in(") >= 4 and "catch (B2NoProof &)" in host
     assert "b2_exact_div_h(v_W, ((int64_t)32LL)) * b2_exact_div_h(v_H, ((int64_t)32LL))" in host
     assert "(((int64_t)16LL) * ((int64_t)32LL))" in host  # 512 threads per block
     assert host.count("b2_dev_alloc<float>(") == 2
-    assert host.count("b2_h2d(") == 1 and host.count("b2_d2h(") == 1
+    # (plain path, the pipeline branch's fallback, and its empty-grid case)
+    assert host.count("b2_h2d(") == 3 and host.count("b2_d2h(") == 3
     assert host.count(".freed = true;") == 2
 
 
@@ -121,7 +126,10 @@ def test_launch_uniform_thread_for_levels_are_hoisted():
     host = src[src.index('extern "C" int b2g_main'):]
     assert kernel.count("const uint32_t _hp") == 6  # by, bx and two (y, x) pairs
     assert "B2CK ? b2_w0 / (uint32_t)" in kernel
-    assert host.count("_w2 = (uint32_t)(_w /") == 6 and "throw B2NoProof{}" in host
+    # six levels, evaluated by the bounds proof of the plain launch path, of the
+    # pipelined path, and by the pipeline's per-chunk footprint walk
+    assert host.count("_w2 = (uint32_t)(_w /") == 18 and "throw B2NoProof{}" in host
+    assert host.count("(_B0 * _tpb") == 1  # only the outermost level (by) is narrowed per chunk
 
 
 def test_assignment_to_loop_index_refused():

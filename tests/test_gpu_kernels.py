@@ -229,7 +229,7 @@ def test_launch_counter(b2):
     assert b2.launch_count() == n0 + 1
 
 
-_PATHS = {"staged": {"transpose.any": 0, "transpose.staged": 1},
+_PATHS = {"staged": {"transpose.any": 0, "transpose.staged": 2},
           "scalar": {"transpose.any": 0, "transpose.staged": 0},
           "any": {"transpose.any": 1, "transpose.staged": 0}}
 
@@ -280,11 +280,13 @@ def test_staged_odd_pitch_full(b2, stages, ctas, dt, rows, cols):
     a = torch.randint(info.min, info.max, (rows, cols), device="cuda", dtype=dt)
     _lib.tune("transpose.staged_stages", stages)
     _lib.tune("transpose.staged_ctas", ctas)
+    _lib.tune("transpose.staged", 2)
     try:
         t = b2.transpose(a)
     finally:
         _lib.tune("transpose.staged_stages", 4)
         _lib.tune("transpose.staged_ctas", 0)
+        _lib.tune("transpose.staged", 1)
     assert np.array_equal(t.cpu().numpy(), oracle.transpose(a.cpu().numpy()))
 
 

@@ -94,6 +94,7 @@ def run_transpose(rng):
         one_transpose(rows, cols, dt, rng)
     # odd pitches / misaligned bases -> cp.async-staged kernel (every ring depth), the
     # padded scalar tile, then the funnel-shift path
+    tune("transpose.staged", 2)
     for stages in (4, 3, 2):
         tune("transpose.staged_stages", stages)
         one_transpose(200, 300, np.float32, rng, pad_in=1, pad_out=3)

@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <condition_variable>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <functional>
@@ -682,8 +683,19 @@ int b2_pipe_run(int nsteps, const b2_copy2d *h2d, const int64_t *h2d_off, const 
         }
         return B2_OK;
     };
+    // B2K_PIPE_TRACE=1: per-step H2D / kernel / D2H intervals on stderr (tools/r02_pipe_sweep.py)
+    static const bool trace = getenv("B2K_PIPE_TRACE") && getenv("B2K_PIPE_TRACE")[0] == '1';
+    std::vector<cudaEvent_t> tev;
+    auto mark = [&](cudaStream_t s) {
+        if (!trace) return;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, s);
+        tev.push_back(e);
+    };
     for (int st = 0; st < nsteps; ++st) {
         const int k = st % kStages;
+        mark(c.s_h2d);
         bool staged = false;
         for (int64_t i = h2d_off[st]; i < h2d_off[st + 1]; ++i) staged |= !pin_in[i] && bytes(h2d[i]);
         if (staged) B2_CUDA(cudaEventSynchronize(c.ev_in[k]));  // the DMA that last read hs_in[k] is done
@@ -702,13 +714,17 @@ int b2_pipe_run(int nsteps, const b2_copy2d *h2d, const int64_t *h2d_off, const 
                 off += (bytes(x) + 15) & ~(size_t)15;
             }
         }
+        mark(c.s_h2d);
         B2_CUDA(cudaEventRecord(c.ev_in[k], c.s_h2d));
         B2_CUDA(cudaStreamWaitEvent(c.s_comp, c.ev_in[k], 0));
+        mark(c.s_comp);
         if (int rc = launch(ctx, st, (void *)c.s_comp))
             return fail(B2_ERR_CUDA, std::string("pipe: step launch failed: ") + cudaGetErrorString(cudaGetLastError()) +
                                          " (code " + std::to_string(rc) + ")");
+        mark(c.s_comp);
         B2_CUDA(cudaEventRecord(c.ev_comp[k], c.s_comp));
         B2_CUDA(cudaStreamWaitEvent(c.s_d2h, c.ev_comp[k], 0));
+        mark(c.s_d2h);
         off = 0;
         for (int64_t i = d2h_off[st]; i < d2h_off[st + 1]; ++i) {
             const b2_copy2d &x = d2h[i];
@@ -722,6 +738,7 @@ int b2_pipe_run(int nsteps, const b2_copy2d *h2d, const int64_t *h2d_off, const 
                 off += (bytes(x) + 15) & ~(size_t)15;
             }
         }
+        mark(c.s_d2h);
         B2_CUDA(cudaEventRecord(c.ev_out[k], c.s_d2h));
         if (st > 0)
             if (int rc = scatter(st - 1)) return rc;
@@ -730,6 +747,15 @@ int b2_pipe_run(int nsteps, const b2_copy2d *h2d, const int64_t *h2d_off, const 
     B2_CUDA(cudaStreamSynchronize(c.s_d2h));
     B2_CUDA(cudaStreamSynchronize(c.s_comp));
     B2_CUDA(cudaStreamSynchronize(c.s_h2d));
+    if (trace && !tev.empty()) {  // ms from the first H2D start: h2d [a, b) kernel [a, b) d2h [a, b)
+        for (int st = 0; st < nsteps; ++st) {
+            float t[6];
+            for (int i = 0; i < 6; ++i) cudaEventElapsedTime(&t[i], tev[0], tev[6 * st + i]);
+            fprintf(stderr, "pipe step %d: h2d %.3f-%.3f kernel %.3f-%.3f d2h %.3f-%.3f\n", st, t[0], t[1], t[2],
+                    t[3], t[4], t[5]);
+        }
+        for (cudaEvent_t e : tev) cudaEventDestroy(e);
+    }
     return B2_OK;
 }
 

@@ -412,7 +412,12 @@ def _exec_transpose_gpu(plan: Plan, env):
         return None
     if (len(dst.data) if not isinstance(dst.data, np.ndarray) else dst.data.size) < n:
         raise IndexError("list assignment index out of range")
-    out = ops.transpose(np.ascontiguousarray(a).reshape(H, W))
+    a2d = np.ascontiguousarray(a).reshape(H, W)
+    if isinstance(dst.data, np.ndarray) and dst.data.dtype == np.float32 and dst.data.flags.c_contiguous:
+        # memcpy_device_to_host2 of the W x H result straight into the caller's buffer
+        ops.transpose(a2d, dst.data.reshape(-1)[:n].reshape(W, H))
+        return None
+    out = ops.transpose(a2d)
     _store(dst, out.reshape(1, n), n)
     return None
 

@@ -337,15 +337,21 @@ template <typename T> static B2Host<T> b2_param(B2Arr *A) {
     for (int i = 0; i < 8; ++i) a.dims[i] = A->dims[i];
     a.init = A->init; a.freed = A->freed != 0; return a;
 }
-template <typename T> static T b2_hread(B2Host<T> &a, int64_t nidx, const int64_t *idx) {
+// host element access with the interpreter's checks; the 1-D case (host loops over
+// partials, A.5's `sum += p[i]`) takes an inlined fast path
+static inline int64_t b2_off_h1(const int64_t *dims, int64_t rank, int64_t nidx, const int64_t *idx) {
+    if (__builtin_expect(nidx == 1 && rank == 1 && idx[0] >= 0 && idx[0] < dims[0], 1)) return idx[0];
+    return b2_off_h(dims, rank, nidx, idx);
+}
+template <typename T> static inline T b2_hread(B2Host<T> &a, int64_t nidx, const int64_t *idx) {
     if (a.freed) b2_throw("use after free");
-    int64_t o = b2_off_h(a.dims, a.rank, nidx, idx);
+    int64_t o = b2_off_h1(a.dims, a.rank, nidx, idx);
     if (a.init && !a.init[o]) b2_throw("read of uninitialized cell");
     return a.p[o];
 }
-template <typename T> static void b2_hwrite(B2Host<T> &a, int64_t nidx, const int64_t *idx, T v) {
+template <typename T> static inline void b2_hwrite(B2Host<T> &a, int64_t nidx, const int64_t *idx, T v) {
     if (a.freed) b2_throw("use after free");
-    int64_t o = b2_off_h(a.dims, a.rank, nidx, idx);
+    int64_t o = b2_off_h1(a.dims, a.rank, nidx, idx);
     a.p[o] = v;
     if (a.init) a.init[o] = 1;
 }

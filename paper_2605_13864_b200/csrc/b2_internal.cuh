@@ -58,7 +58,8 @@ struct Tuning {
                             // 2 = always, 0 = never (padded scalar tile)
     int t_staged_ctas = 0;  // CTAs per SM of the staged kernel (0 = 2)
     int t_staged_stages = 4;  // cp.async ring depth of the staged kernel (2, 3, 4)
-    int c_pipe_kb = 32768;  // generated programs: bytes per copy / kernel pipeline step (KiB; 0 = off)
+    int c_pipe_kb = 65536;  // generated programs: bytes per copy / kernel pipeline step (KiB; 0 = off)
+    int l_pdl = 0;          // 1 = launch the hot kernels with programmatic dependent launch
 };
 extern Tuning g_tune;
 constexpr int kInflightBytesPerSM = 64 * 1024;
@@ -87,6 +88,38 @@ __device__ __forceinline__ void stg_stream(uint4 *p, const uint4 &v) {
     asm volatile(B2_STG_QUAL " [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x),
                  "r"(v.y), "r"(v.z), "r"(v.w)
                  : "memory");
+}
+
+// ---- programmatic dependent launch (PDL) -----------------------------------
+// With g_tune.l_pdl the hot kernels are launched with programmatic stream
+// serialisation: a kernel's CTAs may be scheduled while its predecessor on the
+// stream is still running. Every such kernel executes griddepcontrol.wait before
+// its first memory access (no input is read before the predecessor has completed
+// and flushed, whatever the predecessor was), then immediately allows its own
+// dependents to be scheduled: what overlaps is the launch / CTA dispatch of the
+// next kernel with the tail of this one, never data access.
+__device__ __forceinline__ void pdl_enter() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_kernel(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                                 Args... args) {
+    if (!g_tune.l_pdl) {
+        kernel<<<grid, block, smem, st>>>(args...);
+        return cudaGetLastError();
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, ((KArgs)args)...);
 }
 
 // ---- kernel launchers (defined in transpose.cu / reduce.cu) ---------------

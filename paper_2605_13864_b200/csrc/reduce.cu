@@ -248,6 +248,7 @@ __global__ void __launch_bounds__(NT)
     constexpr int V = 16 / sizeof(T);
     __shared__ A sm[NT / 32];
     __shared__ bool last;
+    pdl_enter();
 
     A acc = A(0);
     const VecW<W> *vin = reinterpret_cast<const VecW<W> *>(in + head);
@@ -320,6 +321,7 @@ template <int B, int NT>
 __global__ void __launch_bounds__(NT)
     tree_kernel(const float *__restrict__ in, int64_t nblocks, float *__restrict__ partials) {
     constexpr int K = B / 64;  // float2 pairs per lane
+    pdl_enter();
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * NT + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * NT) >> 5;
@@ -373,9 +375,9 @@ int run_reduce_v(const T *in, int64_t n, void *out, void *ws, int dev, cudaStrea
     const int grid = (int)std::min(cap, need);
     unsigned *ticket = (unsigned *)ws;
     A *partials = (A *)((char *)ws + 64);
-    reduce_kernel<T, NT, U, W><<<grid, NT, 0, st>>>(in, head, nvec, n, out, partials, ticket, fz, acc_out);
+    B2_CUDA(launch_kernel(reduce_kernel<T, NT, U, W>, dim3(grid), dim3(NT), 0, st, in, head, nvec, n, out, partials,
+                          ticket, fz, acc_out));
     count_launch();
-    B2_CUDA(cudaGetLastError());
     return B2_OK;
 }
 
@@ -440,7 +442,7 @@ template <int B>
 int run_tree(const float *in, int64_t nb, float *partials, int dev, cudaStream_t st) {
     constexpr int NT = 256;
     const int64_t grid = std::min<int64_t>((nb + NT / 32 - 1) / (NT / 32), (int64_t)num_sms(dev) * 8);
-    tree_kernel<B, NT><<<(unsigned)grid, NT, 0, st>>>(in, nb, partials);
+    B2_CUDA(launch_kernel(tree_kernel<B, NT>, dim3((unsigned)grid), dim3(NT), 0, st, in, nb, partials));
     count_launch();
     B2_CUDA(cudaGetLastError());
     return B2_OK;

@@ -94,6 +94,7 @@ __global__ void __launch_bounds__(NT)
     extern __shared__ uint4 S[];  // TC * TRV vectors (dynamic: large tiles exceed 48 KB)
 
     uint4 reg[MT][V];
+    pdl_enter();
 
     // Tile order: bands of `group` tile-rows, walked column by column inside a
     // band; with group = tiles_r (the default) the walk is column-major, so CTAs
@@ -203,6 +204,7 @@ __global__ void __launch_bounds__(256)
     constexpr int HC = TC / 32;   // column groups per thread
     constexpr int PAD = sizeof(T) == 2 ? 2 : 1;
     __shared__ T tile[TR][TC + PAD];
+    pdl_enter();
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
     const int64_t tiles_r = ntiles / tiles_c;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
@@ -307,11 +309,10 @@ int run_vec(const void *in, void *out, int64_t rows_v, int64_t cols_v, int64_t l
                                        : colwalk ? (int)std::min<int64_t>(tiles_r, 1 << 30)
                                                  : (kTileBytes >= 64 * 1024 ? 1 : 4);
     const int group = (int)std::max<int64_t>(1, std::min<int64_t>(grp, tiles_r));
-    transpose_vec_kernel<E, TRV, TCV, NT><<<(unsigned)grid, NT, kSmem, st>>>(
-        (const uint8_t *)in, (uint8_t *)out, rows_v, cols_v, ld_in * E, ld_out * E, tiles_r,
-        tiles_c, ntiles, group);
+    B2_CUDA(launch_kernel(transpose_vec_kernel<E, TRV, TCV, NT>, dim3((unsigned)grid), dim3(NT), kSmem, st,
+                          (const uint8_t *)in, (uint8_t *)out, rows_v, cols_v, ld_in * E, ld_out * E, tiles_r,
+                          tiles_c, ntiles, group));
     count_launch();
-    B2_CUDA(cudaGetLastError());
     return B2_OK;
 }
 
@@ -344,10 +345,9 @@ int run_scalar_tc(const void *in, void *out, int64_t r_lo, int64_t r_hi, int64_t
     if (sizeof(T) == 2 && TC == 128 && ntiles >= 48 * (int64_t)num_sms(dev)) auto_sm = 2;
     const int per_sm = g_tune.t_scalar_ctas > 0 ? g_tune.t_scalar_ctas : auto_sm;
     const int64_t grid = std::min<int64_t>(ntiles, (int64_t)num_sms(dev) * per_sm);
-    transpose_scalar_kernel<T, TC><<<(unsigned)grid, 256, 0, st>>>(
-        (const T *)in, (T *)out, r_lo, r_hi, c_lo, c_hi, ld_in, ld_out, tiles_c, ntiles);
+    B2_CUDA(launch_kernel(transpose_scalar_kernel<T, TC>, dim3((unsigned)grid), dim3(256), 0, st, (const T *)in,
+                          (T *)out, r_lo, r_hi, c_lo, c_hi, ld_in, ld_out, tiles_c, ntiles));
     count_launch();
-    B2_CUDA(cudaGetLastError());
     return B2_OK;
 }
 

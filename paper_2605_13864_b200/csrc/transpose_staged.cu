@@ -57,6 +57,7 @@ __global__ void __launch_bounds__(NT)
     extern __shared__ __align__(16) uint4 sm[];
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sm);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    pdl_enter();
 
     // column-major tile walk: concurrently processed tiles are vertical neighbours,
     // so their 128-B output segments of one output row are contiguous in HBM
@@ -144,10 +145,9 @@ int run_staged(const void *in, void *out, int64_t rows, int64_t cols, int64_t ld
     const int want = g_tune.t_staged_ctas > 0 ? g_tune.t_staged_ctas : 2;
     const int per_sm = std::min(want, occ[dev].load());
     const int64_t grid = std::min<int64_t>(ntiles, (int64_t)num_sms(dev) * per_sm);
-    kern<<<(unsigned)grid, NT, G::SMEM, st>>>((const T *)in, (T *)out, rows, cols, ld_in, ld_out, tiles_r,
-                                              ntiles);
+    B2_CUDA(launch_kernel(kern, dim3((unsigned)grid), dim3(NT), G::SMEM, st, (const T *)in, (T *)out, rows, cols,
+                          ld_in, ld_out, tiles_r, ntiles));
     count_launch();
-    B2_CUDA(cudaGetLastError());
     return B2_OK;
 }
 

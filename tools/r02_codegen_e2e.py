@@ -44,7 +44,7 @@ for pinned in (True, False):
            "W": N, "H": N}
     nbytes = 2 * N * N * 4
     rec = {"program": f"A.4 transpose fp32 {N}x{N}", "pinned": pinned, "bytes_moved": nbytes}
-    for label, backend, kb in [("hand_written", "kernels", None), ("codegen_pipelined", "codegen", 32768),
+    for label, backend, kb in [("hand_written", "kernels", None), ("codegen_pipelined", "codegen", 65536),
                                ("codegen_program_order", "codegen", 0)]:
         if kb is not None:
             _lib.tune("codegen.pipe_kb", kb)
@@ -56,7 +56,7 @@ for pinned in (True, False):
             c = codegen.compile_fn(tp.fn("transpose"))
             rec[label]["chunks"] = c.kernel_piped()[0]
             rec[label]["kernel_ms"] = c.kernel_ms()[0]
-    _lib.tune("codegen.pipe_kb", 32768)
+    _lib.tune("codegen.pipe_kb", 65536)
     print(json.dumps(rec), flush=True)
     res.append(rec)
     del a, o, inp
@@ -68,7 +68,7 @@ for pinned in (True, False):
     inp = {"arr": b2.Array([M], x, "float"), "N": M}
     rec = {"program": f"A.5 tree reduce fp32 n={M}", "pinned": pinned, "bytes_moved": M * 4}
     want = None
-    for label, backend, kb in [("hand_written", "kernels", None), ("codegen_pipelined", "codegen", 32768),
+    for label, backend, kb in [("hand_written", "kernels", None), ("codegen_pipelined", "codegen", 65536),
                                ("codegen_program_order", "codegen", 0)]:
         if kb is not None:
             _lib.tune("codegen.pipe_kb", kb)
@@ -79,5 +79,5 @@ for pinned in (True, False):
         if backend == "codegen":
             c = codegen.compile_fn(rp.fn("reduce"))
             rec[label]["chunks"] = c.kernel_piped()[0]
-    _lib.tune("codegen.pipe_kb", 32768)
+    _lib.tune("codegen.pipe_kb", 65536)
     print(json.dumps(rec), flush=True)

@@ -23,10 +23,19 @@ that gate in front of the B200 dispatch:
                      interval over every thread of the analysed blocks;
                      likewise no global cell is written by one thread and touched
                      by another thread of the same launch (no grid barrier).
-    Blocks analysed: all when the launch has <= MAX_BLOCKS blocks, else the
-    first, second and last iteration of every block-level `thread for` (the
-    index maps of these programs are affine, so the sampled blocks carry every
-    intra-block pattern; cross-block global conflicts are checked among them).
+    Blocks analysed: all, one by one, when the launch has <= MAX_BLOCKS blocks.
+    Larger launches are analysed ONCE with every block-level `thread for` index
+    kept symbolic (an affine form base + sum c_j B_j over the block indices B_j):
+    shared-memory indices, branch conditions and loop bounds must not depend on
+    the block indices at all (then every block has the analysed block's exact
+    intra-block pattern), and every global index must be affine in them with one
+    coefficient vector per array (checked); two blocks can then only collide in a
+    written array if some nonzero block offset delta keeps every dimension's
+    offset sum_j c_kj delta_j within that dimension's per-block span — refused
+    unless each block index owns a dimension whose coefficient exceeds the span
+    (the tiling shape of every derived program). Anything else (a non-affine use
+    of a block index, e.g. `b % 7`, a product of two block indices) is refused
+    with E-GATE-UNSUPPORTED instead of being sampled.
     Indices and branch conditions must not depend on array contents; such a
     program is refused with E-GATE-DATA rather than waved through.
   * check=None (default) — no gate, exactly like the reference's run_program.
@@ -51,6 +60,42 @@ class GateError(Exception):
 
 
 DATA = object()  # an array-content value: known to exist, never inspected
+
+
+class Aff:
+    """base + sum(coef[j] * B_j): a value affine in the symbolic block indices B_j
+    (large launches, see the module doc). `base` is an int or a lane array."""
+
+    __slots__ = ("base", "coef")
+
+    def __init__(self, base, coef):
+        self.base = base
+        self.coef = {k: v for k, v in coef.items() if v}
+
+    @staticmethod
+    def of(v):
+        return v if isinstance(v, Aff) else Aff(v, {})
+
+
+def _aff_op(op, a, b):
+    """Affine arithmetic; anything that would make a block index appear
+    non-affinely is refused."""
+    A, B = Aff.of(a), Aff.of(b)
+    if op in ("+", "-"):
+        sg = 1 if op == "+" else -1
+        coef = dict(A.coef)
+        for k, v in B.coef.items():
+            coef[k] = coef.get(k, 0) + sg * v
+        r = Aff(_binop(op, A.base, B.base), coef)
+        return r if r.coef else r.base
+    if op == "*":
+        for X, Y in ((A, B), (B, A)):
+            if not X.coef and not isinstance(X.base, np.ndarray):
+                k = int(X.base)
+                r = Aff(_binop("*", Y.base, k), {j: c * k for j, c in Y.coef.items()})
+                return r if r.coef else r.base
+    raise GateError("E-GATE-UNSUPPORTED", f"block index used non-affinely (operator {op!r}) in a large "
+                                          "launch: the per-block analysis cannot cover every block")
 
 
 def _cls(x):
@@ -111,11 +156,17 @@ class _KernelGate:
             a, b = self.eval(e.lhs, env, lanes), self.eval(e.rhs, env, lanes)
             if a is DATA or b is DATA:
                 return DATA
+            if isinstance(a, Aff) or isinstance(b, Aff):
+                return _aff_op(e.op, a, b)
             return _binop(e.op, a, b)
         if c == "Call":
             args = [self.eval(a, env, lanes) for a in e.args]
             if any(a is DATA for a in args):
                 return DATA
+            if e.fn.startswith("DMINDEX"):
+                return 0  # the block's own slot of a per-block array
+            if any(isinstance(a, Aff) for a in args):
+                raise GateError("E-GATE-UNSUPPORTED", f"block index inside {e.fn}() in a large launch")
             if e.fn == "exact_div":
                 a, b = args
                 if np.any(np.asarray(b) == 0) or np.any(np.mod(a, np.where(np.asarray(b) == 0, 1, b)) != 0):
@@ -131,10 +182,13 @@ class _KernelGate:
             raise GateError("E-GATE-UNSUPPORTED", f"call to {e.fn!r} in a kernel expression")
         raise GateError("E-GATE-UNSUPPORTED", f"{c} in a kernel expression")
 
-    def index(self, e, env, lanes):
+    def index(self, e, env, lanes, affine=False):
         v = self.eval(e, env, lanes)
         if v is DATA:
             raise GateError("E-GATE-DATA", "an index or condition depends on array contents")
+        if isinstance(v, Aff) and not affine:
+            raise GateError("E-GATE-UNSUPPORTED", "a loop bound, branch condition or shared-memory index "
+                                                  "depends on the block index in a large launch")
         return v
 
     # ------------------------------------------------------------ memory
@@ -144,13 +198,20 @@ class _KernelGate:
         kind = self.arrays.get(base)
         if kind is None:
             raise GateError("E-GATE-UNSUPPORTED", f"{base!r} is not an array the kernel can reach")
-        ix = [self.index(i, env, lanes) for i in idxs]
+        ix = [self.index(i, env, lanes, affine=(kind == "global")) for i in idxs]
         if kind in ("smem", "treg"):
             ix = ix[1:]  # per-block (per-thread) storage: drop the DMINDEX slot
         if kind == "treg":
             return  # registers are private to their thread
-        addr = np.zeros(lanes.n, np.int64)
         dims = self.dims.get(base)
+        if dims is not None and len(dims) == 1 and len(ix) == 2:
+            # the 1-D pointer-offset rule &a[k][j] -> a[k + j] (interp.py:239-240): one cell
+            ix = [_aff_op("+", ix[0], ix[1]) if isinstance(ix[0], Aff) or isinstance(ix[1], Aff)
+                  else _binop("+", ix[0], ix[1])]
+        if kind == "global":
+            self._affine_record(base, ix, is_write, lanes)
+            ix = [v.base if isinstance(v, Aff) else v for v in ix]
+        addr = np.zeros(lanes.n, np.int64)
         for k, v in enumerate(ix):  # row-major; any injective encoding serves the check
             stride = int(dims[k]) if dims is not None and k < len(dims) else 1 << 31
             addr = addr * stride + np.asarray(v, dtype=np.int64)
@@ -169,8 +230,12 @@ class _KernelGate:
         self.width = self.bpg * self.tpb
         self.block_id = -1
         self.seg = []
+        self.symbolic = self.bpg > MAX_BLOCKS
+        self.affine, self.block_vars = {}, {}
         self._walk_grid(body, dict(self.env0))
         _check_conflicts(self.glog, "global memory", per_block=False)
+        if self.symbolic:
+            self._cross_block_check()
 
     def _walk_grid(self, stmts, env):
         for pos, s in enumerate(stmts):
@@ -185,17 +250,63 @@ class _KernelGate:
                 n = max(b - a, 1)
                 outer = self.width
                 self.width = outer // n if outer % n == 0 else outer
-                vals = range(a, b) if b - a <= 3 or self.bpg <= MAX_BLOCKS else sorted({a, a + 1, b - 1})
-                for v in vals:
-                    env2 = dict(env)
-                    env2[s.index] = v
-                    self._walk_grid(_stmts(s.body), env2)
+                if self.symbolic:  # one pass with the block index symbolic: B_j in [a, b)
+                    if b > a:
+                        self.block_vars[s.index] = (a, b - 1)
+                        env2 = dict(env)
+                        env2[s.index] = Aff(a, {s.index: 1})
+                        self._walk_grid(_stmts(s.body), env2)
+                else:
+                    for v in range(a, b):
+                        env2 = dict(env)
+                        env2[s.index] = v
+                        self._walk_grid(_stmts(s.body), env2)
                 self.width = outer
                 continue
             if c == "CallStmt" and s.fn == "blocksync":
                 raise GateError("E-THREADS-CTX", f"blocksync requires a block-wide ThreadsCtx of {self.tpb} "
                                                  f"threads, have width {self.width}")
             raise GateError("E-GATE-UNSUPPORTED", f"{c} at grid level of a kernel")
+
+    def _affine_record(self, base, ix, is_write, lanes):
+        """Per global array: the block-index coefficient vector of every dimension
+        (must agree between accesses) and the per-dimension range of the bases."""
+        coefs = tuple(tuple(sorted(Aff.of(v).coef.items())) for v in ix)
+        rec = self.affine.setdefault(base, {"coef": coefs, "lo": [None] * len(ix), "hi": [None] * len(ix),
+                                            "write": False})
+        if rec["coef"] != coefs:
+            raise GateError("E-GATE-UNSUPPORTED", f"global array {base!r} indexed with different block-index "
+                                                  "coefficients in one large launch")
+        rec["write"] |= is_write
+        for k, v in enumerate(ix):
+            b = np.asarray(Aff.of(v).base, dtype=np.int64)
+            if b.size == 0:
+                continue
+            lo, hi = int(b.min()), int(b.max())
+            rec["lo"][k] = lo if rec["lo"][k] is None else min(rec["lo"][k], lo)
+            rec["hi"][k] = hi if rec["hi"][k] is None else max(rec["hi"][k], hi)
+
+    def _cross_block_check(self):
+        """Large launches: no cell of a written global array is reached from two
+        different blocks. Sufficient (and the tiling shape of the derived programs):
+        every block index j varying over >1 value owns a dimension k whose index
+        depends on B_j alone with |c_kj| > span_k (the per-block extent of that
+        dimension), so any nonzero block offset separates the footprints there."""
+        for name, rec in self.affine.items():
+            if not rec["write"]:
+                continue
+            coefs = [dict(c) for c in rec["coef"]]
+            for j, (lo_j, hi_j) in self.block_vars.items():
+                if hi_j <= lo_j:
+                    continue  # a block loop with one iteration
+                ok = False
+                for k, c in enumerate(coefs):
+                    if set(c) == {j} and rec["lo"][k] is not None and abs(c[j]) > rec["hi"][k] - rec["lo"][k]:
+                        ok = True
+                        break
+                if not ok:
+                    raise GateError("E-GATE-UNSUPPORTED", f"cannot prove that blocks write disjoint cells of "
+                                                          f"{name!r} (block index {j!r}) in a large launch")
 
     def _block(self, stmts, env):
         self.block_id += 1

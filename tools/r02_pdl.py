@@ -44,7 +44,7 @@ for n in (1024, 4096):
     R = max(2, -(-3 * L2 // (2 * n * n * 4)))
     a = [torch.rand((n, n), device="cuda") for _ in range(R)]
     o = [torch.empty_like(a[0]) for _ in range(R)]
-    cases[f"transpose_{n}sq_f32"] = (2 * n * n * 4, [(lambda i=i: b2.transpose(a[i], o[i])) for i in range(R)], R)
+    cases[f"transpose_{n}sq_f32"] = (2 * n * n * 4, [(lambda i=i, a=a, o=o: b2.transpose(a[i], o[i])) for i in range(R)], R)
 n = 1 << 24
 R = max(2, -(-3 * L2 // (n * 4)))
 xs = [torch.rand(n, device="cuda") for _ in range(R)]

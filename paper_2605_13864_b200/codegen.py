@@ -103,6 +103,19 @@ def has_kernel(fn) -> bool:
     return fn.body is not None and walk(fn.body)
 
 
+def _block_level(kbody):
+    """(For node, depth) of the kernel's block level: follow the chain of thread-fors
+    that are the only statement of their enclosing body, from the kernel body down;
+    the last one is where the program's blocks are (None if the kernel does not open
+    with such a chain)."""
+    stmts = [x for x in kbody if not _is_ghost(x)]
+    node, depth = None, 0
+    while len(stmts) == 1 and _cls(stmts[0]) == "For" and stmts[0].mode in ("thread", "magic_thread"):
+        node, depth = stmts[0], depth + 1
+        stmts = [x for x in node.body.stmts if not _is_ghost(x)]
+    return node, depth
+
+
 def _rw_sets(scope):
     """Names read / assigned (as arrays or scalars) anywhere inside a statement tree."""
     reads, writes = set(), set()
@@ -307,6 +320,7 @@ struct B2Ops {
     int64_t dev;
     int (*pipe)(int, const b2_copy2d *, const int64_t *, const b2_copy2d *, const int64_t *, b2_step_fn, void *, int);
     int64_t pipe_chunk;  // target bytes per pipeline step (0: pipelining off)
+    int64_t coarsen;     // largest thread-coarsening factor for check-free launches (1: off)
 };
 static const B2Ops *g_ops;
 static std::vector<void *> *g_dev_allocs;
@@ -380,6 +394,15 @@ template <typename T, typename S> static void b2_d2h(B2Host<T> &d, B2Dev<S> &s, 
 // twice) and of every output it writes (copied right after it); cells no chunk
 // writes are copied after the last one. Only proved (check-free) launches qualify.
 static int b2_kernel_piped[64];
+static int b2_kernel_coarsen[64];
+extern "C" int b2g_kernel_coarsen(int k) { return (k >= 0 && k < 64) ? b2_kernel_coarsen[k] : -1; }
+// program threads per CUDA thread: the largest of 4 / 2 allowed by ops->coarsen that
+// keeps whole warps (tpb / factor a multiple of 32)
+static int b2_coarsen_for(int64_t tpb) {
+    for (int c = 4; c > 1; c /= 2)
+        if (c <= g_ops->coarsen && tpb % (32 * c) == 0) return c;
+    return 1;
+}
 extern "C" int b2g_kernel_piped(int k) { return (k >= 0 && k < 64) ? b2_kernel_piped[k] : -1; }
 static cudaEvent_t b2_pev[2][64];
 static bool b2_pipe_on() { const char *e = getenv("B2K_CODEGEN_PIPE"); return !(e && e[0] == '0'); }
@@ -958,7 +981,12 @@ class _Gen:
                                   f") * (int64_t)sizeof({s.elem}) + 15) / 16 * 16;")
         # kernel body
         dl = []
+        kctx.block_node, kctx.block_depth = _block_level(kbody)
         kctx.emit_seq(kbody, dl, 1, "b2_w0", "b2_rel0")
+        if kctx.block_node is None or kctx.block_hoist is None:
+            kctx.coarsenable = False
+        if any(s_.kind == "treg_arr" for s_, _ in kctx.local_arrays):
+            kctx.coarsenable = False  # per-thread register arrays are not replicated
         self.kernels.append(kctx.render(dl))
         g, t = self.fresh("bpg"), self.fresh("tpb")
         proof = _Proof(self, kctx, f"({g} * {t})").run(kbody)
@@ -1030,8 +1058,21 @@ class _Gen:
         if nk < 64:  # per-kernel evidence for the first 64 kernels of a program
             L.append(f"    b2_kernel_unchecked[{nk}] = {pv} ? 1 : 0;")
             L.append(f"    b2_kernel_piped[{nk}] = 0;")
-        L.append(f"    if ({smem_bytes} > 48 * 1024) {{ cudaFuncSetAttribute({name}<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int){smem_bytes}); "
-                 f"cudaFuncSetAttribute({name}<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int){smem_bytes}); }}")
+        L.append(f"    if ({smem_bytes} > 48 * 1024) {{")
+        for inst in ("true, 1", "false, 1", "false, 2", "false, 4"):
+            L.append(f"      cudaFuncSetAttribute({name}<{inst}>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int){smem_bytes});")
+        L.append("    }")
+        # thread coarsening (check-free launches of statically eligible kernels whose
+        # outermost thread-for walks exactly the program blocks: its width == tpb)
+        co = self.fresh("co")
+        info["co"] = co
+        blk = kctx.block_hoist
+        if kctx.coarsenable and blk:
+            L.append(f"    const int {co} = ({pv} && (int64_t){name}{blk}_w2 == {t}) ? b2_coarsen_for({t}) : 1;")
+        else:
+            L.append(f"    const int {co} = 1;")
+        if nk < 64:
+            L.append(f"    b2_kernel_coarsen[{nk}] = {co};")
         done = self.fresh("piped")
         L.append(f"    bool {done} = false;")
         if piped:
@@ -1040,8 +1081,10 @@ class _Gen:
         L.extend("      " + ln for ln in h2d_lines)
         L.append("      cudaMemset(b2_err_dev, 0, 5 * sizeof(int));")
         L.append("      cudaEventRecord(b2_ev0, 0);")
-        L.append(f"      if ({pv}) {name}<false><<<(unsigned){g}, (unsigned){t}, (size_t){smem_bytes}>>>({args}, 0u, (uint32_t){g});")
-        L.append(f"      else {name}<true><<<(unsigned){g}, (unsigned){t}, (size_t){smem_bytes}>>>({args}, 0u, (uint32_t){g});")
+        L.append(f"      if ({co} == 4) {name}<false, 4><<<(unsigned){g}, (unsigned)({t} / 4), (size_t){smem_bytes}>>>({args}, 0u, (uint32_t){g});")
+        L.append(f"      else if ({co} == 2) {name}<false, 2><<<(unsigned){g}, (unsigned)({t} / 2), (size_t){smem_bytes}>>>({args}, 0u, (uint32_t){g});")
+        L.append(f"      else if ({pv}) {name}<false, 1><<<(unsigned){g}, (unsigned){t}, (size_t){smem_bytes}>>>({args}, 0u, (uint32_t){g});")
+        L.append(f"      else {name}<true, 1><<<(unsigned){g}, (unsigned){t}, (size_t){smem_bytes}>>>({args}, 0u, (uint32_t){g});")
         L.append("      cudaEventRecord(b2_ev1, 0);")
         L.append(f"      b2_check_kernel(b2_err_dev, \"{name}\");")
         if nk < 64:
@@ -1080,7 +1123,9 @@ class _Gen:
             "        const int64_t _b0 = _pl.bnd[_c], _b1 = _pl.bnd[_c + 1];",
             "        if (_b1 <= _b0) return 0;",
             "        if (_c < 64) cudaEventRecord(b2_pev[0][_c], _s);",
-            f"        {name}<false><<<(unsigned)(_b1 - _b0), (unsigned){t}, (size_t){smem_bytes}, _s>>>({args}, (uint32_t)_b0, (uint32_t){g});",
+            f"        if ({info['co']} == 4) {name}<false, 4><<<(unsigned)(_b1 - _b0), (unsigned)({t} / 4), (size_t){smem_bytes}, _s>>>({args}, (uint32_t)_b0, (uint32_t){g});",
+            f"        else if ({info['co']} == 2) {name}<false, 2><<<(unsigned)(_b1 - _b0), (unsigned)({t} / 2), (size_t){smem_bytes}, _s>>>({args}, (uint32_t)_b0, (uint32_t){g});",
+            f"        else {name}<false, 1><<<(unsigned)(_b1 - _b0), (unsigned){t}, (size_t){smem_bytes}, _s>>>({args}, (uint32_t)_b0, (uint32_t){g});",
             "        if (_c < 64) cudaEventRecord(b2_pev[1][_c], _s);",
             "        return cudaGetLastError() == cudaSuccess ? 0 : 1;",
             "      };",
@@ -1154,6 +1199,15 @@ class _KernelCtx:
         self.uniform_const: dict = {}  # id(For) of launch-uniform literal-extent levels
         self.uniform_w = {"b2_w0"}
         self.root_hoist = None  # first hoisted thread-for level directly under the launch width
+        # thread coarsening: the "block level" is the innermost thread-for of the chain
+        # of pass-through grid levels that open the kernel (A.4: by -> bx; A.5: b); its
+        # iterations are the program blocks when its width equals tpb (checked at launch)
+        self.block_node = None  # that For node (set by kernel_scope via find_block_level)
+        self.block_depth = 0    # its thread-for depth
+        self.block_w2 = None    # its per-iteration width variable
+        self.block_hoist = None  # its hoisted-parameter prefix (must be hoisted)
+        self.coarsenable = True  # statically safe to coarsen (see _emit_for / _emit_simple)
+        self.tf_depth = 0       # thread-for nesting depth during emission
 
     def use(self, s):
         if s.kind == "dev_arr":
@@ -1214,10 +1268,13 @@ class _KernelCtx:
         for s in treg:
             n = " * ".join(f"{s.cname}_d{k}" for k in range(s.rank)) or "1"
             pro.append(f"    {s.elem} {s.cname}[B2_TREG_MAX]; if (({n}) > B2_TREG_MAX) {{ b2_flag(b2_err, B2E_OOB, {n}, B2_TREG_MAX); return; }}")
-        out = [f"template <bool B2CK> __global__ void {self.name}({', '.join(params)}) {{",
+        # B2CO > 1 (thread coarsening, check-free launches only): a CUDA block of tpb / B2CO
+        # threads runs one program block of tpb threads; thread c plays program threads
+        # c, c + blockDim.x, ... in every block-level thread-for (see _emit_for)
+        out = [f"template <bool B2CK, int B2CO> __global__ void {self.name}({', '.join(params)}) {{",
                "    extern __shared__ __align__(16) unsigned char b2_smem[];",
-               "    const uint32_t b2_w0 = b2_gtot * blockDim.x;",
-               "    const uint32_t b2_rel0 = (blockIdx.x + b2_boff) * blockDim.x + threadIdx.x;"]
+               "    const uint32_t b2_w0 = b2_gtot * (blockDim.x * B2CO);",
+               "    const uint32_t b2_rel0 = (blockIdx.x + b2_boff) * (blockDim.x * B2CO) + threadIdx.x;"]
         if treg:
             out.insert(0, "#define B2_TREG_MAX 64")
         out.extend(pro)
@@ -1281,7 +1338,17 @@ class _KernelCtx:
             return
         if c == "For":
             with g.scope(self):
-                self._emit_for(st, out, ind, w, rel)
+                if st.mode in ("thread", "magic_thread") and self.block_w2 is not None and w == self.block_w2:
+                    # a block-level thread-for: under thread coarsening (B2CO > 1) each CUDA
+                    # thread plays B2CO program threads, blockDim.x apart (coalescing kept)
+                    rk = g.fresh("relk")
+                    out.append(pad + "#pragma unroll")
+                    out.append(pad + "for (int b2_k = 0; b2_k < B2CO; ++b2_k) {")
+                    out.append(pad + f"    const uint32_t {rk} = {rel} + (uint32_t)b2_k * blockDim.x;")
+                    self._emit_for(st, out, ind + 1, w, rk)
+                    out.append(pad + "}")
+                else:
+                    self._emit_for(st, out, ind, w, rel)
             return
         if c == "If":
             cond, _ = self.dexpr(st.cond)
@@ -1320,6 +1387,8 @@ class _KernelCtx:
                 self.hoist[id(st)] = hp
                 if w == "b2_w0" and self.root_hoist is None:
                     self.root_hoist = hp
+                if st is self.block_node:
+                    self.block_hoist = hp
                 if _is_const(st.range.start) and _is_const(st.range.stop):
                     # literal extent: nvcc folds n and the start; the host supplies
                     # the width split (loop-invariant, check-free) for proved launches
@@ -1347,7 +1416,11 @@ class _KernelCtx:
                 out.append(pad + f"  const int {sh} = B2CK ? (({w2} & ({w2} - 1u)) == 0u ? __ffs({w2}) - 1 : -1) : {hp}_sh;")
                 out.append(pad + f"  const int64_t {v} = (B2CK ? ({s0}) : {hp}_s0) + (int64_t)({sh} >= 0 ? {rel} >> {sh} : {rel} / {w2});")
             out.append(pad + f"  const uint32_t {r2} = {sh} >= 0 ? ({rel} & ({w2} - 1u)) : {rel} % {w2};")
+            if st is self.block_node:
+                self.block_w2 = w2
+            self.tf_depth += 1
             self.emit_seq(st.body.stmts, out, ind + 1, w2, r2)
+            self.tf_depth -= 1
             out.append(pad + "  } }")
             return
         e = g.fresh("stop")
@@ -1362,6 +1435,8 @@ class _KernelCtx:
         c = _cls(st)
         if c == "CallStmt":
             if st.fn in ("blocksync", "kernel_teardown_sync"):
+                if self.tf_depth != self.block_depth:  # a barrier off the block level: no coarsening
+                    self.coarsenable = False
                 out.append(pad + "__syncthreads();")
                 return
             raise UnsupportedProgram(f"call to {st.fn!r} inside a kernel")
@@ -1372,6 +1447,7 @@ class _KernelCtx:
             s = Sym(st.name, "scalar", st.ctype)
             g.syms[st.name] = s
             self.local_syms.add(st.name)
+            s.depth = self.tf_depth
             out.extend(pad + p for p in g.pre)
             if st.ctype == "float":
                 out.append(pad + f"float {s.cname} = {g.store_value(s, code, t)};")
@@ -1386,6 +1462,8 @@ class _KernelCtx:
                     raise UnsupportedProgram(f"{s.name!r} is not assignable")
                 if st.target.base not in self.local_syms:
                     raise UnsupportedProgram(f"kernel assigns host scalar {s.name!r}")
+                if self.tf_depth > self.block_depth and getattr(s, "depth", 0) <= self.block_depth:
+                    self.coarsenable = False  # program threads write a block-level local
                 if st.op == "+=":
                     val, t = (f"({s.cname} + {val})", "i") if (t == "i" and s.ctype == "int") else \
                         (f"((double){s.cname} + (double)({val}))", "d")
@@ -1696,6 +1774,8 @@ class Compiled:
         self.lib.b2g_kernel_unchecked.argtypes = [ctypes.c_int]
         self.lib.b2g_kernel_piped.restype = ctypes.c_int
         self.lib.b2g_kernel_piped.argtypes = [ctypes.c_int]
+        self.lib.b2g_kernel_coarsen.restype = ctypes.c_int
+        self.lib.b2g_kernel_coarsen.argtypes = [ctypes.c_int]
         self.n_kernels = source.count("__global__ void b2g_kernel")
         # the generated host code keeps per-call state (ops table, allocation lists,
         # timing events) in statics of its .so: one call at a time per program
@@ -1710,6 +1790,10 @@ class Compiled:
         surrounding copies (b2_pipe_run), 0 if it ran as one launch between them."""
         return [self.lib.b2g_kernel_piped(k) for k in range(min(self.n_kernels, 64))]
 
+    def kernel_coarsen(self) -> list:
+        """Per kernel: program threads per CUDA thread in its last launch (1, 2, 4)."""
+        return [self.lib.b2g_kernel_coarsen(k) for k in range(min(self.n_kernels, 64))]
+
     def kernel_unchecked(self) -> list:
         """Per kernel: True if its last launch ran the check-free instantiation (all
         accesses proved in bounds on the host for that launch)."""
@@ -1720,7 +1804,7 @@ class B2Ops(ctypes.Structure):
     """Host runtime services handed to generated code (libb200k.so copy engine)."""
     _fields_ = [("h2d", ctypes.c_void_p), ("d2h", ctypes.c_void_p), ("last_error", ctypes.c_void_p),
                 ("alloc", ctypes.c_void_p), ("dfree", ctypes.c_void_p), ("dev", ctypes.c_int64),
-                ("pipe", ctypes.c_void_p), ("pipe_chunk", ctypes.c_int64)]
+                ("pipe", ctypes.c_void_p), ("pipe_chunk", ctypes.c_int64), ("coarsen", ctypes.c_int64)]
 
 
 def _ops(dev: int) -> B2Ops:
@@ -1729,8 +1813,11 @@ def _ops(dev: int) -> B2Ops:
     addr = lambda f: ctypes.cast(f, ctypes.c_void_p).value  # noqa: E731
     # bytes per pipeline step (tune key codegen.pipe_kb; 0 = no copy / kernel pipelining)
     chunk = int(L.b2_tune_get(b"codegen.pipe_kb")) * 1024
+    # thread coarsening of check-free generated kernels (tune key codegen.coarsen; 1 = off)
+    coarsen = max(1, int(L.b2_tune_get(b"codegen.coarsen")))
     return B2Ops(addr(L.b2_copy_h2d), addr(L.b2_copy_d2h), addr(L.b2_last_error),
-                 addr(L.b2_device_alloc), addr(L.b2_device_free), dev, addr(L.b2_pipe_run), max(chunk, 0))
+                 addr(L.b2_device_alloc), addr(L.b2_device_free), dev, addr(L.b2_pipe_run), max(chunk, 0),
+                 coarsen)
 
 
 class B2Arr(ctypes.Structure):

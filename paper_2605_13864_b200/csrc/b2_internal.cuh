@@ -60,6 +60,7 @@ struct Tuning {
     int t_staged_stages = 4;  // cp.async ring depth of the staged kernel (2, 3, 4)
     int c_pipe_kb = 65536;  // generated programs: bytes per copy / kernel pipeline step (KiB; 0 = off)
     int l_pdl = 0;          // 1 = launch the hot kernels with programmatic dependent launch
+    int c_coarsen = 4;      // generated programs: largest thread-coarsening factor (1 = off)
 };
 extern Tuning g_tune;
 constexpr int kInflightBytesPerSM = 64 * 1024;

@@ -327,6 +327,7 @@ static int *tune_slot(const char *key) {
     if (k == "transpose.staged") return &g_tune.t_staged;
     if (k == "codegen.pipe_kb") return &g_tune.c_pipe_kb;
     if (k == "launch.pdl") return &g_tune.l_pdl;
+    if (k == "codegen.coarsen") return &g_tune.c_coarsen;
     if (k == "transpose.staged_ctas") return &g_tune.t_staged_ctas;
     if (k == "transpose.staged_stages") return &g_tune.t_staged_stages;
     return nullptr;

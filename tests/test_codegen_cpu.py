@@ -76,7 +76,10 @@ def test_a4_structure_like_spec_acceptance_1():
     # proved every access in bounds for the concrete launch — in program order
     # between the copies (twice: the plain path and the pipeline's fallback), plus the
     # chunk launch of the copy / kernel pipeline on its stream
-    assert host.count("<true><<<") == 2 and host.count("<false><<<") == 3 and host.count("<<<") == 5
+    # (check-free launches also come thread-coarsened: 2 or 4 program threads per CUDA thread)
+    assert host.count("<true, 1><<<") == 2 and host.count("<false, 1><<<") == 3
+    assert host.count("<false, 2><<<") == 3 and host.count("<false, 4><<<") == 3 and host.count("<<<") == 11
+    assert "template <bool B2CK, int B2CO>" in src and "b2_k < B2CO" in kernel
     assert host.count("b2_run_plan(") == 1 and host.count("b2fp_acc(_fp, 0, 0,") == 2  # d_in read, 2 dims
     assert host.count("b2fp_acc(_fp, 1, 1,") == 2  # d_out written, 2 dims
     assert host.count("b2i_in(") >= 4 and "catch (B2NoProof &)" in host

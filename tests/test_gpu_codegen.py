@@ -151,3 +151,72 @@ def test_bounds_proof_selects_check_free_kernels(b2, monkeypatch):
     with pytest.raises(b2.InterpError, match="out of bounds"):
         b2.run_program(p, "shift", {"arr": [0.5] * 128, "N": 128}, backend="codegen")
     assert not any(c.kernel_unchecked())
+
+
+@pytest.mark.parametrize("H,W", [(64, 96), (256, 512), (1024, 2048)])
+def test_a4_thread_coarsened_bit_exact(b2, H, W):
+    """Check-free launches of A.4 run thread-coarsened (128 CUDA threads play the
+    program's 512 per block): same bits as the oracle, and as coarsening off."""
+    from paper_2605_13864_b200 import _lib, codegen
+    p = _prog(b2, "transpose_gpu.optc")
+    a = np.random.default_rng(H * W).standard_normal((H, W)).astype(np.float32)
+    inp = {"in": a.reshape(-1).tolist(), "out": [0.0] * (H * W), "W": W, "H": H}
+    _, got = b2.run_program(p, "transpose", dict(inp), backend="codegen")
+    c = codegen.compile_fn(p.fn("transpose"))
+    assert c.kernel_coarsen()[0] == 4 and c.kernel_unchecked()[0]
+    assert np.array_equal(np.array(got["out"], np.float32), oracle.transpose(a).reshape(-1))
+    _lib.tune("codegen.coarsen", 1)
+    try:
+        _, plain = b2.run_program(p, "transpose", dict(inp), backend="codegen")
+        assert c.kernel_coarsen()[0] == 1
+    finally:
+        _lib.tune("codegen.coarsen", 4)
+    assert plain["out"] == got["out"]
+
+
+def test_a5_thread_coarsened_bit_exact(b2):
+    from paper_2605_13864_b200 import codegen
+    p = _prog(b2, "reduce_tree_f32.optc")
+    x = np.random.default_rng(9).uniform(-1, 1, 512 * 77).astype(np.float32)
+    ret, _ = b2.run_program(p, "reduce", {"arr": x.tolist(), "N": x.size}, backend="codegen")
+    assert codegen.compile_fn(p.fn("reduce")).kernel_coarsen()[0] == 4
+    want, _ = oracle.reduce_f32_tree512(x)
+    assert np.float32(ret).view(np.uint32) == np.float32(want).view(np.uint32)
+
+
+NOT_COARSENABLE = {
+    # a barrier inside a block-level thread-for (the interpreter treats it as a no-op)
+    "barrier_in_thread_for": "thread for (int t = 0; t < 128; t++) { o[b * 128 + t] = d[b * 128 + t]; blocksync(); }",
+    # program threads accumulate into a block-level local
+    "block_local_written": "float acc = 0.0; thread for (int t = 0; t < 128; t++) { acc = acc + 1.0; "
+                           "o[b * 128 + t] = d[b * 128 + t] + acc; }",
+}
+
+
+@pytest.mark.parametrize("case", sorted(NOT_COARSENABLE))
+def test_coarsening_refused_where_unsound(b2, case):
+    from paper_2605_13864_b200 import codegen
+    src = f"""void f(float* a, float* r, int N) {{
+    float* const d = gmem_malloc1<float>(N);
+    memcpy_host_to_device1(d, a, N);
+    float* const o = gmem_malloc1<float>(N);
+    {{
+        kernel_launch(N / 128, 128, 0);
+        kernel_setup_end();
+        thread for (int b = 0; b < N / 128; b++) {{
+            {NOT_COARSENABLE[case]}
+        }}
+        kernel_teardown_begin();
+        kernel_kill();
+    }}
+    memcpy_device_to_host1(r, o, N);
+    gmem_free(o);
+    gmem_free(d);
+}}
+"""
+    p = b2.parse_program(src)
+    n = 128 * 6
+    x = np.arange(n, dtype=np.float32)
+    b2.run_program(p, "f", {"a": x.tolist(), "r": [0.0] * n, "N": n}, backend="codegen")
+    c = codegen.compile_fn(p.fn("f"))
+    assert c.kernel_unchecked()[0] and c.kernel_coarsen()[0] == 1

@@ -65,3 +65,16 @@ def test_tma_variant_and_tree_kernel(table):
     b = _body(table, "transpose_tmar_kernel<256, 2, 2>")
     assert "UTMALDG" in b and "SYNCS" in b
     assert "SHFL" in _body(table, "tree_kernel<512, 256>")
+
+
+def test_staged_odd_pitch_kernel_uses_cp_async(table):
+    """The 2-byte odd-pitch path fetches 16-B chunks with cp.async (LDGSTS) into its
+    shared-memory ring and waits on commit groups (DEPBAR), one barrier per tile."""
+    b = _body(table, "transpose_staged_kernel<unsigned short, 64, 128, 256, 4>")
+    assert "LDGSTS.E.BYPASS.128" in b and "DEPBAR" in b and "BAR.SYNC" in b
+
+
+def test_fp32_sum_accumulates_in_binary64(table):
+    """fp32 cells are widened (F2F.F64.F32) and added in binary64 (DADD)."""
+    b = _body(table, "reduce_kernel<float, 512, 4, 1>")
+    assert "F2F.F64.F32" in b and "DADD" in b

@@ -20,7 +20,8 @@ DEFAULTS = [  # (demangled-name prefix, role)
     ("transpose_vec_kernel<8, 128, 32, 512>", "fp64 large transpose, 256x64 tile"),
     ("transpose_vec_kernel<2, 16, 16, 256>", "bf16 transpose, 128x128 tile"),
     ("transpose_vec_kernel<4, 16, 16, 256>", "fp32 small / mid transpose, 64x64 tile"),
-    ("transpose_scalar_kernel<unsigned short, 128>", "2-byte odd pitches, padded 64x128 tile"),
+    ("transpose_staged_kernel<unsigned short, 64, 128, 256, 4>", "2-byte odd pitches >= 2^22 cells, cp.async-staged ring"),
+    ("transpose_scalar_kernel<unsigned short, 128>", "2-byte odd pitches (small), padded 64x128 tile"),
     ("transpose_scalar_kernel<unsigned int, 64>", "4-byte odd pitches, padded 64x64 tile"),
     ("reduce_kernel<int, 512, 4, 1>", "C3 int32 sum (bench)"),
     ("reduce_kernel<float, 512, 4, 1>", "fp32 sum"),
@@ -30,7 +31,8 @@ DEFAULTS = [  # (demangled-name prefix, role)
 OPS = [("LDG.128", r"LDG\.E[.A-Z0-9_]*\.128"), ("LDG.256", r"LDG\.E[.A-Z0-9_]*\.256"), ("STG.128", r"STG\.E[.A-Z0-9_]*\.128"),
        ("STG.256", r"STG\.E[.A-Z0-9_]*\.256"), ("STS.128", r"STS\.128"), ("LDS.128", r"LDS\.128"),
        ("LDG.16/32", r"LDG\.E(\.U16|\.U8)?(\.CONSTANT)? "), ("BAR.SYNC", r"BAR\.SYNC"), ("SHFL", r"SHFL\."),
-       ("PRMT", r"PRMT "), ("UTMALDG", r"UTMALDG"), ("ATOMG/RED", r"ATOMG|REDG|RED\."), ("SYNCS", r"SYNCS\.")]
+       ("PRMT", r"PRMT "), ("UTMALDG", r"UTMALDG"), ("ATOMG/RED", r"ATOMG|REDG|RED\."), ("SYNCS", r"SYNCS\."),
+       ("LDGSTS", r"LDGSTS"), ("F2F.F64", r"F2F\.F64\.F32"), ("DADD", r"DADD")]
 
 
 def demangle(names):

@@ -397,10 +397,17 @@ static int b2_kernel_piped[64];
 static int b2_kernel_coarsen[64];
 extern "C" int b2g_kernel_coarsen(int k) { return (k >= 0 && k < 64) ? b2_kernel_coarsen[k] : -1; }
 // program threads per CUDA thread: the largest of 4 / 2 allowed by ops->coarsen that
-// keeps whole warps (tpb / factor a multiple of 32)
-static int b2_coarsen_for(int64_t tpb) {
-    for (int c = 4; c > 1; c /= 2)
-        if (c <= g_ops->coarsen && tpb % (32 * c) == 0) return c;
+// keeps whole warps (tpb / factor a multiple of 32) and still lets a full SM's worth
+// of CUDA threads (2048) be resident: <= 32 blocks and their shared memory within
+// 160 KB. Measured (profiles/r02h_codegen_coarsen.md): the 64x64-tile transpose
+// (16.6 KB per block) at factor 4 could only keep 13 blocks = 1664 threads per SM and
+// ran at 2.7 TB/s against 4.6 at factor 2.
+static int b2_coarsen_for(int64_t tpb, int64_t smem) {
+    for (int c = 4; c > 1; c /= 2) {
+        if (c > g_ops->coarsen || tpb % (32 * c) != 0) continue;
+        const int64_t blocks = 2048 / (tpb / c);
+        if (blocks <= 32 && blocks * smem <= 160 * 1024) return c;
+    }
     return 1;
 }
 extern "C" int b2g_kernel_piped(int k) { return (k >= 0 && k < 64) ? b2_kernel_piped[k] : -1; }
@@ -1068,7 +1075,7 @@ class _Gen:
         info["co"] = co
         blk = kctx.block_hoist
         if kctx.coarsenable and blk:
-            L.append(f"    const int {co} = ({pv} && (int64_t){name}{blk}_w2 == {t}) ? b2_coarsen_for({t}) : 1;")
+            L.append(f"    const int {co} = ({pv} && (int64_t){name}{blk}_w2 == {t}) ? b2_coarsen_for({t}, {smem_bytes}) : 1;")
         else:
             L.append(f"    const int {co} = 1;")
         if nk < 64:

@@ -103,6 +103,32 @@ def has_kernel(fn) -> bool:
     return fn.body is not None and walk(fn.body)
 
 
+# kernel instantiations: <B2CK, B2CO (program threads per CUDA thread), B2IX (index type)>
+_INSTANCES = ("true, 1, int64_t", "false, 1, int64_t", "false, 2, int64_t", "false, 4, int64_t",
+              "false, 1, int32_t", "false, 2, int32_t", "false, 4, int32_t")
+
+
+def _launch_switch(name, pv, ix32, co, grid, t, smem, stream, args):
+    """Host lines launching the instantiation chosen at run time: the checked one
+    unless proved; proved launches coarsened by `co` and in 32-bit index arithmetic
+    when `ix32` (the proof bounded every integer below 2^31)."""
+    L = []
+    for c in (4, 2, 1):
+        for ity in ("int32_t", "int64_t"):
+            cond = f"{pv} && {co} == {c} && {'' if ity == 'int32_t' else '!'}{ix32}"
+            L.append(f"{'if' if not L else 'else if'} ({cond}) {name}<false, {c}, {ity}><<<{grid}, (unsigned)({t} / {c}), "
+                     f"(size_t){smem}, {stream}>>>({args});")
+    L.append(f"else {name}<true, 1, int64_t><<<{grid}, (unsigned){t}, (size_t){smem}, {stream}>>>({args});")
+    return L
+
+
+class Seq_like:
+    """A statement list viewed as a Seq (for _rw_sets)."""
+
+    def __init__(self, stmts):
+        self.stmts = list(stmts)
+
+
 def _block_level(kbody):
     """(For node, depth) of the kernel's block level: follow the chain of thread-fors
     that are the only statement of their enclosing body, from the kernel body down;
@@ -217,14 +243,21 @@ enum { B2E_OOB = 1, B2E_RANK = 2, B2E_DIV = 3, B2E_WIDTH = 4 };
 __device__ __forceinline__ void b2_flag(int *f, int code, int64_t a, int64_t b) {
     if (atomicCAS(f, 0, code) == 0) { f[1] = (int)a; f[2] = (int)b; f[3] = (int)(a >> 32); f[4] = (int)(b >> 32); }
 }
-__host__ __device__ __forceinline__ int64_t b2_div(int64_t a, int64_t b) { return b ? a / b : 0; }
-__host__ __device__ __forceinline__ int64_t b2_mod(int64_t a, int64_t b) { return b ? a - (a / b) * b : 0; }
-__host__ __device__ __forceinline__ int64_t b2_pow2(int64_t k) { return k < 0 ? 0 : ((int64_t)1 << k); }
+// integer helpers in the operands' common type: int64_t on the host and in checked
+// kernels, int32_t in check-free kernels whose launch-time proof bounded every
+// integer expression below 2^31 (then no intermediate can overflow)
+template <typename A, typename B> __host__ __device__ __forceinline__ auto b2_div(A a, B b) -> decltype(a / b) {
+    return b ? a / b : 0;
+}
+template <typename A, typename B> __host__ __device__ __forceinline__ auto b2_mod(A a, B b) -> decltype(a % b) {
+    return b ? a - (a / b) * b : 0;
+}
+template <typename I> __host__ __device__ __forceinline__ I b2_pow2(I k) { return k < 0 ? 0 : ((I)1 << k); }
 static inline int64_t b2_exact_div_h(int64_t a, int64_t b) {
     if (b == 0 || a % b != 0) b2_throw("exact_div(" + std::to_string(a) + ", " + std::to_string(b) + ") is not exact");
     return a / b;
 }
-__device__ __forceinline__ int64_t b2_exact_div_d(int64_t a, int64_t b, int *f) {
+template <typename A, typename B> __device__ __forceinline__ auto b2_exact_div_d(A a, B b, int *f) -> decltype(a / b) {
     if (b == 0 || a % b != 0) { b2_flag(f, B2E_DIV, a, b); return 0; }
     return a / b;
 }
@@ -259,9 +292,17 @@ __device__ __forceinline__ bool b2_chk(int64_t ix, int64_t d, int *f) {
 struct B2NoProof {};
 struct B2I { int64_t lo, hi; };
 static const int64_t B2I_BIG = (int64_t)1 << 62;
+// largest |bound| of any interval the current proof produced: < 2^31 lets the
+// check-free kernel run with 32-bit integer arithmetic (B2IX = int32_t)
+static int64_t b2i_maxabs = 0;
+static inline B2I b2i_t(B2I x) {
+    const int64_t m = std::max(x.lo < 0 ? -x.lo : x.lo, x.hi < 0 ? -x.hi : x.hi);
+    if (m > b2i_maxabs) b2i_maxabs = m;
+    return x;
+}
 static inline B2I b2i_fit(__int128 lo, __int128 hi) {
     if (lo < -(__int128)B2I_BIG || hi > (__int128)B2I_BIG) throw B2NoProof{};
-    return B2I{(int64_t)lo, (int64_t)hi};
+    return b2i_t(B2I{(int64_t)lo, (int64_t)hi});
 }
 static inline B2I b2i_c(int64_t v) { return b2i_fit(v, v); }
 static inline B2I b2i_unknown() { throw B2NoProof{}; }
@@ -275,21 +316,21 @@ static inline B2I b2i_mul(B2I a, B2I b) {
 }
 static inline B2I b2i_div(B2I a, B2I b) {  // truncating, non-negative dividend, constant positive divisor
     if (b.lo != b.hi || b.lo <= 0 || a.lo < 0) throw B2NoProof{};
-    return B2I{a.lo / b.lo, a.hi / b.lo};
+    return b2i_t(B2I{a.lo / b.lo, a.hi / b.lo});
 }
 static inline B2I b2i_mod(B2I a, B2I b) {
     if (b.lo != b.hi || b.lo <= 0 || a.lo < 0) throw B2NoProof{};
-    return a.hi < b.lo ? a : B2I{0, b.lo - 1};
+    return b2i_t(a.hi < b.lo ? a : B2I{0, b.lo - 1});
 }
 static inline B2I b2i_exact_div(B2I a, B2I b) {
     if (b.lo != b.hi || b.lo <= 0) throw B2NoProof{};
     if (a.lo == a.hi && a.lo % b.lo != 0) throw B2NoProof{};  // the kernel will raise: keep its checks
     auto fl = [](int64_t x, int64_t d) { return x >= 0 ? x / d : -((-x + d - 1) / d); };
-    return B2I{fl(a.lo, b.lo), fl(a.hi, b.lo)};
+    return b2i_t(B2I{fl(a.lo, b.lo), fl(a.hi, b.lo)});
 }
 static inline B2I b2i_pow2(B2I k) {  // monotonic: [2^lo, 2^hi]
     if (k.lo < 0 || k.hi > 61) throw B2NoProof{};
-    return B2I{(int64_t)1 << k.lo, (int64_t)1 << k.hi};
+    return b2i_t(B2I{(int64_t)1 << k.lo, (int64_t)1 << k.hi});
 }
 static inline B2I b2i_join(B2I a, B2I b) { return B2I{a.lo < b.lo ? a.lo : b.lo, a.hi > b.hi ? a.hi : b.hi}; }
 static inline int b2i_in(B2I ix, int64_t d) {  // every value of ix indexes [0, d)
@@ -395,6 +436,9 @@ template <typename T, typename S> static void b2_d2h(B2Host<T> &d, B2Dev<S> &s, 
 // writes are copied after the last one. Only proved (check-free) launches qualify.
 static int b2_kernel_piped[64];
 static int b2_kernel_coarsen[64];
+static int b2_kernel_ix32[64];
+extern "C" int b2g_kernel_ix32(int k) { return (k >= 0 && k < 64) ? b2_kernel_ix32[k] : -1; }
+static bool b2_ix32_enabled() { const char *e = getenv("B2K_CODEGEN_IX32"); return !(e && e[0] == '0'); }
 extern "C" int b2g_kernel_coarsen(int k) { return (k >= 0 && k < 64) ? b2_kernel_coarsen[k] : -1; }
 // program threads per CUDA thread: the largest of 4 / 2 allowed by ops->coarsen that
 // keeps whole warps (tpb / factor a multiple of 32) and still lets a full SM's worth
@@ -610,7 +654,13 @@ class _Gen:
         """-> (C code, type) with type in i (int64), f (binary32 value), d (double)."""
         c = _cls(e)
         if c == "IntLit":
-            return f"((int64_t){int(e.value)}LL)", "i"
+            v = int(e.value)
+            if dev is not None and -2**31 < v < 2**31:
+                # kernel code: the index type of the instantiation (int32_t when the launch-time
+                # proof bounds every integer expression of the kernel below 2^31, else int64_t);
+                # array cell values stay int64_t and promote mixed expressions
+                return f"((B2IX){v})", "i"
+            return f"((int64_t){v}LL)", "i"
         if c == "FloatLit":
             return _f32_literal(e.value), "f"
         if c == "Var":
@@ -627,9 +677,10 @@ class _Gen:
             b, tb = self.expr(e.rhs, dev)
             op = e.op
             if op in ("==", "!=", "<", "<=", ">", ">="):
+                ity = "B2IX" if dev is not None else "int64_t"
                 if ta == "i" and tb == "i":
-                    return f"((int64_t)({a} {op} {b}))", "i"
-                return f"((int64_t)((double)({a}) {op} (double)({b})))", "i"
+                    return f"(({ity})({a} {op} {b}))", "i"
+                return f"(({ity})((double)({a}) {op} (double)({b})))", "i"
             if ta == "i" and tb == "i":
                 if op in ("+", "-", "*"):
                     return f"({a} {op} {b})", "i"
@@ -660,7 +711,7 @@ class _Gen:
             k = len(e.args) // 2
             dims = [self.expr(a, dev)[0] for a in e.args[:k]]
             idxs = [self.expr(a, dev)[0] for a in e.args[k:]]
-            out = "((int64_t)0)"
+            out = "((B2IX)0)" if dev is not None else "((int64_t)0)"
             for d, ix in zip(dims, idxs):
                 out = f"({out} * {d} + {ix})"
             return out, "i"
@@ -689,18 +740,18 @@ class _Gen:
         lines = []
         if len(codes) == s.rank + 1 and s.rank == 1:
             ix = self.fresh("ix")
-            lines.append(f"const int64_t {ix} = {codes[0]} + {codes[1]};")
+            lines.append(f"const B2IX {ix} = {codes[0]} + {codes[1]};")
             return f"B2_CHK({ix}, {dims}[0])", ix, lines
         if len(codes) != s.rank:
             raise UnsupportedProgram(f"rank mismatch on {s.name!r}: {len(codes)} indices into {s.rank}-d array")
-        ok, off = [], "((int64_t)0)"
+        ok, off = [], "((B2IX)0)"
         padded = s.kind == "smem_arr" and s.rank >= 2
         for k, cd in enumerate(codes):
             v = self.fresh("ix")
-            lines.append(f"const int64_t {v} = {cd};")
+            lines.append(f"const B2IX {v} = {cd};")
             ok.append(f"B2_CHK({v}, {dims}[{k}])")
             # shared arrays: the last dimension is stored with a padded pitch
-            stride = f"{s.cname}_pitch" if (padded and k == s.rank - 1) else f"{dims}[{k}]"
+            stride = f"(B2IX){s.cname}_pitch" if (padded and k == s.rank - 1) else f"(B2IX){dims}[{k}]"
             off = f"({off} * {stride} + {v})"
         return "(" + " && ".join(ok or ["true"]) + ")", off, lines
 
@@ -988,6 +1039,7 @@ class _Gen:
                                   f") * (int64_t)sizeof({s.elem}) + 15) / 16 * 16;")
         # kernel body
         dl = []
+        kctx.assigned = _rw_sets(Seq_like(kbody))[1]
         kctx.block_node, kctx.block_depth = _block_level(kbody)
         kctx.emit_seq(kbody, dl, 1, "b2_w0", "b2_rel0")
         if kctx.block_node is None or kctx.block_hoist is None:
@@ -1054,19 +1106,28 @@ class _Gen:
         L.append(f"    bool {pv} = false;")
         for hp in kctx.hoist.values():
             L.append(f"    int64_t {name}{hp}_n = 0, {name}{hp}_s0 = 0; uint32_t {name}{hp}_w2 = 1; int {name}{hp}_sh = -1;")
+        ix32 = self.fresh("ix32")
+        info["ix32"] = ix32
+        L.append(f"    bool {ix32} = false;")
         L.append("    if (b2_prove_enabled()) {")
         L.append("      try {")
+        L.append("        b2i_maxabs = 0;")
         L.append("        [&]() {")
         L.extend("          " + ln for ln in info["proof"])
         L.append("        }();")
         L.append(f"        {pv} = true;")
+        # 32-bit index arithmetic: every interval the proof saw, and every device array
+        # the kernel addresses (flat offsets), below 2^31
+        sizes = " && ".join(f"{s_.cname}.n < 2147483647LL" for s_ in kctx.arrays.values()) or "true"
+        L.append(f"        {ix32} = b2_ix32_enabled() && b2i_maxabs < 2147483647LL && {sizes};")
         L.append("      } catch (B2NoProof &) {}")
         L.append("    }")
         if nk < 64:  # per-kernel evidence for the first 64 kernels of a program
             L.append(f"    b2_kernel_unchecked[{nk}] = {pv} ? 1 : 0;")
             L.append(f"    b2_kernel_piped[{nk}] = 0;")
+            L.append(f"    b2_kernel_ix32[{nk}] = {ix32} ? 1 : 0;")
         L.append(f"    if ({smem_bytes} > 48 * 1024) {{")
-        for inst in ("true, 1", "false, 1", "false, 2", "false, 4"):
+        for inst in _INSTANCES:
             L.append(f"      cudaFuncSetAttribute({name}<{inst}>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int){smem_bytes});")
         L.append("    }")
         # thread coarsening (check-free launches of statically eligible kernels whose
@@ -1088,10 +1149,8 @@ class _Gen:
         L.extend("      " + ln for ln in h2d_lines)
         L.append("      cudaMemset(b2_err_dev, 0, 5 * sizeof(int));")
         L.append("      cudaEventRecord(b2_ev0, 0);")
-        L.append(f"      if ({co} == 4) {name}<false, 4><<<(unsigned){g}, (unsigned)({t} / 4), (size_t){smem_bytes}>>>({args}, 0u, (uint32_t){g});")
-        L.append(f"      else if ({co} == 2) {name}<false, 2><<<(unsigned){g}, (unsigned)({t} / 2), (size_t){smem_bytes}>>>({args}, 0u, (uint32_t){g});")
-        L.append(f"      else if ({pv}) {name}<false, 1><<<(unsigned){g}, (unsigned){t}, (size_t){smem_bytes}>>>({args}, 0u, (uint32_t){g});")
-        L.append(f"      else {name}<true, 1><<<(unsigned){g}, (unsigned){t}, (size_t){smem_bytes}>>>({args}, 0u, (uint32_t){g});")
+        L.extend("      " + ln for ln in _launch_switch(name, pv, ix32, co, f"(unsigned){g}", t, smem_bytes, "0",
+                                                   f"{args}, 0u, (uint32_t){g}"))
         L.append("      cudaEventRecord(b2_ev1, 0);")
         L.append(f"      b2_check_kernel(b2_err_dev, \"{name}\");")
         if nk < 64:
@@ -1130,9 +1189,8 @@ class _Gen:
             "        const int64_t _b0 = _pl.bnd[_c], _b1 = _pl.bnd[_c + 1];",
             "        if (_b1 <= _b0) return 0;",
             "        if (_c < 64) cudaEventRecord(b2_pev[0][_c], _s);",
-            f"        if ({info['co']} == 4) {name}<false, 4><<<(unsigned)(_b1 - _b0), (unsigned)({t} / 4), (size_t){smem_bytes}, _s>>>({args}, (uint32_t)_b0, (uint32_t){g});",
-            f"        else if ({info['co']} == 2) {name}<false, 2><<<(unsigned)(_b1 - _b0), (unsigned)({t} / 2), (size_t){smem_bytes}, _s>>>({args}, (uint32_t)_b0, (uint32_t){g});",
-            f"        else {name}<false, 1><<<(unsigned)(_b1 - _b0), (unsigned){t}, (size_t){smem_bytes}, _s>>>({args}, (uint32_t)_b0, (uint32_t){g});",
+            *("        " + ln for ln in _launch_switch(name, "true", info["ix32"], info["co"], "(unsigned)(_b1 - _b0)", t,
+                                                  smem_bytes, "_s", f"{args}, (uint32_t)_b0, (uint32_t){g}")),
             "        if (_c < 64) cudaEventRecord(b2_pev[1][_c], _s);",
             "        return cudaGetLastError() == cudaSuccess ? 0 : 1;",
             "      };",
@@ -1215,6 +1273,7 @@ class _KernelCtx:
         self.block_hoist = None  # its hoisted-parameter prefix (must be hoisted)
         self.coarsenable = True  # statically safe to coarsen (see _emit_for / _emit_simple)
         self.tf_depth = 0       # thread-for nesting depth during emission
+        self.assigned: set = set()  # scalar names assigned anywhere in the kernel body
 
     def use(self, s):
         if s.kind == "dev_arr":
@@ -1265,7 +1324,11 @@ class _KernelCtx:
                 treg.append(s)
         for s in self.scalars.values():
             ty = "double" if s.kind == "param_float" else ("float" if s.ctype == "float" else "int64_t")
-            params.append(f"const {ty} {s.cname}")
+            if ty == "int64_t":  # host ints enter kernel arithmetic in the index type
+                params.append(f"const int64_t {s.cname}_p")
+                pro.append(f"    const B2IX {s.cname} = (B2IX){s.cname}_p;")
+            else:
+                params.append(f"const {ty} {s.cname}")
         for hp in self.hoist.values():
             params.append(f"const int64_t {hp}_n, const int64_t {hp}_s0, const uint32_t {hp}_w2, const int {hp}_sh")
         params.append("int *b2_err")
@@ -1278,7 +1341,7 @@ class _KernelCtx:
         # B2CO > 1 (thread coarsening, check-free launches only): a CUDA block of tpb / B2CO
         # threads runs one program block of tpb threads; thread c plays program threads
         # c, c + blockDim.x, ... in every block-level thread-for (see _emit_for)
-        out = [f"template <bool B2CK, int B2CO> __global__ void {self.name}({', '.join(params)}) {{",
+        out = [f"template <bool B2CK, int B2CO, typename B2IX> __global__ void {self.name}({', '.join(params)}) {{",
                "    extern __shared__ __align__(16) unsigned char b2_smem[];",
                "    const uint32_t b2_w0 = b2_gtot * (blockDim.x * B2CO);",
                "    const uint32_t b2_rel0 = (blockIdx.x + b2_boff) * (blockDim.x * B2CO) + threadIdx.x;"]
@@ -1288,6 +1351,26 @@ class _KernelCtx:
         out.extend(body_lines)
         out.append("}")
         return "\n".join(out) + "\n"
+
+    def _index_expr(self, e) -> bool:
+        """Integer expression of literals, loop indices, host ints and index-kind
+        locals only (no array reads): its intervals are what the bounds proof
+        evaluates, so it may run in the 32-bit index type when they fit."""
+        c = _cls(e)
+        if c == "IntLit":
+            return True
+        if c == "Var":
+            sym = self.g.syms.get(e.name)
+            if sym is None or sym.is_array or sym.ctype == "float" or sym.kind == "param_float":
+                return False
+            if sym.loop or e.name not in self.local_syms:
+                return True
+            return getattr(sym, "ix", False)
+        if c == "BinOp":
+            return e.op in ("+", "-", "*", "/", "%") and self._index_expr(e.lhs) and self._index_expr(e.rhs)
+        if c == "Call" and (e.fn in ("exact_div", "pow2") or e.fn.startswith("DMINDEX")):
+            return all(self._index_expr(a) for a in e.args)
+        return False
 
     def _uniform(self, e) -> bool:
         """Launch-uniform integer expression: constants and captured host ints only."""
@@ -1413,7 +1496,7 @@ class _KernelCtx:
                                      f"{{ b2_flag(b2_err, B2E_WIDTH, {n}, {w}); return; }}")
                     out.append(pad + f"  const uint32_t {w2} = B2CK ? {w} / (uint32_t){n} : {hp}_w2;")
                     out.append(pad + f"  const int {sh} = B2CK ? (({w2} & ({w2} - 1u)) == 0u ? __ffs({w2}) - 1 : -1) : {hp}_sh;")
-                out.append(pad + f"  const int64_t {v} = ({s0}) + (int64_t)({sh} >= 0 ? {rel} >> {sh} : {rel} / {w2});")
+                out.append(pad + f"  const B2IX {v} = ({s0}) + (B2IX)({sh} >= 0 ? {rel} >> {sh} : {rel} / {w2});")
             else:  # proved launches take the host's values: no checks, no divisions
                 out.append(pad + f"{{ const int64_t {n} = B2CK ? (({s1}) - ({s0})) : {hp}_n;")
                 out.append(pad + f"  if ({n} > 0) {{")
@@ -1421,7 +1504,7 @@ class _KernelCtx:
                                  f"{{ b2_flag(b2_err, B2E_WIDTH, {n}, {w}); return; }}")
                 out.append(pad + f"  const uint32_t {w2} = B2CK ? {w} / (uint32_t){n} : {hp}_w2;")
                 out.append(pad + f"  const int {sh} = B2CK ? (({w2} & ({w2} - 1u)) == 0u ? __ffs({w2}) - 1 : -1) : {hp}_sh;")
-                out.append(pad + f"  const int64_t {v} = (B2CK ? ({s0}) : {hp}_s0) + (int64_t)({sh} >= 0 ? {rel} >> {sh} : {rel} / {w2});")
+                out.append(pad + f"  const B2IX {v} = (B2CK ? (B2IX)({s0}) : (B2IX){hp}_s0) + (B2IX)({sh} >= 0 ? {rel} >> {sh} : {rel} / {w2});")
             out.append(pad + f"  const uint32_t {r2} = {sh} >= 0 ? ({rel} & ({w2} - 1u)) : {rel} % {w2};")
             if st is self.block_node:
                 self.block_w2 = w2
@@ -1431,8 +1514,8 @@ class _KernelCtx:
             out.append(pad + "  } }")
             return
         e = g.fresh("stop")
-        out.append(pad + f"{{ const int64_t {e} = {s1};")
-        out.append(pad + f"for (int64_t {v} = {s0}; {v} < {e}; ++{v}) {{")
+        out.append(pad + f"{{ const B2IX {e} = {s1};")
+        out.append(pad + f"for (B2IX {v} = {s0}; {v} < {e}; ++{v}) {{")
         self.emit_seq(st.body.stmts, out, ind + 1, w, rel)
         out.append(pad + "} }")
 
@@ -1451,7 +1534,9 @@ class _KernelCtx:
             if st.alloc is not None:
                 raise UnsupportedProgram(f"{st.alloc} inside a kernel body")
             code, t = self.dexpr(st.init)
+            ix = st.ctype == "int" and st.name not in self.assigned and self._index_expr(st.init)
             s = Sym(st.name, "scalar", st.ctype)
+            s.ix = ix
             g.syms[st.name] = s
             self.local_syms.add(st.name)
             s.depth = self.tf_depth
@@ -1459,7 +1544,9 @@ class _KernelCtx:
             if st.ctype == "float":
                 out.append(pad + f"float {s.cname} = {g.store_value(s, code, t)};")
             else:
-                out.append(pad + f"int64_t {s.cname} = {code};")
+                # index-kind locals (never reassigned, built from literals, loop indices,
+                # host ints and other such locals) take the instantiation's index type
+                out.append(pad + f"{'B2IX' if s.ix else 'int64_t'} {s.cname} = {code};")
             return
         if c == "Assign":
             s = g.sym(st.target.base)
@@ -1783,6 +1870,8 @@ class Compiled:
         self.lib.b2g_kernel_piped.argtypes = [ctypes.c_int]
         self.lib.b2g_kernel_coarsen.restype = ctypes.c_int
         self.lib.b2g_kernel_coarsen.argtypes = [ctypes.c_int]
+        self.lib.b2g_kernel_ix32.restype = ctypes.c_int
+        self.lib.b2g_kernel_ix32.argtypes = [ctypes.c_int]
         self.n_kernels = source.count("__global__ void b2g_kernel")
         # the generated host code keeps per-call state (ops table, allocation lists,
         # timing events) in statics of its .so: one call at a time per program
@@ -1800,6 +1889,10 @@ class Compiled:
     def kernel_coarsen(self) -> list:
         """Per kernel: program threads per CUDA thread in its last launch (1, 2, 4)."""
         return [self.lib.b2g_kernel_coarsen(k) for k in range(min(self.n_kernels, 64))]
+
+    def kernel_ix32(self) -> list:
+        """Per kernel: True if its last launch used 32-bit index arithmetic."""
+        return [self.lib.b2g_kernel_ix32(k) == 1 for k in range(min(self.n_kernels, 64))]
 
     def kernel_unchecked(self) -> list:
         """Per kernel: True if its last launch ran the check-free instantiation (all

@@ -76,10 +76,15 @@ def test_a4_structure_like_spec_acceptance_1():
     # proved every access in bounds for the concrete launch — in program order
     # between the copies (twice: the plain path and the pipeline's fallback), plus the
     # chunk launch of the copy / kernel pipeline on its stream
-    # (check-free launches also come thread-coarsened: 2 or 4 program threads per CUDA thread)
-    assert host.count("<true, 1><<<") == 2 and host.count("<false, 1><<<") == 3
-    assert host.count("<false, 2><<<") == 3 and host.count("<false, 4><<<") == 3 and host.count("<<<") == 11
-    assert "template <bool B2CK, int B2CO>" in src and "b2_k < B2CO" in kernel
+    # (check-free launches also come thread-coarsened — 1, 2 or 4 program threads per
+    # CUDA thread — and in 32-bit index arithmetic when the proof bounds every integer)
+    sites = 3  # the plain path, the pipeline branch's fallback, the pipeline's chunk launch
+    assert host.count("<true, 1, int64_t><<<") == sites
+    for c in (1, 2, 4):
+        for ity in ("int32_t", "int64_t"):
+            assert host.count(f"<false, {c}, {ity}><<<") == sites, (c, ity)
+    assert host.count("<<<") == 7 * sites
+    assert "template <bool B2CK, int B2CO, typename B2IX>" in src and "b2_k < B2CO" in kernel
     assert host.count("b2_run_plan(") == 1 and host.count("b2fp_acc(_fp, 0, 0,") == 2  # d_in read, 2 dims
     assert host.count("b2fp_acc(_fp, 1, 1,") == 2  # d_out written, 2 dims
     assert host.count("b2i_in(") >= 4 and "catch (B2NoProof &)" in host
@@ -96,7 +101,7 @@ def test_a5_structure_tree_loop_with_barrier():
     loop with __syncthreads() inside it."""
     src = codegen.generate(_fn("reduce_tree_f32.optc"))
     kernel = src[src.index("__global__"):src.index('extern "C" int b2g_main')]
-    start = kernel.index("for (int64_t v_k")
+    start = kernel.index("for (B2IX v_k")  # the index type of the instantiation
     depth, i = 0, kernel.index("{", start)
     while True:  # the loop body: up to the brace that closes the for
         depth += {"{": 1, "}": -1}.get(kernel[i], 0)
@@ -160,4 +165,4 @@ def test_block_scoped_declarations():
            "kernel_setup_end(); for (int k = 0; k < 4; k++) { if (N > 0) { float k = 0.5; d[0] = k; } d[k] = 1.0; } "
            "kernel_teardown_begin(); kernel_kill(); } memcpy_device_to_host1(a, d, N); gmem_free(d); }")
     s = codegen.generate(parse_program(src).entry())
-    assert "float v_k" in s and "int64_t v_k" in s
+    assert "float v_k" in s and "B2IX v_k" in s  # the loop index keeps the index type

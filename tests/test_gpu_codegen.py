@@ -220,3 +220,47 @@ def test_coarsening_refused_where_unsound(b2, case):
     b2.run_program(p, "f", {"a": x.tolist(), "r": [0.0] * n, "N": n}, backend="codegen")
     c = codegen.compile_fn(p.fn("f"))
     assert c.kernel_unchecked()[0] and c.kernel_coarsen()[0] == 1
+
+
+WIDE_INTERMEDIATE = """void f(float* a, float* r, int N) {
+    float* const d = gmem_malloc1<float>(N);
+    memcpy_host_to_device1(d, a, N);
+    float* const o = gmem_malloc1<float>(N);
+    {
+        kernel_launch(N / 64, 64, 0);
+        kernel_setup_end();
+        thread for (int b = 0; b < N / 64; b++) {
+            thread for (int t = 0; t < 64; t++) {
+                o[b * 64 + t] = d[b * 64 + (t * 100000000) / 100000000];
+            }
+        }
+        kernel_teardown_begin();
+        kernel_kill();
+    }
+    memcpy_device_to_host1(r, o, N);
+    gmem_free(o);
+    gmem_free(d);
+}
+"""
+
+
+def test_32bit_index_arithmetic_only_when_proved(b2):
+    """Check-free kernels run with 32-bit integer arithmetic only when the launch
+    proof bounds every integer expression below 2^31: A.4 qualifies; an index whose
+    intermediate t * 10^8 reaches 6.3e9 keeps 64-bit arithmetic (in 32 bits it would
+    wrap and read the wrong cell) and still returns the right cells."""
+    from paper_2605_13864_b200 import codegen
+    p = _prog(b2, "transpose_gpu.optc")
+    a = np.random.default_rng(1).standard_normal((64, 96)).astype(np.float32)
+    _, got = b2.run_program(p, "transpose", {"in": a.reshape(-1).tolist(), "out": [0.0] * a.size,
+                                             "W": 96, "H": 64}, backend="codegen")
+    c = codegen.compile_fn(p.fn("transpose"))
+    assert c.kernel_ix32()[0] and c.kernel_unchecked()[0]
+    assert np.array_equal(np.array(got["out"], np.float32), a.T.reshape(-1))
+    q = b2.parse_program(WIDE_INTERMEDIATE)
+    n = 64 * 10
+    x = np.random.default_rng(2).standard_normal(n).astype(np.float32)
+    _, got = b2.run_program(q, "f", {"a": x.tolist(), "r": [0.0] * n, "N": n}, backend="codegen")
+    c = codegen.compile_fn(q.fn("f"))
+    assert c.kernel_unchecked()[0] and not c.kernel_ix32()[0]
+    assert np.array_equal(np.array(got["r"], np.float32), x)

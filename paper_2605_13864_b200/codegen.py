@@ -1274,6 +1274,7 @@ class _KernelCtx:
         self.coarsenable = True  # statically safe to coarsen (see _emit_for / _emit_simple)
         self.tf_depth = 0       # thread-for nesting depth during emission
         self.assigned: set = set()  # scalar names assigned anywhere in the kernel body
+        self.tail_ifs: dict = {}    # id(If) -> stop flag of its coarsening loop
 
     def use(self, s):
         if s.kind == "dev_arr":
@@ -1432,8 +1433,20 @@ class _KernelCtx:
                     # a block-level thread-for: under thread coarsening (B2CO > 1) each CUDA
                     # thread plays B2CO program threads, blockDim.x apart (coalescing kept)
                     rk = g.fresh("relk")
-                    out.append(pad + "#pragma unroll")
-                    out.append(pad + "for (int b2_k = 0; b2_k < B2CO; ++b2_k) {")
+                    tail = self._tail_if(st)
+                    if tail is not None:
+                        # `thread for t { if (t < e) {...} }` with e the same for every program
+                        # thread of the block: t grows with b2_k, so once a played thread fails
+                        # the test every later one does too — stop there (the tree levels of
+                        # A.5 skip most of their idle iterations)
+                        stop = g.fresh("stop")
+                        self.tail_ifs[id(tail)] = stop
+                        out.append(pad + f"bool {stop} = false;")
+                        out.append(pad + "#pragma unroll")
+                        out.append(pad + f"for (int b2_k = 0; b2_k < B2CO && !{stop}; ++b2_k) {{")
+                    else:
+                        out.append(pad + "#pragma unroll")
+                        out.append(pad + "for (int b2_k = 0; b2_k < B2CO; ++b2_k) {")
                     out.append(pad + f"    const uint32_t {rk} = {rel} + (uint32_t)b2_k * blockDim.x;")
                     self._emit_for(st, out, ind + 1, w, rk)
                     out.append(pad + "}")
@@ -1450,9 +1463,41 @@ class _KernelCtx:
                 out.append(pad + "} else {")
                 with g.scope(self):
                     self.emit_seq(st.els.stmts, out, ind + 1, w, rel)
+            elif id(st) in self.tail_ifs:
+                out.append(pad + f"}} else {{ {self.tail_ifs[id(st)]} = true;")
             out.append(pad + "}")
             return
         self._emit_simple(st, out, ind, w, rel)
+
+    def _tail_if(self, st):
+        """The If of `thread for t { if (t < e) {...} }` (or `<=`, no else) when e
+        cannot change from one program thread of the block to the next (it reads
+        no thread-level names and no arrays); else None."""
+        body = [x for x in st.body.stmts if not _is_ghost(x)]
+        if len(body) != 1 or _cls(body[0]) != "If" or body[0].els is not None:
+            return None
+        cond = body[0].cond
+        if _cls(cond) != "BinOp" or cond.op not in ("<", "<=") or _cls(cond.lhs) != "Var" \
+                or cond.lhs.name != st.index:
+            return None
+
+        def uniform(e):
+            c = _cls(e)
+            if c == "IntLit":
+                return True
+            if c == "Var":
+                sym = self.g.syms.get(e.name)
+                if sym is None or sym.is_array or e.name == st.index:
+                    return False
+                if e.name not in self.local_syms:
+                    return True  # host scalar
+                return getattr(sym, "depth", 99) <= self.block_depth
+            if c == "BinOp":
+                return uniform(e.lhs) and uniform(e.rhs)
+            if c == "Call" and e.fn in ("pow2", "exact_div"):
+                return all(uniform(a) for a in e.args)
+            return False
+        return body[0] if uniform(cond.rhs) else None
 
     def _emit_for(self, st, out, ind, w, rel):
         g = self.g
@@ -1462,6 +1507,7 @@ class _KernelCtx:
         pre = g.pre
         g.syms[st.index] = Sym(st.index, "scalar", "int")
         g.syms[st.index].loop = True
+        g.syms[st.index].depth = self.tf_depth + (1 if st.mode in ("thread", "magic_thread") else 0)
         self.local_syms.add(st.index)
         v = "v_" + st.index
         out.extend(pad + p for p in pre)

@@ -103,22 +103,32 @@ def has_kernel(fn) -> bool:
     return fn.body is not None and walk(fn.body)
 
 
-# kernel instantiations: <B2CK, B2CO (program threads per CUDA thread), B2IX (index type)>
-_INSTANCES = ("true, 1, int64_t", "false, 1, int64_t", "false, 2, int64_t", "false, 4, int64_t",
-              "false, 1, int32_t", "false, 2, int32_t", "false, 4, int32_t")
+# kernel instantiations: <B2CK, B2CO (program threads per CUDA thread), B2PK (program
+# blocks per CUDA block), B2IX (index type)>. Packing (B2PK = 2, with twice the base
+# coarsening factor) only exists in 32-bit index arithmetic.
+_VARIANTS = {"int32_t": ((1, 1), (2, 1), (4, 1), (4, 2), (8, 2)),
+             "int64_t": ((1, 1), (2, 1), (4, 1))}
+_INSTANCES = ("true, 1, 1, int64_t",) + tuple(f"false, {c}, {p}, {ity}" for ity, vs in _VARIANTS.items()
+                                             for c, p in vs)
 
 
-def _launch_switch(name, pv, ix32, co, grid, t, smem, stream, args):
+def _launch_switch(name, pv, ix32, co, pk, grid, t, smem, stream, args):
     """Host lines launching the instantiation chosen at run time: the checked one
-    unless proved; proved launches coarsened by `co` and in 32-bit index arithmetic
-    when `ix32` (the proof bounded every integer below 2^31)."""
-    L = []
-    for c in (4, 2, 1):
-        for ity in ("int32_t", "int64_t"):
-            cond = f"{pv} && {co} == {c} && {'' if ity == 'int32_t' else '!'}{ix32}"
-            L.append(f"{'if' if not L else 'else if'} ({cond}) {name}<false, {c}, {ity}><<<{grid}, (unsigned)({t} / {c}), "
-                     f"(size_t){smem}, {stream}>>>({args});")
-    L.append(f"else {name}<true, 1, int64_t><<<{grid}, (unsigned){t}, (size_t){smem}, {stream}>>>({args});")
+    unless proved; proved launches coarsened by `co`, `pk` program blocks per CUDA
+    block (when the launch's block count divides by it; else unpacked at the base
+    factor co / pk) and in 32-bit
+    index arithmetic when `ix32` (the proof bounded every integer below 2^31)."""
+    L = [f"{{ const unsigned _gb = {grid};",
+         f"  const int _pk = (_gb % (unsigned){pk} == 0u) ? {pk} : 1;",
+         f"  const int _co = (_pk == {pk}) ? {co} : {co} / {pk};"]
+    first = True
+    for ity, vs in _VARIANTS.items():
+        for c, p in vs:
+            cond = f"{pv} && _co == {c} && _pk == {p} && {'' if ity == 'int32_t' else '!'}{ix32}"
+            L.append(f"  {'if' if first else 'else if'} ({cond}) {name}<false, {c}, {p}, {ity}><<<_gb / {p}u, "
+                     f"(unsigned)({p} * {t} / {c}), (size_t)({p} * {smem}), {stream}>>>({args});")
+            first = False
+    L.append(f"  else {name}<true, 1, 1, int64_t><<<_gb, (unsigned){t}, (size_t){smem}, {stream}>>>({args}); }}")
     return L
 
 
@@ -362,6 +372,7 @@ struct B2Ops {
     int (*pipe)(int, const b2_copy2d *, const int64_t *, const b2_copy2d *, const int64_t *, b2_step_fn, void *, int);
     int64_t pipe_chunk;  // target bytes per pipeline step (0: pipelining off)
     int64_t coarsen;     // largest thread-coarsening factor for check-free launches (1: off)
+    int64_t pack;        // most program blocks per CUDA block for check-free launches (1: off)
 };
 static const B2Ops *g_ops;
 static std::vector<void *> *g_dev_allocs;
@@ -436,23 +447,39 @@ template <typename T, typename S> static void b2_d2h(B2Host<T> &d, B2Dev<S> &s, 
 // writes are copied after the last one. Only proved (check-free) launches qualify.
 static int b2_kernel_piped[64];
 static int b2_kernel_coarsen[64];
+static int b2_kernel_pack[64];
+extern "C" int b2g_kernel_pack(int k) { return (k >= 0 && k < 64) ? b2_kernel_pack[k] : -1; }
 static int b2_kernel_ix32[64];
 extern "C" int b2g_kernel_ix32(int k) { return (k >= 0 && k < 64) ? b2_kernel_ix32[k] : -1; }
 static bool b2_ix32_enabled() { const char *e = getenv("B2K_CODEGEN_IX32"); return !(e && e[0] == '0'); }
 extern "C" int b2g_kernel_coarsen(int k) { return (k >= 0 && k < 64) ? b2_kernel_coarsen[k] : -1; }
-// program threads per CUDA thread: the largest of 4 / 2 allowed by ops->coarsen that
-// keeps whole warps (tpb / factor a multiple of 32) and still lets a full SM's worth
-// of CUDA threads (2048) be resident: <= 32 blocks and their shared memory within
-// 160 KB. Measured (profiles/r02h_codegen_coarsen.md): the 64x64-tile transpose
-// (16.6 KB per block) at factor 4 could only keep 13 blocks = 1664 threads per SM and
-// ran at 2.7 TB/s against 4.6 at factor 2.
-static int b2_coarsen_for(int64_t tpb, int64_t smem) {
+// Thread coarsening / block packing of a check-free launch (tpb program threads and
+// smem bytes of shared memory per program block): c program threads per CUDA thread,
+// p program blocks per CUDA block of p * tpb / c threads. The base factor c (4 or 2)
+// is the largest that keeps whole warps and a full SM's worth of CUDA threads (2048)
+// resident: <= 32 blocks and their shared memory within 160 KB. Measured
+// (profiles/r02h_codegen_coarsen.md): the 64x64-tile transpose (16.6 KB per block) at
+// c = 4 could only keep 13 blocks = 1664 threads per SM and ran at 2.7 TB/s against
+// 4.6 at c = 2. When that base configuration sits at the 32-blocks-per-SM cap (CUDA
+// blocks of <= 64 threads: small program blocks such as A.5's), the cap, not the
+// threads, limits the program blocks in flight; then two program blocks share one
+// CUDA block at twice the factor (same block size, 2x the program blocks per SM: A.5
+// 2.6 -> 3.0 TB/s, profiles/r02j_codegen_pack.md). 8-fold coarsening alone (A.4: 32
+// program blocks per SM instead of 16) measured 4-7 % slower and is not used.
+// Packing needs `packable` (no barrier under block-dependent control flow), an even
+// block count and, like c = 8, 32-bit indices.
+static void b2_pack_for(int64_t tpb, int64_t smem, int64_t grid, bool packable, bool ix32, int *co, int *pk) {
+    *co = 1; *pk = 1;
     for (int c = 4; c > 1; c /= 2) {
         if (c > g_ops->coarsen || tpb % (32 * c) != 0) continue;
         const int64_t blocks = 2048 / (tpb / c);
-        if (blocks <= 32 && blocks * smem <= 160 * 1024) return c;
+        if (blocks <= 32 && blocks * smem <= 160 * 1024) { *co = c; break; }
     }
-    return 1;
+    const int64_t T = tpb / *co;
+    if (*co > 1 && 2 * *co <= g_ops->coarsen && g_ops->pack >= 2 && packable && ix32 && grid % 2 == 0 &&
+        2048 / T == 32 && 32 * 2 * smem <= 160 * 1024) {
+        *co *= 2; *pk = 2;
+    }
 }
 extern "C" int b2g_kernel_piped(int k) { return (k >= 0 && k < 64) ? b2_kernel_piped[k] : -1; }
 static cudaEvent_t b2_pev[2][64];
@@ -1132,15 +1159,16 @@ class _Gen:
         L.append("    }")
         # thread coarsening (check-free launches of statically eligible kernels whose
         # outermost thread-for walks exactly the program blocks: its width == tpb)
-        co = self.fresh("co")
-        info["co"] = co
+        co, pk = self.fresh("co"), self.fresh("pk")
+        info["co"], info["pk"] = co, pk
         blk = kctx.block_hoist
+        L.append(f"    int {co} = 1, {pk} = 1;")
         if kctx.coarsenable and blk:
-            L.append(f"    const int {co} = ({pv} && (int64_t){name}{blk}_w2 == {t}) ? b2_coarsen_for({t}, {smem_bytes}) : 1;")
-        else:
-            L.append(f"    const int {co} = 1;")
+            L.append(f"    if ({pv} && (int64_t){name}{blk}_w2 == {t}) b2_pack_for({t}, {smem_bytes}, {g}, "
+                     f"{'true' if kctx.packable else 'false'}, {ix32}, &{co}, &{pk});")
         if nk < 64:
             L.append(f"    b2_kernel_coarsen[{nk}] = {co};")
+            L.append(f"    b2_kernel_pack[{nk}] = {pk};")
         done = self.fresh("piped")
         L.append(f"    bool {done} = false;")
         if piped:
@@ -1149,7 +1177,7 @@ class _Gen:
         L.extend("      " + ln for ln in h2d_lines)
         L.append("      cudaMemset(b2_err_dev, 0, 5 * sizeof(int));")
         L.append("      cudaEventRecord(b2_ev0, 0);")
-        L.extend("      " + ln for ln in _launch_switch(name, pv, ix32, co, f"(unsigned){g}", t, smem_bytes, "0",
+        L.extend("      " + ln for ln in _launch_switch(name, pv, ix32, co, pk, f"(unsigned){g}", t, smem_bytes, "0",
                                                    f"{args}, 0u, (uint32_t){g}"))
         L.append("      cudaEventRecord(b2_ev1, 0);")
         L.append(f"      b2_check_kernel(b2_err_dev, \"{name}\");")
@@ -1189,7 +1217,7 @@ class _Gen:
             "        const int64_t _b0 = _pl.bnd[_c], _b1 = _pl.bnd[_c + 1];",
             "        if (_b1 <= _b0) return 0;",
             "        if (_c < 64) cudaEventRecord(b2_pev[0][_c], _s);",
-            *("        " + ln for ln in _launch_switch(name, "true", info["ix32"], info["co"], "(unsigned)(_b1 - _b0)", t,
+            *("        " + ln for ln in _launch_switch(name, "true", info["ix32"], info["co"], info["pk"], "(unsigned)(_b1 - _b0)", t,
                                                   smem_bytes, "_s", f"{args}, (uint32_t)_b0, (uint32_t){g}")),
             "        if (_c < 64) cudaEventRecord(b2_pev[1][_c], _s);",
             "        return cudaGetLastError() == cudaSuccess ? 0 : 1;",
@@ -1272,6 +1300,8 @@ class _KernelCtx:
         self.block_w2 = None    # its per-iteration width variable
         self.block_hoist = None  # its hoisted-parameter prefix (must be hoisted)
         self.coarsenable = True  # statically safe to coarsen (see _emit_for / _emit_simple)
+        self.packable = True     # every barrier under launch-uniform control flow only
+        self.nonuniform_cf = 0   # depth of enclosing ifs / fors whose condition / bounds vary
         self.tf_depth = 0       # thread-for nesting depth during emission
         self.assigned: set = set()  # scalar names assigned anywhere in the kernel body
         self.tail_ifs: dict = {}    # id(If) -> stop flag of its coarsening loop
@@ -1342,10 +1372,19 @@ class _KernelCtx:
         # B2CO > 1 (thread coarsening, check-free launches only): a CUDA block of tpb / B2CO
         # threads runs one program block of tpb threads; thread c plays program threads
         # c, c + blockDim.x, ... in every block-level thread-for (see _emit_for)
-        out = [f"template <bool B2CK, int B2CO, typename B2IX> __global__ void {self.name}({', '.join(params)}) {{",
-               "    extern __shared__ __align__(16) unsigned char b2_smem[];",
-               "    const uint32_t b2_w0 = b2_gtot * (blockDim.x * B2CO);",
-               "    const uint32_t b2_rel0 = (blockIdx.x + b2_boff) * (blockDim.x * B2CO) + threadIdx.x;"]
+        # B2PK > 1 (block packing): the CUDA block runs B2PK consecutive program blocks side
+        # by side, b2_pbw CUDA threads each, every one with its own slice of the dynamic
+        # shared memory; their barriers coincide (packing requires every barrier to sit in
+        # launch-uniform control flow, see _emit_simple)
+        out = [f"template <bool B2CK, int B2CO, int B2PK, typename B2IX> __global__ void {self.name}({', '.join(params)}) {{",
+               "    extern __shared__ __align__(16) unsigned char b2_smem0[];",
+               "    const uint32_t b2_pbw = blockDim.x / B2PK;",
+               "    const uint32_t b2_sub = B2PK == 1 ? 0u : threadIdx.x / b2_pbw;",
+               "    unsigned char *b2_smem = b2_smem0;",
+               "    if (B2PK > 1) { uint32_t b2_dsm; asm(\"mov.u32 %0, %%dynamic_smem_size;\" : \"=r\"(b2_dsm)); "
+               "b2_smem += b2_sub * (b2_dsm / B2PK); }",
+               "    const uint32_t b2_w0 = b2_gtot * (b2_pbw * B2CO);",
+               "    const uint32_t b2_rel0 = (blockIdx.x * B2PK + b2_sub + b2_boff) * (b2_pbw * B2CO) + (threadIdx.x - b2_sub * b2_pbw);"]
         if treg:
             out.insert(0, "#define B2_TREG_MAX 64")
         out.extend(pro)
@@ -1431,7 +1470,7 @@ class _KernelCtx:
             with g.scope(self):
                 if st.mode in ("thread", "magic_thread") and self.block_w2 is not None and w == self.block_w2:
                     # a block-level thread-for: under thread coarsening (B2CO > 1) each CUDA
-                    # thread plays B2CO program threads, blockDim.x apart (coalescing kept)
+                    # thread plays B2CO program threads, b2_pbw apart (coalescing kept)
                     rk = g.fresh("relk")
                     tail = self._tail_if(st)
                     if tail is not None:
@@ -1447,7 +1486,7 @@ class _KernelCtx:
                     else:
                         out.append(pad + "#pragma unroll")
                         out.append(pad + "for (int b2_k = 0; b2_k < B2CO; ++b2_k) {")
-                    out.append(pad + f"    const uint32_t {rk} = {rel} + (uint32_t)b2_k * blockDim.x;")
+                    out.append(pad + f"    const uint32_t {rk} = {rel} + (uint32_t)b2_k * b2_pbw;")
                     self._emit_for(st, out, ind + 1, w, rk)
                     out.append(pad + "}")
                 else:
@@ -1457,6 +1496,8 @@ class _KernelCtx:
             cond, _ = self.dexpr(st.cond)
             out.extend(pad + p for p in g.pre)
             out.append(pad + f"if ({cond}) {{")
+            nu = not self._uniform(st.cond)
+            self.nonuniform_cf += nu
             with g.scope(self):
                 self.emit_seq(st.then.stmts, out, ind + 1, w, rel)
             if st.els is not None:
@@ -1465,6 +1506,7 @@ class _KernelCtx:
                     self.emit_seq(st.els.stmts, out, ind + 1, w, rel)
             elif id(st) in self.tail_ifs:
                 out.append(pad + f"}} else {{ {self.tail_ifs[id(st)]} = true;")
+            self.nonuniform_cf -= nu
             out.append(pad + "}")
             return
         self._emit_simple(st, out, ind, w, rel)
@@ -1562,7 +1604,10 @@ class _KernelCtx:
         e = g.fresh("stop")
         out.append(pad + f"{{ const B2IX {e} = {s1};")
         out.append(pad + f"for (B2IX {v} = {s0}; {v} < {e}; ++{v}) {{")
+        nu = not (self._uniform(st.range.start) and self._uniform(st.range.stop))
+        self.nonuniform_cf += nu
         self.emit_seq(st.body.stmts, out, ind + 1, w, rel)
+        self.nonuniform_cf -= nu
         out.append(pad + "} }")
 
     def _emit_simple(self, st, out, ind, w, rel):
@@ -1573,6 +1618,8 @@ class _KernelCtx:
             if st.fn in ("blocksync", "kernel_teardown_sync"):
                 if self.tf_depth != self.block_depth:  # a barrier off the block level: no coarsening
                     self.coarsenable = False
+                if self.nonuniform_cf:  # packed program blocks could disagree on reaching it
+                    self.packable = False
                 out.append(pad + "__syncthreads();")
                 return
             raise UnsupportedProgram(f"call to {st.fn!r} inside a kernel")
@@ -1916,6 +1963,8 @@ class Compiled:
         self.lib.b2g_kernel_piped.argtypes = [ctypes.c_int]
         self.lib.b2g_kernel_coarsen.restype = ctypes.c_int
         self.lib.b2g_kernel_coarsen.argtypes = [ctypes.c_int]
+        self.lib.b2g_kernel_pack.restype = ctypes.c_int
+        self.lib.b2g_kernel_pack.argtypes = [ctypes.c_int]
         self.lib.b2g_kernel_ix32.restype = ctypes.c_int
         self.lib.b2g_kernel_ix32.argtypes = [ctypes.c_int]
         self.n_kernels = source.count("__global__ void b2g_kernel")
@@ -1933,8 +1982,12 @@ class Compiled:
         return [self.lib.b2g_kernel_piped(k) for k in range(min(self.n_kernels, 64))]
 
     def kernel_coarsen(self) -> list:
-        """Per kernel: program threads per CUDA thread in its last launch (1, 2, 4)."""
+        """Per kernel: program threads per CUDA thread in its last launch (1, 2, 4; 8 packed)."""
         return [self.lib.b2g_kernel_coarsen(k) for k in range(min(self.n_kernels, 64))]
+
+    def kernel_pack(self) -> list:
+        """Per kernel: program blocks per CUDA block in its last launch (1, 2)."""
+        return [self.lib.b2g_kernel_pack(k) for k in range(min(self.n_kernels, 64))]
 
     def kernel_ix32(self) -> list:
         """Per kernel: True if its last launch used 32-bit index arithmetic."""
@@ -1950,7 +2003,8 @@ class B2Ops(ctypes.Structure):
     """Host runtime services handed to generated code (libb200k.so copy engine)."""
     _fields_ = [("h2d", ctypes.c_void_p), ("d2h", ctypes.c_void_p), ("last_error", ctypes.c_void_p),
                 ("alloc", ctypes.c_void_p), ("dfree", ctypes.c_void_p), ("dev", ctypes.c_int64),
-                ("pipe", ctypes.c_void_p), ("pipe_chunk", ctypes.c_int64), ("coarsen", ctypes.c_int64)]
+                ("pipe", ctypes.c_void_p), ("pipe_chunk", ctypes.c_int64), ("coarsen", ctypes.c_int64),
+                ("pack", ctypes.c_int64)]
 
 
 def _ops(dev: int) -> B2Ops:
@@ -1961,9 +2015,11 @@ def _ops(dev: int) -> B2Ops:
     chunk = int(L.b2_tune_get(b"codegen.pipe_kb")) * 1024
     # thread coarsening of check-free generated kernels (tune key codegen.coarsen; 1 = off)
     coarsen = max(1, int(L.b2_tune_get(b"codegen.coarsen")))
+    # program blocks per CUDA block for small program blocks (tune key codegen.pack; 1 = off)
+    pack = max(1, int(L.b2_tune_get(b"codegen.pack")))
     return B2Ops(addr(L.b2_copy_h2d), addr(L.b2_copy_d2h), addr(L.b2_last_error),
                  addr(L.b2_device_alloc), addr(L.b2_device_free), dev, addr(L.b2_pipe_run), max(chunk, 0),
-                 coarsen)
+                 coarsen, pack)
 
 
 class B2Arr(ctypes.Structure):

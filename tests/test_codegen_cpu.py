@@ -79,12 +79,16 @@ def test_a4_structure_like_spec_acceptance_1():
     # (check-free launches also come thread-coarsened — 1, 2 or 4 program threads per
     # CUDA thread — and in 32-bit index arithmetic when the proof bounds every integer)
     sites = 3  # the plain path, the pipeline branch's fallback, the pipeline's chunk launch
-    assert host.count("<true, 1, int64_t><<<") == sites
-    for c in (1, 2, 4):
-        for ity in ("int32_t", "int64_t"):
-            assert host.count(f"<false, {c}, {ity}><<<") == sites, (c, ity)
-    assert host.count("<<<") == 7 * sites
-    assert "template <bool B2CK, int B2CO, typename B2IX>" in src and "b2_k < B2CO" in kernel
+    # (and with several small program blocks packed into one CUDA block: B2PK)
+    assert host.count("<true, 1, 1, int64_t><<<") == sites
+    variants = {"int32_t": ((1, 1), (2, 1), (4, 1), (4, 2), (8, 2)),
+                "int64_t": ((1, 1), (2, 1), (4, 1))}
+    for ity, vs in variants.items():
+        for c, pk in vs:
+            assert host.count(f"<false, {c}, {pk}, {ity}><<<") == sites, (c, pk, ity)
+    assert host.count("<<<") == 9 * sites
+    assert "template <bool B2CK, int B2CO, int B2PK, typename B2IX>" in src and "b2_k < B2CO" in kernel
+    assert "b2_k * b2_pbw" in kernel and "%%dynamic_smem_size" in kernel
     assert host.count("b2_run_plan(") == 1 and host.count("b2fp_acc(_fp, 0, 0,") == 2  # d_in read, 2 dims
     assert host.count("b2fp_acc(_fp, 1, 1,") == 2  # d_out written, 2 dims
     assert host.count("b2i_in(") >= 4 and "catch (B2NoProof &)" in host

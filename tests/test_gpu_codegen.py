@@ -163,25 +163,85 @@ def test_a4_thread_coarsened_bit_exact(b2, H, W):
     inp = {"in": a.reshape(-1).tolist(), "out": [0.0] * (H * W), "W": W, "H": H}
     _, got = b2.run_program(p, "transpose", dict(inp), backend="codegen")
     c = codegen.compile_fn(p.fn("transpose"))
-    assert c.kernel_coarsen()[0] == 4 and c.kernel_unchecked()[0]
+    # 512 program threads per block, 4 KB of shared memory: 4 per CUDA thread (128-thread
+    # blocks, 16 resident per SM = 2048 threads), below the 32-block cap: no packing
+    assert c.kernel_coarsen()[0] == 4 and c.kernel_pack()[0] == 1 and c.kernel_unchecked()[0]
     assert np.array_equal(np.array(got["out"], np.float32), oracle.transpose(a).reshape(-1))
-    _lib.tune("codegen.coarsen", 1)
-    try:
-        _, plain = b2.run_program(p, "transpose", dict(inp), backend="codegen")
-        assert c.kernel_coarsen()[0] == 1
-    finally:
-        _lib.tune("codegen.coarsen", 4)
-    assert plain["out"] == got["out"]
+    prev = _lib.tuning("codegen.coarsen")
+    for co in (2, 1):
+        _lib.tune("codegen.coarsen", co)
+        try:
+            _, plain = b2.run_program(p, "transpose", dict(inp), backend="codegen")
+            assert c.kernel_coarsen()[0] == co
+        finally:
+            _lib.tune("codegen.coarsen", prev)
+        assert plain["out"] == got["out"]
 
 
-def test_a5_thread_coarsened_bit_exact(b2):
-    from paper_2605_13864_b200 import codegen
+@pytest.mark.parametrize("blocks,co,pk", [(77, 4, 1), (78, 8, 2), (4096, 8, 2)])
+def test_a5_thread_coarsened_bit_exact(b2, blocks, co, pk):
+    """A.5 (256 program threads, 1 KB of shared memory per block): an even block count
+    packs two program blocks per 64-thread CUDA block at 8 program threads per CUDA
+    thread (64 program blocks resident per SM); an odd one stays unpacked at 4. Same
+    bits as the oracle's tree order and as packing / coarsening off."""
+    from paper_2605_13864_b200 import _lib, codegen
     p = _prog(b2, "reduce_tree_f32.optc")
-    x = np.random.default_rng(9).uniform(-1, 1, 512 * 77).astype(np.float32)
+    x = np.random.default_rng(blocks).uniform(-1, 1, 512 * blocks).astype(np.float32)
     ret, _ = b2.run_program(p, "reduce", {"arr": x.tolist(), "N": x.size}, backend="codegen")
-    assert codegen.compile_fn(p.fn("reduce")).kernel_coarsen()[0] == 4
+    c = codegen.compile_fn(p.fn("reduce"))
+    assert (c.kernel_coarsen()[0], c.kernel_pack()[0]) == (co, pk)
     want, _ = oracle.reduce_f32_tree512(x)
     assert np.float32(ret).view(np.uint32) == np.float32(want).view(np.uint32)
+    prev = _lib.tuning("codegen.pack")
+    _lib.tune("codegen.pack", 1)
+    try:
+        plain, _ = b2.run_program(p, "reduce", {"arr": x.tolist(), "N": x.size}, backend="codegen")
+        assert c.kernel_pack()[0] == 1
+    finally:
+        _lib.tune("codegen.pack", prev)
+    assert np.float32(plain).view(np.uint32) == np.float32(want).view(np.uint32)
+
+
+def test_packing_refused_for_block_dependent_barriers(b2):
+    """A barrier under an `if` on the block index: packed program blocks would disagree
+    on reaching it, so the launch stays one program block per CUDA block (still
+    coarsened), with the interpreter's results."""
+    from paper_2605_13864_b200 import codegen
+    src = """void f(float* a, float* r, int N) {
+    float* const d = gmem_malloc1<float>(N);
+    memcpy_host_to_device1(d, a, N);
+    float* const o = gmem_malloc1<float>(N);
+    {
+        kernel_launch(N / 128, 128, 4 * 128);
+        float* const s = __smem_malloc1<float>(128);
+        kernel_setup_end();
+        thread for (int b = 0; b < N / 128; b++) {
+            thread for (int t = 0; t < 128; t++) { s[DMINDEX1(N / 128, b)][t] = d[b * 128 + t]; }
+            if (b % 2 == 0) {
+                blocksync();
+                thread for (int t = 0; t < 128; t++) { o[b * 128 + t] = s[DMINDEX1(N / 128, b)][127 - t]; }
+            } else {
+                thread for (int t = 0; t < 128; t++) { o[b * 128 + t] = s[DMINDEX1(N / 128, b)][t] * 2.0; }
+            }
+        }
+        kernel_teardown_begin();
+        __smem_free1(s, 128);
+        kernel_kill();
+    }
+    memcpy_device_to_host1(r, o, N);
+    gmem_free(o);
+    gmem_free(d);
+}
+"""
+    p = b2.parse_program(src)
+    n = 128 * 64
+    x = np.arange(n, dtype=np.float32)
+    _, got = b2.run_program(p, "f", {"a": x.tolist(), "r": [0.0] * n, "N": n}, backend="codegen")
+    c = codegen.compile_fn(p.fn("f"))
+    assert c.kernel_unchecked()[0] and c.kernel_pack()[0] == 1
+    blk = x.reshape(-1, 128)
+    want = np.where((np.arange(64) % 2 == 0)[:, None], blk[:, ::-1], blk * 2)
+    assert np.array_equal(np.array(got["r"], np.float32), want.reshape(-1))
 
 
 NOT_COARSENABLE = {

@@ -11,7 +11,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libb200k.so")
-SOURCES = ["capi.cu", "transpose.cu", "transpose_tma.cu", "transpose_any.cu", "transpose_staged.cu", "reduce.cu"]
+SOURCES = ["capi.cu", "transpose.cu", "transpose_tma.cu", "transpose_any.cu", "transpose_staged.cu", "transpose_cpa.cu", "reduce.cu"]
 HEADERS = ["b2_internal.cuh", os.path.join("..", "..", "include", "b2k.h")]
 
 NVCC_FLAGS = [

@@ -60,7 +60,11 @@ struct Tuning {
     int t_staged_stages = 4;  // cp.async ring depth of the staged kernel (2, 3, 4)
     int c_pipe_kb = 65536;  // generated programs: bytes per copy / kernel pipeline step (KiB; 0 = off)
     int l_pdl = 0;          // 1 = launch the hot kernels with programmatic dependent launch
-    int c_coarsen = 4;      // generated programs: largest thread-coarsening factor (1 = off)
+    int c_coarsen = 8;      // generated programs: largest thread-coarsening factor (1 = off; 8 only packed)
+    int c_pack = 2;         // generated programs: most program blocks per CUDA block (1 = off)
+    int t_cpa = 0;          // 1 = cp.async-loaded tiles for aligned transposes (transpose_cpa.cu)
+    int t_cpa_variant = 0;  // tile rows / stages of the cp.async path (see cpa_for)
+    int t_cpa_ctas = 0;     // CTAs per SM of the cp.async path (0 = as many as fit)
 };
 extern Tuning g_tune;
 constexpr int kInflightBytesPerSM = 64 * 1024;
@@ -130,6 +134,8 @@ int launch_transpose_tma(const void *in, void *out, int64_t rows, int64_t cols, 
                          int64_t ld_out, int dev, cudaStream_t st);
 int launch_transpose_any(const void *in, void *out, int64_t rows, int64_t cols, int64_t ld_in,
                          int64_t ld_out, int esize, int dev, cudaStream_t st);
+int launch_transpose_cpa(const void *in, void *out, int64_t rv, int64_t cv, int64_t ld_in, int64_t ld_out,
+                         int esize, int dev, cudaStream_t st);
 int launch_transpose_staged(const void *in, void *out, int64_t rows, int64_t cols, int64_t ld_in,
                             int64_t ld_out, int esize, int dev, cudaStream_t st);
 

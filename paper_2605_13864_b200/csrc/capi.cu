@@ -328,8 +328,12 @@ static int *tune_slot(const char *key) {
     if (k == "codegen.pipe_kb") return &g_tune.c_pipe_kb;
     if (k == "launch.pdl") return &g_tune.l_pdl;
     if (k == "codegen.coarsen") return &g_tune.c_coarsen;
+    if (k == "codegen.pack") return &g_tune.c_pack;
     if (k == "transpose.staged_ctas") return &g_tune.t_staged_ctas;
     if (k == "transpose.staged_stages") return &g_tune.t_staged_stages;
+    if (k == "transpose.cpa") return &g_tune.t_cpa;
+    if (k == "transpose.cpa_variant") return &g_tune.t_cpa_variant;
+    if (k == "transpose.cpa_ctas") return &g_tune.t_cpa_ctas;
     return nullptr;
 }
 

@@ -443,7 +443,8 @@ int dispatch(const void *in, void *out, int64_t rows, int64_t cols, int64_t ld_i
     }
     const int64_t rv = rows - rows % V, cv = cols - cols % V;
     if constexpr (E >= 2) {
-        int rc = run_vec_for<E>(in, out, rv, cv, ld_in, ld_out, dev, st);
+        int rc = g_tune.t_cpa ? launch_transpose_cpa(in, out, rv, cv, ld_in, ld_out, E, dev, st)
+                              : run_vec_for<E>(in, out, rv, cv, ld_in, ld_out, dev, st);
         if (rc) return rc;
     }
     return run_scalar_all<T>(in, out, rows, cols, rv, cv, ld_in, ld_out, dev, st);

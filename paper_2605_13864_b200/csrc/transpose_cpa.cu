@@ -1,0 +1,243 @@
+// cp.async-loaded tiled transpose for sm_100a (16-B aligned bases and pitches).
+//
+// The same permutation as transpose_vec_kernel (transpose.cu; SURVEY A.1 / A.4,
+// PAPER.md:1041-1068), with the load side moved off the register file: every
+// input tile row (512 B = 32 x 16-B chunks) is fetched by one warp-wide
+// `cp.async.cg` straight from L2 into shared memory, into an S-stage ring, so
+// S - 1 tiles per CTA are in flight without holding a single register.
+//
+//   * shared layout: input orientation, row i of the tile at i * 32 chunks, chunk
+//     k stored at slot k ^ ((i / R) & 7) (R = 8 rows, 4 for 8-byte cells). The
+//     cp.async writes of a row are a permutation of its 32 slots (conflict-free);
+//   * stage-out: a warp unit is one chunk column x 64 tile rows; each lane gathers
+//     the cells of one output row segment with scalar LDS at a constant stride (all
+//     rows of a lane share one swizzle; the rows the warp reads at one instruction
+//     hit distinct 16-B bank groups, see Lane below) and writes 32 B with one
+//     256-bit L2-evict-first store (2-byte cells: two 16-B stores into two output
+//     rows) — the LDG path's store side;
+//   * one __syncthreads per tile (the paper's blocksync between the shared-tile
+//     write and the transposed read) also frees the stage the next
+//     cp.async group refills; persistent grid, column-major tile walk as in the
+//     LDG path.
+// Edge cells outside the V-multiple interior are left to the padded scalar tile
+// (transpose.cu), exactly like the LDG path.
+#include "b2_internal.cuh"
+
+namespace b2 {
+namespace {
+
+__device__ __forceinline__ void cpa16(uint32_t saddr, const void *g) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void lds64(uint32_t a, uint32_t &x, uint32_t &y) {
+    asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(x), "=r"(y) : "r"(a));
+}
+// 256-bit store, L2 evict-first (the LDG path's stage-out store, transpose.cu)
+__device__ __forceinline__ void stg256(uint8_t *p, const uint4 &a, const uint4 &b) {
+    asm volatile("st.global.L1::no_allocate.L2::evict_first.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p),
+                 "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
+                 : "memory");
+}
+
+// Per cell width: a warp unit is one 16-B chunk column x 64 tile rows, and every lane
+// assembles two 16-B output vectors from 8 (4-byte, 2-byte cells) or 4 (8-byte cells)
+// shared loads:
+//   4-byte: lane (cw = lane % 4, rg = lane / 4): cell column cw of rows rg*8 .. +7 ->
+//           32 B of one output row (8 x LDS.32);
+//   8-byte: lane (cw = lane % 2, rg = lane / 2): rows rg*4 .. +3 -> 32 B (4 x LDS.64);
+//   2-byte: lane (cwp = lane % 4, rg = lane / 4): the 32-bit word cwp (cell columns
+//           2 cwp, 2 cwp + 1) of rows rg*8 .. +7 -> two output rows of 16 B each
+//           (8 x LDS.32, PRMT split).
+// The lane's rows share one swizzle, and the rows a warp touches at one instruction
+// hit distinct 16-B bank groups: swizzle period R = 8 rows (4 for 8-byte cells).
+template <int E>
+struct Lane {
+    static constexpr int R = E == 8 ? 4 : 8;  // tile rows per lane = swizzle period
+};
+
+// TR input rows x 512 B per tile; NT threads; S stages.
+template <int E, int TR, int NT, int S>
+struct Cpa {
+    static constexpr int V = 16 / E;
+    static constexpr int CH = 32;                 // 16-B chunks per tile row (512 B)
+    static constexpr int TC = CH * V;             // cells per tile row
+    static constexpr int STAGE = TR * CH * 16;    // bytes per stage
+    static constexpr int SMEM = S * STAGE;
+    static constexpr int LOADS = TR * CH / NT;    // cp.async per thread per tile
+    static constexpr int UNITS = CH * (TR / 64);  // warp units (chunk column x 64 rows) per tile
+    static_assert(TR % 64 == 0 && (TR * CH) % NT == 0 && S >= 2, "tile / thread mismatch");
+};
+
+template <int E, int TR, int NT, int S>
+__global__ void __launch_bounds__(NT)
+    transpose_cpa_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, int64_t rows_v,
+                         int64_t cols_v, int64_t ld_in_b, int64_t ld_out_b, int64_t tiles_r, int64_t tiles_c,
+                         int64_t ntiles, int group) {
+    using G = Cpa<E, TR, NT, S>;
+    constexpr int V = G::V, CH = G::CH, TC = G::TC, NW = NT / 32, R = Lane<E>::R;
+    extern __shared__ __align__(128) uint4 smem[];
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    pdl_enter();
+
+    auto origin = [&](int64_t tile, int64_t &r0, int64_t &c0) {
+        const int64_t per_band = (int64_t)group * tiles_c;
+        const int64_t band = tile / per_band, w = tile - band * per_band;
+        const int64_t rows_in_band = min((int64_t)group, tiles_r - band * group);
+        r0 = (band * group + w % rows_in_band) * TR;
+        c0 = (w / rows_in_band) * TC;
+    };
+    auto load = [&](int64_t tile, int stage) {
+        int64_t r0, c0;
+        origin(tile, r0, c0);
+        const uint32_t st = sbase + (uint32_t)(stage * G::STAGE);
+#pragma unroll
+        for (int m = 0; m < G::LOADS; ++m) {
+            const int idx = threadIdx.x + m * NT;
+            const int i = idx / CH, k = idx % CH;  // a warp fetches one 512-B row run
+            const int64_t r = r0 + i, c = c0 + k * V;
+            if (r < rows_v && c < cols_v)
+                cpa16(st + (uint32_t)((i * CH + (k ^ ((i / R) & 7))) * 16), in + r * ld_in_b + c * E);
+        }
+    };
+
+    int64_t t = blockIdx.x;
+#pragma unroll
+    for (int s = 0; s < S - 1; ++s) {
+        const int64_t tl = t + (int64_t)s * gridDim.x;
+        if (tl < ntiles) load(tl, s);
+        cpa_commit();
+    }
+    const bool st256 = ((uintptr_t)out % 32 == 0) && (ld_out_b % 32 == 0);
+    for (int it = 0; t < ntiles; t += gridDim.x, ++it) {
+        cpa_wait<S - 2>();
+        __syncthreads();  // tile `it` visible; the stage read in iteration it - 1 is free
+        {
+            const int64_t tl = t + (int64_t)(S - 1) * gridDim.x;
+            if (tl < ntiles) load(tl, (it + S - 1) % S);
+            cpa_commit();
+        }
+        int64_t r0, c0;
+        origin(t, r0, c0);
+        const uint32_t st = sbase + (uint32_t)((it % S) * G::STAGE);
+#pragma unroll 2
+        for (int u = warp; u < G::UNITS; u += NW) {  // UNITS / NW = 1-4
+            const int kc = u % CH, rb = u / CH;
+            if constexpr (E == 2) {
+                const int cwp = lane & 3, i0 = rb * 64 + (lane >> 2) * 8;
+                const uint32_t a = st + (uint32_t)((i0 * CH + (kc ^ ((i0 / R) & 7))) * 16 + cwp * 4);
+                uint32_t w[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) w[k] = lds32(a + k * CH * 16);
+                const uint4 lo = make_uint4(__byte_perm(w[0], w[1], 0x5410), __byte_perm(w[2], w[3], 0x5410),
+                                            __byte_perm(w[4], w[5], 0x5410), __byte_perm(w[6], w[7], 0x5410));
+                const uint4 hi = make_uint4(__byte_perm(w[0], w[1], 0x7632), __byte_perm(w[2], w[3], 0x7632),
+                                            __byte_perm(w[4], w[5], 0x7632), __byte_perm(w[6], w[7], 0x7632));
+                const int64_t oc = c0 + kc * V + 2 * cwp, orr = r0 + i0;  // oc + 1 < cols_v iff oc < cols_v
+                if (oc < cols_v && orr < rows_v) {
+                    stg_stream(reinterpret_cast<uint4 *>(out + oc * ld_out_b + orr * E), lo);
+                    stg_stream(reinterpret_cast<uint4 *>(out + (oc + 1) * ld_out_b + orr * E), hi);
+                }
+            } else {
+                const int cw = lane % V, i0 = rb * 64 + (lane / V) * R;
+                const uint32_t a = st + (uint32_t)((i0 * CH + (kc ^ ((i0 / R) & 7))) * 16 + cw * E);
+                uint4 p, q;
+                if constexpr (E == 4) {
+                    p = make_uint4(lds32(a), lds32(a + CH * 16), lds32(a + 2 * CH * 16), lds32(a + 3 * CH * 16));
+                    q = make_uint4(lds32(a + 4 * CH * 16), lds32(a + 5 * CH * 16), lds32(a + 6 * CH * 16),
+                                   lds32(a + 7 * CH * 16));
+                } else {
+                    lds64(a, p.x, p.y);
+                    lds64(a + CH * 16, p.z, p.w);
+                    lds64(a + 2 * CH * 16, q.x, q.y);
+                    lds64(a + 3 * CH * 16, q.z, q.w);
+                }
+                const int64_t oc = c0 + kc * V + cw, orr = r0 + i0;  // output row / first column
+                if (oc < cols_v && orr < rows_v) {
+                    uint8_t *d = out + oc * ld_out_b + orr * E;
+                    if (orr + V < rows_v) {
+                        if (st256) stg256(d, p, q);
+                        else {
+                            stg_stream(reinterpret_cast<uint4 *>(d), p);
+                            stg_stream(reinterpret_cast<uint4 *>(d + 16), q);
+                        }
+                    } else {
+                        stg_stream(reinterpret_cast<uint4 *>(d), p);
+                    }
+                }
+            }
+        }
+    }
+    cpa_wait<0>();
+}
+
+template <int E, int TR, int NT, int S>
+int run_cpa(const void *in, void *out, int64_t rv, int64_t cv, int64_t ld_in, int64_t ld_out, int dev,
+            cudaStream_t st) {
+    using G = Cpa<E, TR, NT, S>;
+    const int64_t tiles_r = (rv + TR - 1) / TR, tiles_c = (cv + G::TC - 1) / G::TC;
+    const int64_t ntiles = tiles_r * tiles_c;
+    if (ntiles == 0) return B2_OK;
+    auto kern = transpose_cpa_kernel<E, TR, NT, S>;
+    static std::atomic<int> occ[64];
+    if (occ[dev] == 0) {
+        if (G::SMEM > 48 * 1024)
+            B2_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM));
+        int o = 0;
+        B2_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, NT, G::SMEM));
+        occ[dev] = o > 0 ? o : 1;
+    }
+    const int per_sm = std::min(g_tune.t_cpa_ctas > 0 ? g_tune.t_cpa_ctas : occ[dev].load(), occ[dev].load());
+    const int64_t grid = std::min<int64_t>(ntiles, (int64_t)num_sms(dev) * per_sm);
+    // same walk rule as the LDG path (transpose.cu run_vec): column-major when a
+    // column block holds about as many tiles as there are resident CTAs
+    const bool colwalk = tiles_r * 4 >= (int64_t)num_sms(dev) * 3;
+    const int grp = g_tune.t_group > 0 ? g_tune.t_group
+                                       : colwalk ? (int)std::min<int64_t>(tiles_r, 1 << 30) : 1;
+    const int group = (int)std::max<int64_t>(1, std::min<int64_t>(grp, tiles_r));
+    B2_CUDA(launch_kernel(kern, dim3((unsigned)grid), dim3(NT), G::SMEM, st, (const uint8_t *)in, (uint8_t *)out,
+                          rv, cv, ld_in * E, ld_out * E, tiles_r, tiles_c, ntiles, group));
+    count_launch();
+    return B2_OK;
+}
+
+// g_tune.t_cpa_variant (tile rows, threads, stages; shared memory -> CTAs per SM):
+//   0: 64, 256, 4 (128 KB, 1)    1: 64, 512, 4 (128 KB, 1)    2: 64, 512, 3 (96 KB, 2)
+//   3: 128, 512, 2 (128 KB, 1)   4: 128, 1024, 2 (128 KB, 1)  5: 64, 256, 3 (96 KB, 2)
+//   6: 64, 1024, 3 (96 KB, 2)
+template <int E>
+int cpa_for(const void *in, void *out, int64_t rv, int64_t cv, int64_t ld_in, int64_t ld_out, int dev,
+            cudaStream_t st) {
+    switch (g_tune.t_cpa_variant) {
+    case 1: return run_cpa<E, 64, 512, 4>(in, out, rv, cv, ld_in, ld_out, dev, st);
+    case 2: return run_cpa<E, 64, 512, 3>(in, out, rv, cv, ld_in, ld_out, dev, st);
+    case 3: return run_cpa<E, 128, 512, 2>(in, out, rv, cv, ld_in, ld_out, dev, st);
+    case 4: return run_cpa<E, 128, 1024, 2>(in, out, rv, cv, ld_in, ld_out, dev, st);
+    case 5: return run_cpa<E, 64, 256, 3>(in, out, rv, cv, ld_in, ld_out, dev, st);
+    case 6: return run_cpa<E, 64, 1024, 3>(in, out, rv, cv, ld_in, ld_out, dev, st);
+    default: return run_cpa<E, 64, 256, 4>(in, out, rv, cv, ld_in, ld_out, dev, st);
+    }
+}
+
+}  // namespace
+
+int launch_transpose_cpa(const void *in, void *out, int64_t rv, int64_t cv, int64_t ld_in, int64_t ld_out,
+                         int esize, int dev, cudaStream_t st) {
+    switch (esize) {
+    case 2: return cpa_for<2>(in, out, rv, cv, ld_in, ld_out, dev, st);
+    case 4: return cpa_for<4>(in, out, rv, cv, ld_in, ld_out, dev, st);
+    case 8: return cpa_for<8>(in, out, rv, cv, ld_in, ld_out, dev, st);
+    default: return fail(B2_ERR_UNSUPPORTED, "cp.async transpose: cell width must be 2, 4 or 8 bytes");
+    }
+}
+
+}  // namespace b2

@@ -106,6 +106,22 @@ def workload_name(args, world):
             f"(global, strong scaling: row blocks / shards over {world} GPU{'s' if world > 1 else ''})")
 
 
+def transpose_kernel_label(rows, cols):
+    """The kernel the library dispatches for an aligned fp32 rows x cols transpose
+    (transpose.cu dispatch / transpose_cpa.cu transpose_cpa_wanted, at the knob values
+    this process runs with)."""
+    from paper_2605_13864_b200 import _lib
+    cpa, sms = _lib.tuning("transpose.cpa"), 148
+    if cpa == 2 or (cpa == 1 and rows * cols * 4 > 256 << 20 and (rows // 256) * (cols // 64) >= 2 * sms):
+        if cpa == 2:
+            return f"transpose_cpa_kernel variant {_lib.tuning('transpose.cpa_variant')} (forced)"
+        return ("transpose_cpa_kernel<4,256,16,256,2,1> (cp.async-loaded 256x64 fp32 tiles, "
+                "2 x 64-KB stages, L2 evict-first loads, 1 CTA/SM)")
+    if (rows // 256) * (cols // 128) >= 8 * sms:
+        return "transpose_vec_kernel<4,64,32,512> (256x128 fp32 tile, 1 CTA/SM)"
+    return "transpose_vec_kernel<4,16,16,256> (64x64 fp32 tile)"
+
+
 def config_for(args, world):
     """The workload config, identical in both arms (the driver compares them)."""
     return {"workload": workload_name(args, world), "rows": args.rows, "cols": args.cols, "n": args.n,
@@ -532,9 +548,7 @@ def main():
                     " of the int64 partial" if world > 1 else "none (1 GPU)"),
         "combine_note": combine_note,
         "roofline": {"bound": "hbm",
-                     "kernel": ("transpose_vec_kernel<4,64,32,512> (256x128 fp32 tile, 1 CTA/SM)"
-                                if (rows // 256) * (cols // 128) >= 8 * 148 else
-                                "transpose_vec_kernel<4,16,16,256> (64x64 fp32 tile)"),
+                     "kernel": transpose_kernel_label(rows, cols),
                      "achieved": ach_t, "peak": peak, "unit": "GB/s", "frac": ach_t / peak,
                      "traffic": traffic, "algorithmic_bytes": bytes_t, "peak_source": peak_src,
                      "frac_nominal_8TBs": ach_t / NOMINAL_HBM},

@@ -62,9 +62,11 @@ struct Tuning {
     int l_pdl = 0;          // 1 = launch the hot kernels with programmatic dependent launch
     int c_coarsen = 8;      // generated programs: largest thread-coarsening factor (1 = off; 8 only packed)
     int c_pack = 2;         // generated programs: most program blocks per CUDA block (1 = off)
-    int t_cpa = 0;          // 1 = cp.async-loaded tiles for aligned transposes (transpose_cpa.cu)
-    int t_cpa_variant = 0;  // tile rows / stages of the cp.async path (see cpa_for)
+    int t_cpa = 1;          // cp.async-loaded tiles for aligned transposes (transpose_cpa.cu): 1 = auto
+                            // (large interiors), 2 = always (geometry t_cpa_variant), 0 = LDG path only
+    int t_cpa_variant = 0;  // tile geometry of the forced cp.async path (see cpa_for)
     int t_cpa_ctas = 0;     // CTAs per SM of the cp.async path (0 = as many as fit)
+    int t_cpa_hint = 1;     // cp.async L2 hint of the auto geometry: 1 = evict-first policy, 0 = none, 2 = 256-B prefetch
 };
 extern Tuning g_tune;
 constexpr int kInflightBytesPerSM = 64 * 1024;
@@ -136,6 +138,7 @@ int launch_transpose_any(const void *in, void *out, int64_t rows, int64_t cols, 
                          int64_t ld_out, int esize, int dev, cudaStream_t st);
 int launch_transpose_cpa(const void *in, void *out, int64_t rv, int64_t cv, int64_t ld_in, int64_t ld_out,
                          int esize, int dev, cudaStream_t st);
+bool transpose_cpa_wanted(int64_t rv, int64_t cv, int esize, int dev);
 int launch_transpose_staged(const void *in, void *out, int64_t rows, int64_t cols, int64_t ld_in,
                             int64_t ld_out, int esize, int dev, cudaStream_t st);
 

@@ -334,6 +334,7 @@ static int *tune_slot(const char *key) {
     if (k == "transpose.cpa") return &g_tune.t_cpa;
     if (k == "transpose.cpa_variant") return &g_tune.t_cpa_variant;
     if (k == "transpose.cpa_ctas") return &g_tune.t_cpa_ctas;
+    if (k == "transpose.cpa_hint") return &g_tune.t_cpa_hint;
     return nullptr;
 }
 

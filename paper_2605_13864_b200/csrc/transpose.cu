@@ -5,7 +5,11 @@
 // the W x H transpose of the H x W input, a pure permutation, bit-exact for every
 // element width.
 //
-// Vector path (16-B aligned pitches, the HBM-bound hot path):
+// Large aligned matrices (the C4 hot path) go to the cp.async-loaded tiles of
+// transpose_cpa.cu since round 2; this file's register-staged vector path serves the
+// smaller aligned ones (and every size with transpose.cpa = 0).
+//
+// Vector path (16-B aligned pitches):
 //   * each thread owns V x V "micro-tiles" (V = 16 / sizeof(elem)): V 128-bit
 //     coalesced loads from V consecutive input rows, an in-register V x V
 //     transpose (PRMT byte permutes for 2-byte cells), then V 128-bit stores into
@@ -443,8 +447,10 @@ int dispatch(const void *in, void *out, int64_t rows, int64_t cols, int64_t ld_i
     }
     const int64_t rv = rows - rows % V, cv = cols - cols % V;
     if constexpr (E >= 2) {
-        int rc = g_tune.t_cpa ? launch_transpose_cpa(in, out, rv, cv, ld_in, ld_out, E, dev, st)
-                              : run_vec_for<E>(in, out, rv, cv, ld_in, ld_out, dev, st);
+        // aligned interior: cp.async-loaded tiles (transpose_cpa.cu) on large matrices,
+        // register-staged LDG tiles below (and with transpose.cpa = 0)
+        int rc = transpose_cpa_wanted(rv, cv, E, dev) ? launch_transpose_cpa(in, out, rv, cv, ld_in, ld_out, E, dev, st)
+                                                      : run_vec_for<E>(in, out, rv, cv, ld_in, ld_out, dev, st);
         if (rc) return rc;
     }
     return run_scalar_all<T>(in, out, rows, cols, rv, cv, ld_in, ld_out, dev, st);

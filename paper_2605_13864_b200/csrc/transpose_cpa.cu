@@ -26,8 +26,15 @@
 namespace b2 {
 namespace {
 
-__device__ __forceinline__ void cpa16(uint32_t saddr, const void *g) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g) : "memory");
+template <int H>
+__device__ __forceinline__ void cpa16(uint32_t saddr, const void *g, uint64_t pol) {
+    if constexpr (H == 1)  // L2 evict-first policy (read-once input)
+        asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(saddr), "l"(g), "l"(pol)
+                     : "memory");
+    else if constexpr (H == 2)  // 256-B L2 prefetch
+        asm volatile("cp.async.cg.shared.global.L2::256B [%0], [%1], 16;" ::"r"(saddr), "l"(g) : "memory");
+    else
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g) : "memory");
 }
 __device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
@@ -64,29 +71,31 @@ struct Lane {
     static constexpr int R = E == 8 ? 4 : 8;  // tile rows per lane = swizzle period
 };
 
-// TR input rows x 512 B per tile; NT threads; S stages.
-template <int E, int TR, int NT, int S>
+// TR input rows x CH 16-B chunks per tile; NT threads; S stages.
+template <int E, int TR, int CH_, int NT, int S>
 struct Cpa {
     static constexpr int V = 16 / E;
-    static constexpr int CH = 32;                 // 16-B chunks per tile row (512 B)
+    static constexpr int CH = CH_;                // 16-B chunks per tile row (256 or 512 B)
     static constexpr int TC = CH * V;             // cells per tile row
     static constexpr int STAGE = TR * CH * 16;    // bytes per stage
     static constexpr int SMEM = S * STAGE;
     static constexpr int LOADS = TR * CH / NT;    // cp.async per thread per tile
     static constexpr int UNITS = CH * (TR / 64);  // warp units (chunk column x 64 rows) per tile
-    static_assert(TR % 64 == 0 && (TR * CH) % NT == 0 && S >= 2, "tile / thread mismatch");
+    static_assert(TR % 64 == 0 && (TR * CH) % NT == 0 && S >= 2 && CH % 8 == 0, "tile / thread mismatch");
 };
 
-template <int E, int TR, int NT, int S>
+template <int E, int TR, int CH_, int NT, int S, int H>
 __global__ void __launch_bounds__(NT)
     transpose_cpa_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, int64_t rows_v,
                          int64_t cols_v, int64_t ld_in_b, int64_t ld_out_b, int64_t tiles_r, int64_t tiles_c,
                          int64_t ntiles, int group) {
-    using G = Cpa<E, TR, NT, S>;
+    using G = Cpa<E, TR, CH_, NT, S>;
     constexpr int V = G::V, CH = G::CH, TC = G::TC, NW = NT / 32, R = Lane<E>::R;
     extern __shared__ __align__(128) uint4 smem[];
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint64_t pol = 0;
+    if constexpr (H == 1) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
     pdl_enter();
 
     auto origin = [&](int64_t tile, int64_t &r0, int64_t &c0) {
@@ -103,10 +112,10 @@ __global__ void __launch_bounds__(NT)
 #pragma unroll
         for (int m = 0; m < G::LOADS; ++m) {
             const int idx = threadIdx.x + m * NT;
-            const int i = idx / CH, k = idx % CH;  // a warp fetches one 512-B row run
+            const int i = idx / CH, k = idx % CH;  // a warp fetches 512 B of row runs
             const int64_t r = r0 + i, c = c0 + k * V;
             if (r < rows_v && c < cols_v)
-                cpa16(st + (uint32_t)((i * CH + (k ^ ((i / R) & 7))) * 16), in + r * ld_in_b + c * E);
+                cpa16<H>(st + (uint32_t)((i * CH + (k ^ ((i / R) & 7))) * 16), in + r * ld_in_b + c * E, pol);
         }
     };
 
@@ -180,14 +189,14 @@ __global__ void __launch_bounds__(NT)
     cpa_wait<0>();
 }
 
-template <int E, int TR, int NT, int S>
+template <int E, int TR, int CH, int NT, int S, int H>
 int run_cpa(const void *in, void *out, int64_t rv, int64_t cv, int64_t ld_in, int64_t ld_out, int dev,
             cudaStream_t st) {
-    using G = Cpa<E, TR, NT, S>;
+    using G = Cpa<E, TR, CH, NT, S>;
     const int64_t tiles_r = (rv + TR - 1) / TR, tiles_c = (cv + G::TC - 1) / G::TC;
     const int64_t ntiles = tiles_r * tiles_c;
     if (ntiles == 0) return B2_OK;
-    auto kern = transpose_cpa_kernel<E, TR, NT, S>;
+    auto kern = transpose_cpa_kernel<E, TR, CH, NT, S, H>;
     static std::atomic<int> occ[64];
     if (occ[dev] == 0) {
         if (G::SMEM > 48 * 1024)
@@ -210,25 +219,66 @@ int run_cpa(const void *in, void *out, int64_t rv, int64_t cv, int64_t ld_in, in
     return B2_OK;
 }
 
-// g_tune.t_cpa_variant (tile rows, threads, stages; shared memory -> CTAs per SM):
-//   0: 64, 256, 4 (128 KB, 1)    1: 64, 512, 4 (128 KB, 1)    2: 64, 512, 3 (96 KB, 2)
-//   3: 128, 512, 2 (128 KB, 1)   4: 128, 1024, 2 (128 KB, 1)  5: 64, 256, 3 (96 KB, 2)
-//   6: 64, 1024, 3 (96 KB, 2)
+// Geometry. Auto (transpose.cpa = 1): 256 x 256-B tiles, 256 threads, 2 stages for 4-
+// and 8-byte cells; 128 x 256-B tiles, 512 threads, 4 stages for 2-byte cells
+// (profiles/r02k_cpa.md: two 64-KB stages, i.e. one tile loading while one drains,
+// measured best for 4 / 8-byte cells, the ~64 KB in flight per SM of the LDG path's
+// residency rule; 2-byte cells keep more in flight). The 4 / 8-byte loads carry an
+// L2 evict-first policy (transpose.cpa_hint = 1, default: the input is read once; in
+// the bench step that took the transpose + sum from 0.9 % behind the LDG path to
+// 0.2-0.5 % ahead, the following reduction included); 0 = no hint, 2 = a 256-B L2
+// prefetch hint (slower). transpose.cpa = 2 takes g_tune.t_cpa_variant (tile
+// rows x row bytes, threads, stages; shared memory), always with the evict-first hint:
+//   0: 256 x 256 B, 512, 2 (128 KB)  1: 128 x 512 B, 512, 2 (128 KB)
+//   2: 256 x 256 B, 256, 2 (128 KB)  3: 256 x 256 B, 1024, 2 (128 KB)
+//   4: 384 x 256 B, 512, 2 (192 KB)  5: 128 x 256 B, 512, 4 (128 KB)
+//   6: 512 x 128 B, 512, 2 (128 KB)  7: 448 x 256 B, 512, 2 (224 KB)
+//   8: 256 x 256 B, 128, 2 (128 KB)  9: 192 x 256 B, 256, 2 (96 KB)
+template <int E, int H>
+int cpa_auto(const void *in, void *out, int64_t rv, int64_t cv, int64_t ld_in, int64_t ld_out, int dev,
+             cudaStream_t st) {
+    if constexpr (E == 2) return run_cpa<E, 128, 16, 512, 4, H>(in, out, rv, cv, ld_in, ld_out, dev, st);
+    else return run_cpa<E, 256, 16, 256, 2, H>(in, out, rv, cv, ld_in, ld_out, dev, st);
+}
+
 template <int E>
 int cpa_for(const void *in, void *out, int64_t rv, int64_t cv, int64_t ld_in, int64_t ld_out, int dev,
             cudaStream_t st) {
+    if (g_tune.t_cpa != 2) {
+        // the evict-first hint pays for 4 / 8-byte cells; the 2-byte geometry's four
+        // stages measured 11 % slower with it (r02k_cpa.md), so 2-byte loads go unhinted
+        if (g_tune.t_cpa_hint == 0 || E == 2) return cpa_auto<E, 0>(in, out, rv, cv, ld_in, ld_out, dev, st);
+        if (g_tune.t_cpa_hint == 2) return cpa_auto<E, 2>(in, out, rv, cv, ld_in, ld_out, dev, st);
+        return cpa_auto<E, 1>(in, out, rv, cv, ld_in, ld_out, dev, st);
+    }
     switch (g_tune.t_cpa_variant) {
-    case 1: return run_cpa<E, 64, 512, 4>(in, out, rv, cv, ld_in, ld_out, dev, st);
-    case 2: return run_cpa<E, 64, 512, 3>(in, out, rv, cv, ld_in, ld_out, dev, st);
-    case 3: return run_cpa<E, 128, 512, 2>(in, out, rv, cv, ld_in, ld_out, dev, st);
-    case 4: return run_cpa<E, 128, 1024, 2>(in, out, rv, cv, ld_in, ld_out, dev, st);
-    case 5: return run_cpa<E, 64, 256, 3>(in, out, rv, cv, ld_in, ld_out, dev, st);
-    case 6: return run_cpa<E, 64, 1024, 3>(in, out, rv, cv, ld_in, ld_out, dev, st);
-    default: return run_cpa<E, 64, 256, 4>(in, out, rv, cv, ld_in, ld_out, dev, st);
+    case 1: return run_cpa<E, 128, 32, 512, 2, 1>(in, out, rv, cv, ld_in, ld_out, dev, st);
+    case 2: return run_cpa<E, 256, 16, 256, 2, 1>(in, out, rv, cv, ld_in, ld_out, dev, st);
+    case 3: return run_cpa<E, 256, 16, 1024, 2, 1>(in, out, rv, cv, ld_in, ld_out, dev, st);
+    case 4: return run_cpa<E, 384, 16, 512, 2, 1>(in, out, rv, cv, ld_in, ld_out, dev, st);
+    case 5: return run_cpa<E, 128, 16, 512, 4, 1>(in, out, rv, cv, ld_in, ld_out, dev, st);
+    case 6: return run_cpa<E, 512, 8, 512, 2, 1>(in, out, rv, cv, ld_in, ld_out, dev, st);
+    case 7: return run_cpa<E, 448, 16, 512, 2, 1>(in, out, rv, cv, ld_in, ld_out, dev, st);
+    case 8: return run_cpa<E, 256, 16, 128, 2, 1>(in, out, rv, cv, ld_in, ld_out, dev, st);
+    case 9: return run_cpa<E, 192, 16, 256, 2, 1>(in, out, rv, cv, ld_in, ld_out, dev, st);
+    default: return run_cpa<E, 256, 16, 512, 2, 1>(in, out, rv, cv, ld_in, ld_out, dev, st);
     }
 }
 
 }  // namespace
+
+// Default dispatch (transpose.cpa = 1): the cp.async path takes aligned interiors
+// whose input exceeds twice the 126-MB L2 (it measured level with or ahead of the LDG
+// path there: fp32 32768^2 +0.6 %, 32000x32008 +1.5 %, bf16 32768x65536 +2.5 %;
+// profiles/r02k_cpa.md) and that hold at least two tiles per SM; smaller ones (fp32
+// 4096^2: -1.3 %; C1 1024^2: 64 tiles) keep the LDG path's tiles. transpose.cpa = 2
+// forces it, 0 disables it.
+bool transpose_cpa_wanted(int64_t rv, int64_t cv, int esize, int dev) {
+    if (g_tune.t_cpa == 0) return false;
+    if (g_tune.t_cpa == 2) return true;
+    const int64_t tr = esize == 2 ? 128 : 256, tc = 256 / esize;  // auto tiles: rows x 256-B rows
+    return rv * cv * esize > (int64_t(256) << 20) && (rv / tr) * (cv / tc) >= 2 * (int64_t)num_sms(dev);
+}
 
 int launch_transpose_cpa(const void *in, void *out, int64_t rv, int64_t cv, int64_t ld_in, int64_t ld_out,
                          int esize, int dev, cudaStream_t st) {

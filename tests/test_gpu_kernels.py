@@ -66,6 +66,37 @@ def test_transpose_sweep(b2, shape, dt):
     assert np.array_equal(got, ref)
 
 
+LOAD_SHAPES = [(64, 64), (256, 64), (300, 520), (4100, 4104), (1024, 2048), (8192, 1032), (520, 4096), (72, 9000)]
+
+
+@pytest.mark.parametrize("setting", [(0, 0), (1, 0)] + [(2, v) for v in range(10)])
+@pytest.mark.parametrize("dt", [torch.bfloat16, torch.float32, torch.float64])
+def test_transpose_load_paths(b2, setting, dt):
+    """Aligned interiors through every load path: the register-staged LDG tiles
+    (transpose.cpa = 0), the default auto dispatch, and every cp.async geometry forced
+    (transpose.cpa = 2): ragged tiles, pitched views whose neighbours must stay untouched;
+    bit-exact against torch's transpose."""
+    from paper_2605_13864_b200 import _lib
+    cpa, variant = setting
+    iv = {torch.bfloat16: torch.int16, torch.float32: torch.int32, torch.float64: torch.int64}[dt]
+    _lib.tune("transpose.cpa", cpa)
+    _lib.tune("transpose.cpa_variant", variant)
+    try:
+        for (r, c) in LOAD_SHAPES:
+            g = torch.Generator(device="cuda").manual_seed(r * 31 + c)
+            a = torch.randn((r, c), device="cuda", generator=g).to(dt)
+            assert torch.equal(b2.transpose(a).view(iv), a.t().contiguous().view(iv)), (r, c)
+            base = torch.randn((r, c + 32), device="cuda", generator=g).to(dt)
+            view = base[:, 16:16 + c]  # pitch c + 32, 16-B aligned start for every width
+            outb = torch.full((c, (r + 64 + 7) // 8 * 8), -7.0, device="cuda").to(dt)  # 16-B pitch
+            b2.transpose(view, outb[:, 32:32 + r])
+            assert torch.equal(outb[:, 32:32 + r].view(iv), view.t().contiguous().view(iv)), (r, c)
+            assert bool((outb[:, :32] == -7).all()) and bool((outb[:, 32 + r:] == -7).all())
+    finally:
+        _lib.tune("transpose.cpa", 1)
+        _lib.tune("transpose.cpa_variant", 0)
+
+
 def test_transpose_pitched(b2):
     base = torch.arange(300 * 520, device="cuda", dtype=torch.float32).reshape(300, 520)
     view = base[:, 8:508]  # pitch 520, 16-B aligned start

@@ -1,6 +1,7 @@
 """Static SASS properties of the built library (no GPU needed: cuobjdump of the
 in-tree libb200k.so): the default kernels keep their 128-bit loads, 256-bit
 evict-first stores and swizzled 128-bit shared-memory traffic, and nothing spills."""
+import re
 import os
 import shutil
 import subprocess
@@ -44,6 +45,18 @@ def test_bench_transpose_vector_memory_ops(table):
         b = _body(table, k)
         assert "LDG.E.NA.128" in b and ".EFL2.256" in b, k
         assert "STS.128" in b and "LDS.128" in b, k
+
+
+def test_cpa_transpose_async_copies(table):
+    """The default large-matrix transpose (transpose_cpa.cu): tiles land in shared
+    memory by cp.async (LDGSTS, no register staging), one barrier per tile, scalar
+    conflict-free gathers, 256-bit evict-first stores; every cell width."""
+    for k in ("transpose_cpa_kernel<4, 256, 16, 256, 2, 1>", "transpose_cpa_kernel<8, 256, 16, 256, 2, 1>",
+              "transpose_cpa_kernel<2, 128, 16, 512, 4, 1>"):
+        b = _body(table, k)
+        assert "LDGSTS.E.BYPASS.128" in b and "LDGDEPBAR" in b and "DEPBAR.LE" in b, k
+        assert "BAR.SYNC" in b and "LDS" in b and not re.search(r"\bSTS\b", b) and "LDG.E" not in b, k
+        assert ".EFL2.256" in b or k.startswith("transpose_cpa_kernel<2"), k
 
 
 def test_reduce_vector_loads_and_shuffles(table):

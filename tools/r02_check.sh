@@ -10,6 +10,4 @@ B2K_PARITY_LOG=$PWD/gpurun_out/fp32_parity.jsonl timeout 1800 python -m pytest t
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
 timeout 900 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo "ref rc=$?" >> gpurun_out/bench_ref.err
 timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?" >> gpurun_out/bench.err
-[ -d abtest ] && timeout 900 bash tools/ab_bench.sh > gpurun_out/ab_bench.txt 2>&1
-timeout 600 ncu --metrics gpu__time_duration.sum,l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum,l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_st.sum,l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --kernel-name-base demangled -k "regex:transpose_vec_kernel" -c 2 --log-file gpurun_out/ncu_conflicts.csv python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --no-graph > gpurun_out/ncu_conflicts.log 2>&1
-tail -3 gpurun_out/pytest_gpu.log; tail -2 gpurun_out/smoke.log; tail -1 gpurun_out/bench_ref.err; tail -1 gpurun_out/bench.err; cat gpurun_out/ab_bench.txt
+timeout 600 ncu --metrics gpu__time_duration.sum,l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum,l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_st.sum,l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --kernel-name-base demangled -k "regex:transpose_(vec|cpa)_kernel" -c 2 --log-file gpurun_out/ncu_conflicts.csv python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --no-graph > gpurun_out/ncu_conflicts.log 2>&1

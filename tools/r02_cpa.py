@@ -29,14 +29,17 @@ def timeit(fn, reps=10):
     return statistics.median(ts)
 
 
-SETTINGS = [("ldg", {})] + [(f"cpa{v}", {"transpose.cpa": 1, "transpose.cpa_variant": v}) for v in range(7)]
+SETTINGS = [("ldg", {"transpose.cpa": 0}), ("auto", {"transpose.cpa": 1}),
+            ("auto_nohint", {"transpose.cpa": 1, "transpose.cpa_hint": 0})] + \
+    [(f"cpa{v}", {"transpose.cpa": 2, "transpose.cpa_variant": v}) for v in range(10)]
 if len(sys.argv) > 1:
     SETTINGS = [s for s in SETTINGS if s[0] in sys.argv[1].split(",")]
 
 
 def apply(knobs):
-    _lib.tune("transpose.cpa", 0)
+    _lib.tune("transpose.cpa", 1)
     _lib.tune("transpose.cpa_variant", 0)
+    _lib.tune("transpose.cpa_hint", 1)
     for k, v in knobs.items():
         _lib.tune(k, v)
 

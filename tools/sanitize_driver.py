@@ -126,6 +126,16 @@ def run_transpose(rng):
     one_transpose(520, 300, np.float32, rng)
     one_transpose(600, 130, np.float64, rng)
     tune("transpose.big", 1)
+    # cp.async-loaded tiles (the default on large matrices; forced here, every geometry,
+    # every cell width, ragged tiles, pitched / offset views)
+    tune("transpose.cpa", 2)
+    for v in range(10):
+        tune("transpose.cpa_variant", v)
+        one_transpose(520, 300, np.float32, rng, pad_in=4, pad_out=8)
+        one_transpose(264, 136, np.uint16, rng, pad_in=8)
+        one_transpose(200, 70, np.float64, rng, pad_out=2)
+    tune("transpose.cpa_variant", 0)
+    tune("transpose.cpa", 1)
     # TMA-staged variants: 1 = UTMALDG/UTMASTG + mbarrier ring; 2 = TMA-loaded
     # input stages, register transpose, direct stores (all stage counts)
     tune("transpose.tma", 1)

@@ -78,7 +78,26 @@ struct DevCtx {
     unsigned long long mb_epoch = 0;
 };
 
-DevCtx g_ctx[64];
+// Per device: kLanes independent pipeline contexts ("lanes": streams, events, stage
+// buffers, workspace). Lane 0 also owns the device-wide state (the workspace lent to
+// ws == NULL callers, the multi-GPU slots and mailbox); the host-buffer pipelines take
+// any free lane, so concurrent calls from several host threads (a transpose and a
+// reduction) overlap their PCIe traffic instead of serialising on one context.
+constexpr int kLanes = 2;
+DevCtx g_lanes[64][kLanes];
+#define g_ctx_of(dev) (g_lanes[dev][0])
+
+struct Lane {
+    DevCtx *c;
+    std::unique_lock<std::mutex> lock;
+};
+Lane acquire_lane(int dev) {
+    for (int i = 0; i < kLanes; ++i) {
+        std::unique_lock<std::mutex> l(g_lanes[dev][i].mu, std::try_to_lock);
+        if (l.owns_lock()) return {&g_lanes[dev][i], std::move(l)};
+    }
+    return {&g_lanes[dev][0], std::unique_lock<std::mutex>(g_lanes[dev][0].mu)};
+}
 
 int check_dev(int dev) {
     static std::atomic<int> s_count{-1};
@@ -202,8 +221,10 @@ class CopyPool {
         for (auto &t : th_) t.join();
     }
     int size() const { return (int)th_.size() + 1; }
-    // run f(part) for part in [0, size()); the caller runs part 0
+    // run f(part) for part in [0, size()); the caller runs part 0. One job at a time:
+    // concurrent submitters (pipelines on several lanes / devices) queue here.
     void run(const std::function<void(int)> &f) {
+        std::lock_guard<std::mutex> one(submit_);
         {
             std::lock_guard<std::mutex> g(m_);
             job_ = &f;
@@ -237,7 +258,7 @@ class CopyPool {
         }
     }
     std::vector<std::thread> th_;
-    std::mutex m_;
+    std::mutex submit_, m_;
     std::condition_variable cv_, done_;
     const std::function<void(int)> *job_ = nullptr;
     int pending_ = 0;
@@ -400,7 +421,7 @@ int b2_reduce_sum(const void *in, int64_t n, int dtype, void *out, void *ws, siz
     if ((!in && n) || !out) return fail(B2_ERR_INVALID, "reduce: NULL buffer");
     if (int rc = check_dev(dev)) return rc;
     if (!ws) {
-        DevCtx &c = g_ctx[dev];
+        DevCtx &c = g_ctx_of(dev);
         std::lock_guard<std::mutex> g(c.mu);
         if (int rc = ctx_init(c, dev)) return rc;
         ws = c.ws;
@@ -436,7 +457,7 @@ int b2_reduce_tree(const float *in, int64_t n, int block, float *result_host, in
     if (!in || !result_host) return fail(B2_ERR_INVALID, "tree: NULL buffer");
     if (int rc = tree_args(n, block)) return rc;
     if (int rc = check_dev(dev)) return rc;
-    DevCtx &c = g_ctx[dev];
+    DevCtx &c = g_ctx_of(dev);
     std::lock_guard<std::mutex> g(c.mu);
     if (int rc = ctx_init(c, dev)) return rc;
     const int64_t nb = n / block;
@@ -462,8 +483,8 @@ int b2_reduce_tree_host(const float *in_host, int64_t n, int block, float *resul
     if (!in_host || !result_host) return fail(B2_ERR_INVALID, "tree: NULL buffer");
     if (int rc = tree_args(n, block)) return rc;
     if (int rc = check_dev(dev)) return rc;
-    DevCtx &c = g_ctx[dev];
-    std::lock_guard<std::mutex> g(c.mu);
+    Lane lane = acquire_lane(dev);  // any free pipeline lane of the device
+    DevCtx &c = *lane.c;
     if (int rc = ctx_init(c, dev)) return rc;
     int64_t ce = (int64_t)(chunk_bytes() / sizeof(float));
     ce -= ce % block;
@@ -552,7 +573,7 @@ int b2_reduce_sum_fused(const void *in, int64_t n, int dtype, void *out, void *w
     if ((!in && n) || !out || !mailbox) return fail(B2_ERR_INVALID, "reduce: NULL buffer");
     if (int rc = check_dev(dev)) return rc;
     if (!ws) {
-        DevCtx &c = g_ctx[dev];
+        DevCtx &c = g_ctx_of(dev);
         std::lock_guard<std::mutex> g(c.mu);
         if (int rc = ctx_init(c, dev)) return rc;
         ws = c.ws;
@@ -644,8 +665,8 @@ int b2_pipe_run(int nsteps, const b2_copy2d *h2d, const int64_t *h2d_off, const 
         return fail(B2_ERR_INVALID, "pipe: bad arguments");
     if (nsteps == 0) return B2_OK;
     if (int rc = check_dev(dev)) return rc;
-    DevCtx &c = g_ctx[dev];
-    std::lock_guard<std::mutex> g(c.mu);
+    Lane lane = acquire_lane(dev);  // any free pipeline lane of the device
+    DevCtx &c = *lane.c;
     if (int rc = ctx_init(c, dev)) return rc;
     auto bytes = [](const b2_copy2d &x) { return (size_t)x.width * (size_t)x.height; };
     // pinned or pageable, per copy; the largest per-step pageable volume sizes the ring
@@ -772,8 +793,8 @@ int b2_copy_h2d(void *dst_dev, const void *src_host, size_t bytes, int dev) {
     if (!bytes) return B2_OK;
     if (!dst_dev || !src_host) return fail(B2_ERR_INVALID, "copy: NULL buffer");
     if (int rc = check_dev(dev)) return rc;
-    DevCtx &c = g_ctx[dev];
-    std::lock_guard<std::mutex> g(c.mu);
+    Lane lane = acquire_lane(dev);  // any free pipeline lane of the device
+    DevCtx &c = *lane.c;
     if (int rc = ctx_init(c, dev)) return rc;
     // like cudaMemcpy: ordered after the work already queued on the legacy default
     // stream (our copy streams are non-blocking, so this is explicit)
@@ -799,8 +820,8 @@ int b2_copy_d2h(void *dst_host, const void *src_dev, size_t bytes, int dev) {
     if (!bytes) return B2_OK;
     if (!dst_host || !src_dev) return fail(B2_ERR_INVALID, "copy: NULL buffer");
     if (int rc = check_dev(dev)) return rc;
-    DevCtx &c = g_ctx[dev];
-    std::lock_guard<std::mutex> g(c.mu);
+    Lane lane = acquire_lane(dev);  // any free pipeline lane of the device
+    DevCtx &c = *lane.c;
     if (int rc = ctx_init(c, dev)) return rc;
     B2_CUDA(cudaEventRecord(c.ev_legacy, cudaStreamLegacy));  // see b2_copy_h2d
     B2_CUDA(cudaStreamWaitEvent(c.s_d2h, c.ev_legacy, 0));
@@ -842,8 +863,8 @@ int b2_transpose_host(const void *in_host, void *out_host, int64_t rows, int64_t
     if (ld_in < cols || ld_out < rows)
         return fail(B2_ERR_INVALID, "transpose: pitch smaller than row length");
     if (int rc = check_dev(dev)) return rc;
-    DevCtx &c = g_ctx[dev];
-    std::lock_guard<std::mutex> g(c.mu);
+    Lane lane = acquire_lane(dev);  // any free pipeline lane of the device
+    DevCtx &c = *lane.c;
     if (int rc = ctx_init(c, dev)) return rc;
     // Chunk = a cr x cc block of the input -> a cc x cr block of the output, both
     // moved as 2-D DMA copies. Rows of either copy shorter than ~4 KB drop the copy
@@ -925,8 +946,8 @@ int b2_reduce_sum_host(const void *in_host, int64_t n, int dtype, void *out_host
     if (n < 0) return fail(B2_ERR_INVALID, "reduce: negative length");
     if ((!in_host && n) || !out_host) return fail(B2_ERR_INVALID, "reduce: NULL buffer");
     if (int rc = check_dev(dev)) return rc;
-    DevCtx &c = g_ctx[dev];
-    std::lock_guard<std::mutex> g(c.mu);
+    Lane lane = acquire_lane(dev);  // any free pipeline lane of the device
+    DevCtx &c = *lane.c;
     if (int rc = ctx_init(c, dev)) return rc;
     const int64_t ce = std::min<int64_t>(std::max<int64_t>(n, 1), (int64_t)(chunk_bytes() / E));
     if (int rc = ensure_stages(c, (size_t)ce * E)) return rc;
@@ -1026,7 +1047,7 @@ static int enable_peer(int from, int to) {
 
 static int multi_ctx(int dev) {
     if (int rc = check_dev(dev)) return rc;
-    DevCtx &c = g_ctx[dev];
+    DevCtx &c = g_ctx_of(dev);
     if (int rc = ctx_init(c, dev)) return rc;
     if (!c.d_slots) {
         B2_CUDA(cudaMalloc(&c.d_slots, kMaxShards * 8));
@@ -1042,7 +1063,7 @@ struct MultiLock {
         std::vector<int> d(devs);
         std::sort(d.begin(), d.end());
         d.erase(std::unique(d.begin(), d.end()), d.end());
-        for (int x : d) locks.emplace_back(g_ctx[x].mu);
+        for (int x : d) locks.emplace_back(g_ctx_of(x).mu);
     }
 };
 
@@ -1052,7 +1073,7 @@ int b2_init(int ndev) {
     if (ndev <= 0 || ndev > have) ndev = have;
     std::lock_guard<std::mutex> g(g_multi_mu);
     for (int d = 0; d < ndev; ++d) {
-        std::lock_guard<std::mutex> l(g_ctx[d].mu);
+        std::lock_guard<std::mutex> l(g_ctx_of(d).mu);
         if (int rc = multi_ctx(d)) return rc;
     }
     for (int a = 0; a < ndev; ++a)
@@ -1097,7 +1118,7 @@ int b2_transpose_multi(const void *const *in, void *const *out, const int64_t *r
     // every device's stream first waits for the legacy stream (inputs produced there)
     for (int g = 0; g < nshards; ++g) {
         if (rows[g] == 0 || cols == 0) continue;
-        DevCtx &c = g_ctx[devs[g]];
+        DevCtx &c = g_ctx_of(devs[g]);
         if (int rc = check_dev(devs[g])) return rc;
         B2_CUDA(cudaEventRecord(c.ev_legacy, cudaStreamLegacy));
         B2_CUDA(cudaStreamWaitEvent(c.s_comp, c.ev_legacy, 0));
@@ -1107,7 +1128,7 @@ int b2_transpose_multi(const void *const *in, void *const *out, const int64_t *r
     for (int g = 0; g < nshards; ++g) {
         if (rows[g] == 0 || cols == 0) continue;
         if (int rc = check_dev(devs[g])) return rc;
-        B2_CUDA(cudaStreamSynchronize(g_ctx[devs[g]].s_comp));
+        B2_CUDA(cudaStreamSynchronize(g_ctx_of(devs[g]).s_comp));
     }
     return B2_OK;
 }
@@ -1143,7 +1164,7 @@ int b2_reduce_sum_multi(const void *const *shards, const int64_t *n, int nshards
         if (int rc = multi_ctx(devs[g])) return rc;
         fused = fused && enable_peer(devs[g], root);
     }
-    DevCtx &rc_ = g_ctx[root];
+    DevCtx &rc_ = g_ctx_of(root);
     if (fused && !rc_.mailbox) {
         if (int rc = check_dev(root)) return rc;
         B2_CUDA(cudaMalloc(&rc_.mailbox, mailbox_bytes()));
@@ -1154,7 +1175,7 @@ int b2_reduce_sum_multi(const void *const *shards, const int64_t *n, int nshards
     // non-root shards first: shards sharing the root's device then precede the
     // root's kernel on the same stream, so its wait can never block them
     auto launch = [&](int g) -> int {
-        DevCtx &c = g_ctx[devs[g]];
+        DevCtx &c = g_ctx_of(devs[g]);
         if (int rc = check_dev(devs[g])) return rc;
         B2_CUDA(cudaEventRecord(c.ev_legacy, cudaStreamLegacy));
         B2_CUDA(cudaStreamWaitEvent(c.s_comp, c.ev_legacy, 0));
@@ -1175,15 +1196,15 @@ int b2_reduce_sum_multi(const void *const *shards, const int64_t *n, int nshards
     std::vector<char> part(8 * nshards, 0);
     for (int g = 0; g < nshards; ++g) {
         if (fused && g > 0) continue;
-        DevCtx &c = g_ctx[devs[g]];
+        DevCtx &c = g_ctx_of(devs[g]);
         if (int rc = check_dev(devs[g])) return rc;
         B2_CUDA(cudaMemcpyAsync((char *)c.h_slots + 8 * g, (char *)c.d_slots + 8 * g, 8,
                                 cudaMemcpyDeviceToHost, c.s_comp));
     }
     for (int g = 0; g < nshards; ++g) {
         if (int rc = check_dev(devs[g])) return rc;
-        B2_CUDA(cudaStreamSynchronize(g_ctx[devs[g]].s_comp));
-        memcpy(&part[8 * g], (char *)g_ctx[devs[g]].h_slots + 8 * g, 8);
+        B2_CUDA(cudaStreamSynchronize(g_ctx_of(devs[g]).s_comp));
+        memcpy(&part[8 * g], (char *)g_ctx_of(devs[g]).h_slots + 8 * g, 8);
     }
     if (fused) {
         uint64_t st = 0;

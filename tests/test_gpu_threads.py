@@ -1,5 +1,6 @@
 """Concurrent host threads on one device (ctypes releases the GIL, so the calls
-really overlap): the host-buffer pipelines serialise on the per-device context,
+really overlap): the host-buffer pipelines run on one of the device's two pipeline
+lanes each (a third concurrent call waits for lane 0),
 device calls on per-thread streams with per-thread reduce workspaces run
 concurrently, and run_program is re-entrant. Every result is checked against the
 CPU oracle; none may be torn or mixed up between threads."""
@@ -59,6 +60,46 @@ def test_host_pipelines_from_threads():
             assert b2.reduce_sum(x) == _s(x), (k, it)
 
     _run_threads(work)
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+def test_host_pipelines_on_lanes(pinned):
+    """Many-chunk host pipelines (1 MiB stages) of every kind at once — transposes,
+    int / fp32 sums, A.5 tree sums — so two lanes stream concurrently and further
+    calls queue for lane 0; pageable sources go through each lane's own pinned ring."""
+    import paper_2605_13864_b200 as b2
+    from paper_2605_13864_b200 import _lib
+
+    def buf(a):
+        if not pinned:
+            return a
+        t = torch.empty(a.shape, dtype=torch.from_numpy(a[:0]).dtype, pin_memory=True)
+        t.numpy()[...] = a
+        return t.numpy()
+
+    def work(k):
+        rng = np.random.default_rng(500 + k)
+        for it in range(3):
+            if k % 3 == 0:
+                a = buf(rng.integers(0, 2**32, (1300 + k, 900 + 7 * it), dtype=np.uint32).view(np.float32))
+                out = b2.transpose(a)
+                assert out.view(np.uint32).tobytes() == _t(a), (k, it)
+            elif k % 3 == 1:
+                x = buf(rng.integers(-2**31, 2**31, 1_500_000 + 1031 * k, dtype=np.int32))
+                assert b2.reduce_sum(x) == _s(x), (k, it)
+            else:
+                x = buf(rng.uniform(-1, 1, 512 * (3000 + k)).astype(np.float32))
+                with _oracle_mu:
+                    want, _ = oracle.reduce_f32_tree512(x)
+                got = b2.reduce_tree512(x)
+                assert np.float32(got).view(np.uint32) == np.float32(want).view(np.uint32), (k, it)
+
+    prev = _lib.tuning("host.chunk_mb")
+    _lib.tune("host.chunk_mb", 1)
+    try:
+        _run_threads(work)
+    finally:
+        _lib.tune("host.chunk_mb", prev)
 
 
 def test_device_calls_on_per_thread_streams():

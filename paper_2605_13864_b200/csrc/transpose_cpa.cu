@@ -207,11 +207,10 @@ int run_cpa(const void *in, void *out, int64_t rv, int64_t cv, int64_t ld_in, in
     }
     const int per_sm = std::min(g_tune.t_cpa_ctas > 0 ? g_tune.t_cpa_ctas : occ[dev].load(), occ[dev].load());
     const int64_t grid = std::min<int64_t>(ntiles, (int64_t)num_sms(dev) * per_sm);
-    // same walk rule as the LDG path (transpose.cu run_vec): column-major when a
-    // column block holds about as many tiles as there are resident CTAs
-    const bool colwalk = tiles_r * 4 >= (int64_t)num_sms(dev) * 3;
-    const int grp = g_tune.t_group > 0 ? g_tune.t_group
-                                       : colwalk ? (int)std::min<int64_t>(tiles_r, 1 << 30) : 1;
+    // column-major tile walk at every size (unlike the LDG path's mid-size row bands:
+    // with these 256-row tiles the column walk measured level or ahead everywhere,
+    // 16384x32768 fp32 +1.8 %; profiles/r02m_shard_shapes.md)
+    const int grp = g_tune.t_group > 0 ? g_tune.t_group : (int)std::min<int64_t>(tiles_r, 1 << 30);
     const int group = (int)std::max<int64_t>(1, std::min<int64_t>(grp, tiles_r));
     B2_CUDA(launch_kernel(kern, dim3((unsigned)grid), dim3(NT), G::SMEM, st, (const uint8_t *)in, (uint8_t *)out,
                           rv, cv, ld_in * E, ld_out * E, tiles_r, tiles_c, ntiles, group));

@@ -75,11 +75,17 @@ B2_API int b2_device_count(int *count);
 B2_API uint64_t b2_launch_count(void);
 B2_API size_t b2_dtype_size(int dtype);
 /* Performance knobs (process-wide; the defaults are the tuned values):
- *   "transpose.variant" tile shape, "transpose.group" tile-rows per band of the
- *   tile walk, "transpose.ctas_per_sm", "reduce.variant" <threads, loads in
+ *   "transpose.cpa" cp.async-loaded tiles for large aligned matrices (1 = auto,
+ *   2 = always, 0 = LDG tiles only), "transpose.cpa_variant" / "transpose.cpa_hint"
+ *   / "transpose.cpa_ctas" (forced geometry, L2 load hint, CTAs per SM),
+ *   "transpose.variant" LDG tile shape, "transpose.group" tile-rows per band of the
+ *   tile walk, "transpose.ctas_per_sm", "transpose.staged" / "transpose.tma" /
+ *   "transpose.any" alternative paths, "reduce.variant" <threads, loads in
  *   flight>, "reduce.ctas_per_sm" (0 = occupancy limit), "reduce.spin_ms"
- *   (bounded wait of the fused combine, default 20000). Results never depend
- *   on them. b2_tune_get returns -1 for an unknown key. */
+ *   (bounded wait of the fused combine, default 20000), "host.chunk_mb" host
+ *   pipeline stage, "codegen.pipe_kb" / "codegen.coarsen" / "codegen.pack"
+ *   generated-program pipelining, coarsening and block packing, "launch.pdl".
+ *   Results never depend on them. b2_tune_get returns -1 for an unknown key. */
 B2_API int b2_tune_set(const char *key, int64_t value);
 B2_API int64_t b2_tune_get(const char *key);
 

@@ -646,6 +646,9 @@ class _Gen:
         self.nk = 0
         self.tmp = 0
         self.params = []
+        # binary64 code of ONE +, -, * of two binary32 values -> the same operation in
+        # binary32 (see f32_op): what a float store of that code may emit instead
+        self.f32ops: dict = {}
         for i, (pn, pt) in enumerate(fn.params):
             if pt.endswith("*"):
                 s = Sym(pn, "param_arr", pt[:-1], index=i)
@@ -716,7 +719,10 @@ class _Gen:
                 if op == "%":
                     return f"b2_mod({a}, {b})", "i"
             if op in ("+", "-", "*"):
-                return f"((double)({a}) {op} (double)({b}))", "d"
+                code = f"((double)({a}) {op} (double)({b}))"
+                if ta == "f" and tb == "f":
+                    self.f32_op(code, a, op, b, dev is not None)
+                return code, "d"
             raise UnsupportedProgram(f"operator {op!r} on floating-point operands")
         if c == "Call":
             return self.call_expr(e, dev)
@@ -802,8 +808,36 @@ class _Gen:
         zero = "0.0f" if s.ctype == "float" else "0"
         return f"({ok} ? {s.cname}[{off}] : {zero})", t
 
+    def f32_op(self, code, a, op, b, device):
+        """Record that the binary64 `code` is one +, -, * of the binary32 values a, b.
+        The interpreter evaluates it in binary64 and rounds to binary32 at the store
+        (interp.py:43-44, 83-84); with 53 >= 2 x 24 + 2 bits that double rounding is
+        innocuous for a single +, -, * (the binary64 result rounded to binary32 is the
+        correctly rounded binary32 result; products are even exact in binary64), so a
+        float store of `code` may compute it directly in binary32: one FADD / FMUL
+        instead of two F2F.F64, a DADD and an F2F back. __f*_rn never contract into
+        FMAs; the host side is compiled with -ffp-contract=off."""
+        if device:
+            fn = {"+": "__fadd_rn", "-": "__fsub_rn", "*": "__fmul_rn"}[op]
+            self.f32ops[code] = f"{fn}({a}, {b})"
+        else:
+            self.f32ops[code] = f"((float)({a}) {op} (float)({b}))"
+
+    def plus_eq(self, s, old, val, t, device, icast):
+        """`x += val` for the cell / scalar `old` of symbol s -> (code, type): int64 for
+        int x and int val, else binary64 (interp.py:262-270), recorded as a binary32
+        op when x is float and val a binary32 value."""
+        if t == "i" and s.ctype == "int":
+            return f"({icast}{old} + {val})", "i"
+        code = f"((double){old} + (double)({val}))"
+        if s.ctype == "float" and t == "f":
+            self.f32_op(code, old, "+", val, device)
+        return code, "d"
+
     def store_value(self, s, code, t):
         if s.ctype == "float":
+            if t == "d" and code in self.f32ops:
+                return self.f32ops[code]
             return f"(float)({code})" if t != "f" else code
         if t != "i":
             raise UnsupportedProgram("float value stored into an int cell")
@@ -955,8 +989,7 @@ class _Gen:
             if s.loop:
                 raise UnsupportedProgram(f"{s.name!r} is not assignable")
             if a.op == "+=":
-                val, t = (f"({s.cname} + {val})", "i") if (t == "i" and s.ctype == "int") else \
-                    (f"((double){s.cname} + (double)({val}))", "d")
+                val, t = self.plus_eq(s, s.cname, val, t, False, "")
             return [f"{s.cname} = {self.store_value(s, val, t)};"]
         if s.kind not in ("param_arr", "host_arr"):
             raise UnsupportedProgram(f"host code writes device/shared array {s.name!r}")
@@ -965,8 +998,7 @@ class _Gen:
         lines = [f"const int64_t {ix}[] = {{{', '.join(codes) or '0'}}};"]
         if a.op == "+=":
             old = f"b2_hread({s.cname}, {len(codes)}, {ix})"
-            val, t = (f"((int64_t){old} + {val})", "i") if (t == "i" and s.ctype == "int") else \
-                (f"((double){old} + (double)({val}))", "d")
+            val, t = self.plus_eq(s, old, val, t, False, "(int64_t)")
         lines.append(f"b2_hwrite({s.cname}, {len(codes)}, {ix}, ({s.elem})({self.store_value(s, val, t)}));")
         return lines
 
@@ -1652,8 +1684,7 @@ class _KernelCtx:
                 if self.tf_depth > self.block_depth and getattr(s, "depth", 0) <= self.block_depth:
                     self.coarsenable = False  # program threads write a block-level local
                 if st.op == "+=":
-                    val, t = (f"({s.cname} + {val})", "i") if (t == "i" and s.ctype == "int") else \
-                        (f"((double){s.cname} + (double)({val}))", "d")
+                    val, t = g.plus_eq(s, s.cname, val, t, True, "")
                 out.extend(pad + p for p in g.pre)
                 out.append(pad + f"{s.cname} = {g.store_value(s, val, t)};")
                 return
@@ -1666,8 +1697,7 @@ class _KernelCtx:
             ok, off, lines = g._dev_offset(s, codes)
             cell = f"{s.cname}[{off}]"
             if st.op == "+=":
-                val, t = (f"((int64_t){cell} + {val})", "i") if (t == "i" and s.ctype == "int") else \
-                    (f"((double){cell} + (double)({val}))", "d")
+                val, t = g.plus_eq(s, cell, val, t, True, "(int64_t)")
             # a memory write in a context wider than one thread runs once (interp semantics)
             guard = f"{rel} == 0 && " if w != "1" else ""
             body = g.pre + lines + [f"if ({guard}{ok}) {cell} = ({s.elem})({g.store_value(s, val, t)});"]

@@ -170,3 +170,44 @@ def test_block_scoped_declarations():
            "kernel_teardown_begin(); kernel_kill(); } memcpy_device_to_host1(a, d, N); gmem_free(d); }")
     s = codegen.generate(parse_program(src).entry())
     assert "float v_k" in s and "B2IX v_k" in s  # the loop index keeps the index type
+
+
+F32_OPS = """void f(float* a, float* b, float* r, int N) {
+    float* const d_a = gmem_malloc1<float>(N);
+    memcpy_host_to_device1(d_a, a, N);
+    float* const d_b = gmem_malloc1<float>(N);
+    memcpy_host_to_device1(d_b, b, N);
+    float* const d_r = gmem_malloc1<float>(5 * N);
+    {
+        kernel_launch(N / 64, 64, 0);
+        kernel_setup_end();
+        thread for (int i = 0; i < N; i++) {
+            d_r[5 * i] = d_a[i] + d_b[i];
+            d_r[5 * i + 1] = d_a[i] - d_b[i];
+            d_r[5 * i + 2] = d_a[i] * d_b[i];
+            d_r[5 * i + 3] = d_a[i] * d_b[i] + d_a[i];
+            float t = d_a[i];
+            t += d_b[i];
+            d_r[5 * i + 4] = t;
+        }
+        kernel_teardown_begin();
+        kernel_kill();
+    }
+    memcpy_device_to_host1(r, d_r, 5 * N);
+    gmem_free(d_r);
+    gmem_free(d_b);
+    gmem_free(d_a);
+}
+"""
+
+
+def test_single_float_ops_stored_in_binary32():
+    """One +, -, * (or +=) of two binary32 values stored into a float computes in
+    binary32 (__fadd_rn / __fsub_rn / __fmul_rn: the binary64 result the interpreter
+    rounds is the same bits); a nested expression keeps binary64 evaluation."""
+    src = codegen.generate(parse_program(F32_OPS).entry())
+    kernel = src[src.index("__global__"):src.index('extern "C" int b2g_main')]
+    assert kernel.count("__fadd_rn(") == 2 and kernel.count("__fsub_rn(") == 1
+    assert kernel.count("__fmul_rn(") == 1  # a*b + a keeps the interpreter's binary64 evaluation
+    nested = [ln for ln in kernel.splitlines() if "((double)(((double)(" in ln]
+    assert len(nested) == 1 and "__f" not in nested[0]

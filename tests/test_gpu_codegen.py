@@ -324,3 +324,28 @@ def test_32bit_index_arithmetic_only_when_proved(b2):
     c = codegen.compile_fn(q.fn("f"))
     assert c.kernel_unchecked()[0] and not c.kernel_ix32()[0]
     assert np.array_equal(np.array(got["r"], np.float32), x)
+
+
+def test_single_float_ops_match_binary64_rounding(b2):
+    """Stores of one +, -, * (and +=) of two binary32 values run in binary32 on the
+    device; the interpreter computes them in binary64 and rounds at the store
+    (interp.py:43-44, 262-270). Bit-for-bit the same over wide exponents, subnormals,
+    exact cancellation and overflow to inf; the nested a * b + a keeps binary64."""
+    from test_codegen_cpu import F32_OPS
+    rng = np.random.default_rng(2024)
+    n = 64 * 4096
+    mant = rng.uniform(1, 2, n)
+    a = (rng.choice([-1, 1], n) * mant * np.exp2(rng.integers(-149, 128, n))).astype(np.float32)
+    b = (rng.choice([-1, 1], n) * rng.uniform(1, 2, n) * np.exp2(rng.integers(-149, 128, n))).astype(np.float32)
+    b[::7] = -a[::7]                                   # exact cancellation
+    b[1::7] = a[1::7] * np.float32(1 + 2**-23)         # near-ties
+    a[2::7] = np.float32(3.4028235e38)                 # overflow to inf
+    a[3::7] = np.float32(1e-45) * 3                    # subnormals
+    r = np.zeros(5 * n, np.float32)
+    p = b2.parse_program(F32_OPS)
+    b2.run_program(p, "f", {"a": b2.Array.from_numpy(a), "b": b2.Array.from_numpy(b),
+                            "r": b2.Array.from_numpy(r), "N": n}, backend="codegen")
+    a64, b64 = a.astype(np.float64), b.astype(np.float64)
+    with np.errstate(over="ignore"):
+        want = np.stack([a64 + b64, a64 - b64, a64 * b64, a64 * b64 + a64, a64 + b64], 1).astype(np.float32)
+    assert np.array_equal(r.reshape(n, 5).view(np.uint32), want.view(np.uint32))

@@ -58,7 +58,6 @@ struct Tuning {
                             // 2 = always, 0 = never (padded scalar tile)
     int t_staged_ctas = 0;  // CTAs per SM of the staged kernel (0 = 2)
     int t_staged_stages = 4;  // cp.async ring depth of the staged kernel (2, 3, 4)
-    int t_staged_hint = 0;  // 1 = L2 evict-first policy on the staged kernel's cp.async loads
     int c_pipe_kb = 65536;  // generated programs: bytes per copy / kernel pipeline step (KiB; 0 = off)
     int l_pdl = 0;          // 1 = launch the hot kernels with programmatic dependent launch
     int c_coarsen = 8;      // generated programs: largest thread-coarsening factor (1 = off; 8 only packed)

@@ -27,13 +27,8 @@
 namespace b2 {
 namespace {
 
-// pol != 0: L2 cache policy for the read-once input (transpose.staged_hint)
-__device__ __forceinline__ void cp_async16(uint32_t saddr, const void *g, uint64_t pol) {
-    if (pol)
-        asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(saddr), "l"(g), "l"(pol)
-                     : "memory");
-    else
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g) : "memory");
+__device__ __forceinline__ void cp_async16(uint32_t saddr, const void *g) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
@@ -54,7 +49,7 @@ struct Staged {
 template <typename T, int TR, int TC, int NT, int S>
 __global__ void __launch_bounds__(NT)
     transpose_staged_kernel(const T *__restrict__ in, T *__restrict__ out, int64_t rows, int64_t cols,
-                            int64_t ld_in, int64_t ld_out, int64_t tiles_r, int64_t ntiles, int hint) {
+                            int64_t ld_in, int64_t ld_out, int64_t tiles_r, int64_t ntiles) {
     using G = Staged<T, TR, TC, NT, S>;
     constexpr int E = G::E, V = G::V, CH = G::CH;
     constexpr int NW = NT / 32;
@@ -62,8 +57,6 @@ __global__ void __launch_bounds__(NT)
     extern __shared__ __align__(16) uint4 sm[];
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sm);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint64_t pol = 0;
-    if (hint) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
     pdl_enter();
 
     // column-major tile walk: concurrently processed tiles are vertical neighbours,
@@ -85,7 +78,7 @@ __global__ void __launch_bounds__(NT)
             const uintptr_t ab = ga & ~(uintptr_t)15;
             const int ph = (int)(ga - ab) / E;
             const int nch = (ph + ncols - 1) / V + 1;
-            if (k < nch) cp_async16(st_base + (uint32_t)((G::row_slot(i) + k) * 16), (const void *)(ab + 16 * k), pol);
+            if (k < nch) cp_async16(st_base + (uint32_t)((G::row_slot(i) + k) * 16), (const void *)(ab + 16 * k));
         }
     };
 
@@ -153,7 +146,7 @@ int run_staged(const void *in, void *out, int64_t rows, int64_t cols, int64_t ld
     const int per_sm = std::min(want, occ[dev].load());
     const int64_t grid = std::min<int64_t>(ntiles, (int64_t)num_sms(dev) * per_sm);
     B2_CUDA(launch_kernel(kern, dim3((unsigned)grid), dim3(NT), G::SMEM, st, (const T *)in, (T *)out, rows, cols,
-                          ld_in, ld_out, tiles_r, ntiles, g_tune.t_staged_hint));
+                          ld_in, ld_out, tiles_r, ntiles));
     count_launch();
     return B2_OK;
 }

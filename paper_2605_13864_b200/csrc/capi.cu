@@ -85,7 +85,7 @@ struct DevCtx {
 // reduction) overlap their PCIe traffic instead of serialising on one context.
 constexpr int kLanes = 2;
 DevCtx g_lanes[64][kLanes];
-#define g_ctx_of(dev) (g_lanes[dev][0])
+inline DevCtx &g_ctx_of(int dev) { return g_lanes[dev][0]; }  // lane 0: device-wide state
 
 struct Lane {
     DevCtx *c;

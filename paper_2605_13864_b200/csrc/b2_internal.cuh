@@ -54,10 +54,11 @@ struct Tuning {
     int t_tma_stages = 2;   // input stages in flight per CTA (2, 3, 4, 6); 2 x 2 CTAs/SM measured best
     int t_scalar_tile = 0;  // padded scalar tile width: 0 = auto (2-byte 128, else 64), 64, 128 (2/4-byte)
     int r_spin_ms = 20000;  // fused combine: bounded wait per epoch before giving up (status word)
-    int t_staged = 1;       // odd pitches / unaligned views: cp.async-staged kernel 1 = auto (large 2-byte),
-                            // 2 = always, 0 = never (padded scalar tile)
+    int t_staged = 1;       // odd pitches / unaligned views: cp.async-staged kernel 1 = auto (2-byte cells
+                            // from 2^22 cells, any width beyond 256 MB), 2 = always, 0 = never (scalar tile)
     int t_staged_ctas = 0;  // CTAs per SM of the staged kernel (0 = 2)
     int t_staged_stages = 4;  // cp.async ring depth of the staged kernel (2, 3, 4)
+    int t_staged_geom = 0;  // staged kernel tile geometry (see staged_geom; 0 = auto by size)
     int c_pipe_kb = 65536;  // generated programs: bytes per copy / kernel pipeline step (KiB; 0 = off)
     int l_pdl = 0;          // 1 = launch the hot kernels with programmatic dependent launch
     int c_coarsen = 8;      // generated programs: largest thread-coarsening factor (1 = off; 8 only packed)

@@ -352,6 +352,7 @@ static int *tune_slot(const char *key) {
     if (k == "codegen.pack") return &g_tune.c_pack;
     if (k == "transpose.staged_ctas") return &g_tune.t_staged_ctas;
     if (k == "transpose.staged_stages") return &g_tune.t_staged_stages;
+    if (k == "transpose.staged_geom") return &g_tune.t_staged_geom;
     if (k == "transpose.cpa") return &g_tune.t_cpa;
     if (k == "transpose.cpa_variant") return &g_tune.t_cpa_variant;
     if (k == "transpose.cpa_ctas") return &g_tune.t_cpa_ctas;

@@ -438,8 +438,11 @@ int dispatch(const void *in, void *out, int64_t rows, int64_t cols, int64_t ld_i
             // tile (bf16 4097x8191 3.6 -> 4.6 TB/s, 16385x16383 3.76 -> 5.15 TB/s); 4- and
             // 8-byte cells and small matrices stay on the scalar tile, which is on par or
             // faster there (profiles/r02c_odd_staged.md). t_staged = 2 forces it.
+            // Round 2: every cell width beyond 256 MB of input, on 128-row tiles
+            // (+4..12 % over the scalar tile for 4- / 8-byte cells, profiles/r02s_odd_geom.md).
             const bool use = g_tune.t_staged == 2 ||
-                             (g_tune.t_staged == 1 && E == 2 && rows * cols >= (int64_t(1) << 22));
+                             (g_tune.t_staged == 1 && ((E == 2 && rows * cols >= (int64_t(1) << 22)) ||
+                                                       rows * cols * E > (int64_t(256) << 20)));
             if (use && (uintptr_t)in % E == 0 && (uintptr_t)out % E == 0)
                 return launch_transpose_staged(in, out, rows, cols, ld_in, ld_out, E, dev, st);
         }

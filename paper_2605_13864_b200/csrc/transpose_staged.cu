@@ -27,8 +27,13 @@
 namespace b2 {
 namespace {
 
-__device__ __forceinline__ void cp_async16(uint32_t saddr, const void *g) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g) : "memory");
+template <int H>
+__device__ __forceinline__ void cp_async16(uint32_t saddr, const void *g, uint64_t pol) {
+    if constexpr (H == 1)  // L2 evict-first policy (read-once input)
+        asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(saddr), "l"(g), "l"(pol)
+                     : "memory");
+    else
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
@@ -46,17 +51,20 @@ struct Staged {
     __device__ static __forceinline__ int row_slot(int i) { return i * CH + ROT * (i >> 3); }
 };
 
-template <typename T, int TR, int TC, int NT, int S>
+template <typename T, int TR, int TC, int NT, int S, int H>
 __global__ void __launch_bounds__(NT)
     transpose_staged_kernel(const T *__restrict__ in, T *__restrict__ out, int64_t rows, int64_t cols,
                             int64_t ld_in, int64_t ld_out, int64_t tiles_r, int64_t ntiles) {
     using G = Staged<T, TR, TC, NT, S>;
     constexpr int E = G::E, V = G::V, CH = G::CH;
     constexpr int NW = NT / 32;
-    static_assert(TR == 64, "one warp covers a 64-cell output segment as two 32-lane runs");
+    constexpr int RPL = TR / 32;  // tile rows per lane: a warp writes TR-cell output segments as RPL 32-lane runs
+    static_assert(TR % 32 == 0, "tile rows must be a multiple of the warp width");
     extern __shared__ __align__(16) uint4 sm[];
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sm);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint64_t pol = 0;
+    if constexpr (H == 1) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
     pdl_enter();
 
     // column-major tile walk: concurrently processed tiles are vertical neighbours,
@@ -78,7 +86,7 @@ __global__ void __launch_bounds__(NT)
             const uintptr_t ab = ga & ~(uintptr_t)15;
             const int ph = (int)(ga - ab) / E;
             const int nch = (ph + ncols - 1) / V + 1;
-            if (k < nch) cp_async16(st_base + (uint32_t)((G::row_slot(i) + k) * 16), (const void *)(ab + 16 * k));
+            if (k < nch) cp_async16<H>(st_base + (uint32_t)((G::row_slot(i) + k) * 16), (const void *)(ab + 16 * k), pol);
         }
     };
 
@@ -103,11 +111,14 @@ __global__ void __launch_bounds__(NT)
         const int ncols = (int)(cols - c0 < TC ? cols - c0 : TC);
         const int nrows = (int)(rows - r0 < TR ? rows - r0 : TR);
         const char *stage = reinterpret_cast<const char *>(sm) + (size_t)(it % S) * G::SLOTS * 16;
-        // this lane's two tile rows (i = lane, lane + 32): byte address of cell (i, j = 0)
-        const char *src[2];
-        bool ok[2];
+        // this lane's tile rows (i = lane + 32 h): byte address of cell (i, j = 0). The
+        // 32 rows one instruction reads are consecutive, so every h sees the bank
+        // spread of row_slot's rotation (rows 32 h .. 32 h + 31 are rows 0 .. 31 shifted
+        // by a constant number of slots)
+        const char *src[RPL];
+        bool ok[RPL];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < RPL; ++h) {
             const int i = lane + 32 * h;
             ok[h] = i < nrows;
             const uintptr_t ga = (uintptr_t)(in + (r0 + (ok[h] ? i : 0)) * ld_in + c0);
@@ -118,22 +129,22 @@ __global__ void __launch_bounds__(NT)
         for (int j = warp; j < ncols; j += NW) {
             T *d = dst + (int64_t)j * ld_out;
 #pragma unroll
-            for (int h = 0; h < 2; ++h)
+            for (int h = 0; h < RPL; ++h)
                 if (ok[h]) d[32 * h] = *reinterpret_cast<const T *>(src[h] + j * E);
         }
     }
     cp_async_wait<0>();
 }
 
-template <typename T, int TC, int S>
+template <typename T, int TC, int S, int TR = 64, int CTAS = 2, int H = 0>
 int run_staged(const void *in, void *out, int64_t rows, int64_t cols, int64_t ld_in, int64_t ld_out,
                int dev, cudaStream_t st) {
-    constexpr int TR = 64, NT = 256;
+    constexpr int NT = 256;
     using G = Staged<T, TR, TC, NT, S>;
     const int64_t tiles_r = (rows + TR - 1) / TR, tiles_c = (cols + TC - 1) / TC;
     const int64_t ntiles = tiles_r * tiles_c;
     if (ntiles == 0) return B2_OK;
-    auto kern = transpose_staged_kernel<T, TR, TC, NT, S>;
+    auto kern = transpose_staged_kernel<T, TR, TC, NT, S, H>;
     static std::atomic<int> occ[64];
     if (occ[dev] == 0) {
         if (G::SMEM > 48 * 1024)
@@ -142,7 +153,7 @@ int run_staged(const void *in, void *out, int64_t rows, int64_t cols, int64_t ld
         B2_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, NT, G::SMEM));
         occ[dev] = o > 0 ? o : 1;
     }
-    const int want = g_tune.t_staged_ctas > 0 ? g_tune.t_staged_ctas : 2;
+    const int want = g_tune.t_staged_ctas > 0 ? g_tune.t_staged_ctas : CTAS;
     const int per_sm = std::min(want, occ[dev].load());
     const int64_t grid = std::min<int64_t>(ntiles, (int64_t)num_sms(dev) * per_sm);
     B2_CUDA(launch_kernel(kern, dim3((unsigned)grid), dim3(NT), G::SMEM, st, (const T *)in, (T *)out, rows, cols,
@@ -151,25 +162,38 @@ int run_staged(const void *in, void *out, int64_t rows, int64_t cols, int64_t ld
     return B2_OK;
 }
 
+// Tile geometries behind transpose.staged_geom (tile rows x 256-B rows, stages, CTAs
+// per SM, L2 load hint): 1 = 256 rows, 2 stages, 1 CTA; 2 = 128 rows, 2 stages, 2
+// CTAs; 3 = 1 + evict-first; 4 = 128 rows, 3 stages, 1 CTA; 5 = 2 + evict-first;
+// 6 = 64 rows, t_staged_stages (4) x 2 CTAs. 0 = auto: geometry 2 for inputs beyond
+// 256 MB (2x L2), else geometry 6 (profiles/r02s_odd_geom.md: 128-row tiles x 2
+// stages x 2 CTAs measured +4..12 % on the large C5 odd shapes of every cell width,
+// the 64-row ring stays ahead on mid sizes; the hint costs everywhere).
+template <typename T, int TC>
+int staged_geom(const void *in, void *out, int64_t rows, int64_t cols, int64_t ld_in, int64_t ld_out, int dev,
+                cudaStream_t st) {
+    int geom = g_tune.t_staged_geom;
+    if (geom == 0) geom = rows * cols * (int64_t)sizeof(T) > (int64_t(256) << 20) ? 2 : 6;
+    switch (geom) {
+    case 1: return run_staged<T, TC, 2, 256, 1>(in, out, rows, cols, ld_in, ld_out, dev, st);
+    case 2: return run_staged<T, TC, 2, 128, 2>(in, out, rows, cols, ld_in, ld_out, dev, st);
+    case 3: return run_staged<T, TC, 2, 256, 1, 1>(in, out, rows, cols, ld_in, ld_out, dev, st);
+    case 4: return run_staged<T, TC, 3, 128, 1>(in, out, rows, cols, ld_in, ld_out, dev, st);
+    case 5: return run_staged<T, TC, 2, 128, 2, 1>(in, out, rows, cols, ld_in, ld_out, dev, st);
+    default: break;
+    }
+    const int s = g_tune.t_staged_stages;
+    if (s == 3) return run_staged<T, TC, 3>(in, out, rows, cols, ld_in, ld_out, dev, st);
+    if (s == 2) return run_staged<T, TC, 2>(in, out, rows, cols, ld_in, ld_out, dev, st);
+    return run_staged<T, TC, 4>(in, out, rows, cols, ld_in, ld_out, dev, st);
+}
+
 template <typename T>
 int staged_for(const void *in, void *out, int64_t rows, int64_t cols, int64_t ld_in, int64_t ld_out,
                int dev, cudaStream_t st) {
-    // 128-B input row runs: 64 cells of 2 bytes, 32 of 4, 16 of 8 -> tiles of 64 rows
-    // x 128 / 64 / 32 cells (16 KB of cells per stage for 2-byte cells)
-    const int s = g_tune.t_staged_stages;
-    if constexpr (sizeof(T) == 2) {
-        if (s == 3) return run_staged<T, 128, 3>(in, out, rows, cols, ld_in, ld_out, dev, st);
-        if (s == 2) return run_staged<T, 128, 2>(in, out, rows, cols, ld_in, ld_out, dev, st);
-        return run_staged<T, 128, 4>(in, out, rows, cols, ld_in, ld_out, dev, st);
-    } else if constexpr (sizeof(T) == 4) {
-        if (s == 3) return run_staged<T, 64, 3>(in, out, rows, cols, ld_in, ld_out, dev, st);
-        if (s == 2) return run_staged<T, 64, 2>(in, out, rows, cols, ld_in, ld_out, dev, st);
-        return run_staged<T, 64, 4>(in, out, rows, cols, ld_in, ld_out, dev, st);
-    } else {
-        if (s == 3) return run_staged<T, 32, 3>(in, out, rows, cols, ld_in, ld_out, dev, st);
-        if (s == 2) return run_staged<T, 32, 2>(in, out, rows, cols, ld_in, ld_out, dev, st);
-        return run_staged<T, 32, 4>(in, out, rows, cols, ld_in, ld_out, dev, st);
-    }
+    // 256-B input row runs: 128 cells of 2 bytes, 64 of 4, 32 of 8 (each staged row
+    // 17 x 16 B with its alignment phase)
+    return staged_geom<T, 256 / (int)sizeof(T)>(in, out, rows, cols, ld_in, ld_out, dev, st);
 }
 
 }  // namespace

@@ -312,14 +312,42 @@ def test_staged_odd_pitch_full(b2, stages, ctas, dt, rows, cols):
     _lib.tune("transpose.staged_stages", stages)
     _lib.tune("transpose.staged_ctas", ctas)
     _lib.tune("transpose.staged", 2)
+    _lib.tune("transpose.staged_geom", 6)  # the 64-row ring at every size
     try:
         t = b2.transpose(a)
     finally:
         _lib.tune("transpose.staged_stages", 4)
         _lib.tune("transpose.staged_ctas", 0)
         _lib.tune("transpose.staged", 1)
+        _lib.tune("transpose.staged_geom", 0)
     assert np.array_equal(t.cpu().numpy(), oracle.transpose(a.cpu().numpy()))
 
+
+
+@pytest.mark.parametrize("geom", [1, 2, 3, 4, 5, 6])
+@pytest.mark.parametrize("dt", [torch.int16, torch.int32, torch.int64])
+@pytest.mark.parametrize("rows,cols,oin,oout", [(4097, 8191, 0, 0), (777, 10003, 3, 1), (300, 65, 1, 2),
+                                                (64, 129, 0, 5), (5000, 31, 7, 0)])
+def test_staged_geometries(b2, geom, dt, rows, cols, oin, oout):
+    """Every tile geometry of the staged kernel (64 / 128 / 256 tile rows, ring depth,
+    residency, L2 hint) on odd pitches and misaligned views: whole result against the
+    CPU oracle, neighbours of the output view untouched."""
+    from paper_2605_13864_b200 import _lib
+    info = torch.iinfo(dt)
+    src = torch.randint(info.min, info.max, (rows, cols + oin + 3), device="cuda", dtype=dt)
+    view = src[:, oin:oin + cols]
+    dst = torch.full((cols, rows + oout + 5), 7, device="cuda", dtype=dt)
+    oview = dst[:, oout:oout + rows]
+    _lib.tune("transpose.staged_geom", geom)
+    _lib.tune("transpose.staged", 2)
+    try:
+        b2.transpose(view, oview)
+    finally:
+        _lib.tune("transpose.staged_geom", 0)
+        _lib.tune("transpose.staged", 1)
+    assert np.array_equal(oview.contiguous().cpu().numpy(), oracle.transpose(view.contiguous().cpu().numpy()))
+    rest = torch.cat([dst[:, :oout].reshape(-1), dst[:, oout + rows:].reshape(-1)])
+    assert bool((rest == 7).all())
 
 
 @pytest.mark.parametrize("shape", [(64, 64), (1000, 1000), (333, 516), (4096, 4096), (100, 36), (65, 4100)])

@@ -101,6 +101,11 @@ def run_transpose(rng):
         one_transpose(130, 390, np.uint16, rng, pad_in=1, pad_out=1)
         one_transpose(70, 45, np.float64, rng, pad_in=1, pad_out=3)
     tune("transpose.staged_stages", 4)
+    for geom in range(1, 6):  # 128 / 256-row tiles, ring depths, the evict-first hint
+        tune("transpose.staged_geom", geom)
+        one_transpose(300, 130, np.float32, rng, pad_in=1, pad_out=3)
+        one_transpose(270, 260, np.uint16, rng, pad_in=3, pad_out=1)
+    tune("transpose.staged_geom", 0)
     one_transpose(128, 96, np.float32, rng, off=1)
     one_transpose(120, 88, np.uint16, rng, pad_in=3, off=1)
     tune("transpose.staged", 0)

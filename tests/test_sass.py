@@ -83,8 +83,11 @@ def test_tma_variant_and_tree_kernel(table):
 def test_staged_odd_pitch_kernel_uses_cp_async(table):
     """The 2-byte odd-pitch path fetches 16-B chunks with cp.async (LDGSTS) into its
     shared-memory ring and waits on commit groups (DEPBAR), one barrier per tile."""
-    b = _body(table, "transpose_staged_kernel<unsigned short, 64, 128, 256, 4>")
-    assert "LDGSTS.E.BYPASS.128" in b and "DEPBAR" in b and "BAR.SYNC" in b
+    for k in ("transpose_staged_kernel<unsigned short, 64, 128, 256, 4, 0>",    # 2-byte, >= 2^22 cells
+              "transpose_staged_kernel<unsigned int, 128, 64, 256, 2, 0>",      # any width, > 256 MB
+              "transpose_staged_kernel<unsigned long, 128, 32, 256, 2, 0>"):
+        b = _body(table, k)
+        assert "LDGSTS.E.BYPASS.128" in b and "DEPBAR" in b and "BAR.SYNC" in b, k
 
 
 def test_fp32_sum_accumulates_in_binary64(table):

@@ -16,11 +16,15 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 LIB = os.path.join(ROOT, "paper_2605_13864_b200", "libb200k.so")
 
 DEFAULTS = [  # (demangled-name prefix, role)
-    ("transpose_vec_kernel<4, 64, 32, 512>", "C4 fp32 transpose, 256x128 tile, 1 CTA/SM (bench)"),
-    ("transpose_vec_kernel<8, 128, 32, 512>", "fp64 large transpose, 256x64 tile"),
-    ("transpose_vec_kernel<2, 16, 16, 256>", "bf16 transpose, 128x128 tile"),
+    ("transpose_cpa_kernel<4, 256, 16, 256, 2, 1>", "C4 fp32 transpose (bench): cp.async-loaded 256x64 tiles, 2 stages"),
+    ("transpose_cpa_kernel<8, 256, 16, 256, 2, 1>", "fp64 aligned transpose > 256 MB, cp.async-loaded"),
+    ("transpose_cpa_kernel<2, 128, 16, 512, 4, 0>", "bf16 aligned transpose > 256 MB, cp.async-loaded"),
+    ("transpose_vec_kernel<4, 64, 32, 512>", "fp32 aligned <= 256 MB, 256x128 LDG tile (round-1 C4 default)"),
+    ("transpose_vec_kernel<8, 128, 32, 512>", "fp64 aligned <= 256 MB, 256x64 LDG tile"),
+    ("transpose_vec_kernel<2, 16, 16, 256>", "bf16 aligned <= 256 MB, 128x128 LDG tile"),
     ("transpose_vec_kernel<4, 16, 16, 256>", "fp32 small / mid transpose, 64x64 tile"),
-    ("transpose_staged_kernel<unsigned short, 64, 128, 256, 4>", "2-byte odd pitches >= 2^22 cells, cp.async-staged ring"),
+    ("transpose_staged_kernel<unsigned short, 64, 128, 256, 4, 0>", "2-byte odd pitches >= 2^22 cells, cp.async-staged ring"),
+    ("transpose_staged_kernel<unsigned int, 128, 64, 256, 2, 0>", "odd pitches > 256 MB (any width), 128-row staged tiles"),
     ("transpose_scalar_kernel<unsigned short, 128>", "2-byte odd pitches (small), padded 64x128 tile"),
     ("transpose_scalar_kernel<unsigned int, 64>", "4-byte odd pitches, padded 64x64 tile"),
     ("reduce_kernel<int, 512, 4, 1>", "C3 int32 sum (bench)"),

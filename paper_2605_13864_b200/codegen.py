@@ -1403,7 +1403,8 @@ class _KernelCtx:
             pro.append(f"    {s.elem} {s.cname}[B2_TREG_MAX]; if (({n}) > B2_TREG_MAX) {{ b2_flag(b2_err, B2E_OOB, {n}, B2_TREG_MAX); return; }}")
         # B2CO > 1 (thread coarsening, check-free launches only): a CUDA block of tpb / B2CO
         # threads runs one program block of tpb threads; thread c plays program threads
-        # c, c + blockDim.x, ... in every block-level thread-for (see _emit_for)
+        # c, c + b2_pbw, ... (b2_pbw = blockDim.x / B2PK) in every block-level thread-for
+        # (see _emit_for)
         # B2PK > 1 (block packing): the CUDA block runs B2PK consecutive program blocks side
         # by side, b2_pbw CUDA threads each, every one with its own slice of the dynamic
         # shared memory; their barriers coincide (packing requires every barrier to sit in

@@ -15,10 +15,13 @@
 // so cell (i, j) of the tile sits at row_base(i) + (phase(i) + j) * E: the
 // transposed read is one LDS per cell at an address that advances by a constant,
 // and the store is a coalesced warp-wide run of one output row (64 cells = one
-// 128-B segment for 2-byte cells). Rows are placed at a rotation of 2 * (i / 8)
-// 16-B slots so the 32 rows a warp reads at one column spread over the banks
-// (<= 2-way, 1.5 wavefronts on average over all phases / pitches; brute-forced
-// for every odd pitch class).
+// 128-B segment for 2-byte cells). Rows are placed at a rotation of ROT * (i / 8)
+// 16-B slots so the 32 rows a warp reads at one column spread over the banks.
+// Brute-forced over every odd pitch class, base phase and column (round 2): 2-byte
+// cells ROT = 2 (1.5 wavefronts per LDS.U16, the best any rotation reaches); 4- and
+// 8-byte cells ROT = 1 — conflict-free (1 wavefront per LDS.32, 2 per LDS.64, the
+// minimum), where ROT = 2 had made every read exactly 2-way (ncu: 9.5 M conflicts of
+// 24.7 M wavefronts on fp32 16385x16383).
 //
 // Loads only touch aligned 16-B chunks that contain at least one cell of the
 // row, so they never leave the row's allocation pages.
@@ -45,7 +48,7 @@ struct Staged {
     static constexpr int E = sizeof(T);
     static constexpr int V = 16 / E;                 // cells per 16-B chunk
     static constexpr int CH = TC / V + 1;            // chunks per staged row (phase < V)
-    static constexpr int ROT = 2;                    // rotation step (slots) per 8 rows
+    static constexpr int ROT = E == 2 ? 2 : 1;       // rotation step (slots) per 8 rows
     static constexpr int SLOTS = TR * CH + ROT * (TR / 8 - 1) + 1;  // per stage
     static constexpr int SMEM = S * SLOTS * 16;
     __device__ static __forceinline__ int row_slot(int i) { return i * CH + ROT * (i >> 3); }

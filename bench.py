@@ -112,7 +112,7 @@ def transpose_kernel_label(rows, cols):
     this process runs with)."""
     from paper_2605_13864_b200 import _lib
     cpa, sms = _lib.tuning("transpose.cpa"), 148
-    if cpa == 2 or (cpa == 1 and rows * cols * 4 > 256 << 20 and (rows // 256) * (cols // 64) >= 2 * sms):
+    if cpa == 2 or (cpa == 1 and rows * cols * 4 >= 256 << 20 and (rows // 256) * (cols // 64) >= 2 * sms):
         if cpa == 2:
             return f"transpose_cpa_kernel variant {_lib.tuning('transpose.cpa_variant')} (forced)"
         return ("transpose_cpa_kernel<4,256,16,256,2,1> (cp.async-loaded 256x64 fp32 tiles, "

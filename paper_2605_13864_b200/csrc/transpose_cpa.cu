@@ -227,12 +227,13 @@ int run_cpa(const void *in, void *out, int64_t rv, int64_t cv, int64_t ld_in, in
 // the bench step that took the transpose + sum from 0.9 % behind the LDG path to
 // 0.2-0.5 % ahead, the following reduction included); 0 = no hint, 2 = a 256-B L2
 // prefetch hint (slower). transpose.cpa = 2 takes g_tune.t_cpa_variant (tile
-// rows x row bytes, threads, stages; shared memory), always with the evict-first hint:
+// rows x row bytes, threads, stages; shared memory), with the evict-first hint (0-9):
 //   0: 256 x 256 B, 512, 2 (128 KB)  1: 128 x 512 B, 512, 2 (128 KB)
 //   2: 256 x 256 B, 256, 2 (128 KB)  3: 256 x 256 B, 1024, 2 (128 KB)
 //   4: 384 x 256 B, 512, 2 (192 KB)  5: 128 x 256 B, 512, 4 (128 KB)
 //   6: 512 x 128 B, 512, 2 (128 KB)  7: 448 x 256 B, 512, 2 (224 KB)
 //   8: 256 x 256 B, 128, 2 (128 KB)  9: 192 x 256 B, 256, 2 (96 KB)
+//   10 / 11: the auto geometry of the cell width without / with the evict-first hint
 template <int E, int H>
 int cpa_auto(const void *in, void *out, int64_t rv, int64_t cv, int64_t ld_in, int64_t ld_out, int dev,
              cudaStream_t st) {
@@ -260,6 +261,8 @@ int cpa_for(const void *in, void *out, int64_t rv, int64_t cv, int64_t ld_in, in
     case 7: return run_cpa<E, 448, 16, 512, 2, 1>(in, out, rv, cv, ld_in, ld_out, dev, st);
     case 8: return run_cpa<E, 256, 16, 128, 2, 1>(in, out, rv, cv, ld_in, ld_out, dev, st);
     case 9: return run_cpa<E, 192, 16, 256, 2, 1>(in, out, rv, cv, ld_in, ld_out, dev, st);
+    case 10: return cpa_auto<E, 0>(in, out, rv, cv, ld_in, ld_out, dev, st);  // auto geometry, no hint
+    case 11: return cpa_auto<E, 1>(in, out, rv, cv, ld_in, ld_out, dev, st);  // auto geometry, evict-first
     default: return run_cpa<E, 256, 16, 512, 2, 1>(in, out, rv, cv, ld_in, ld_out, dev, st);
     }
 }
@@ -276,7 +279,10 @@ bool transpose_cpa_wanted(int64_t rv, int64_t cv, int esize, int dev) {
     if (g_tune.t_cpa == 0) return false;
     if (g_tune.t_cpa == 2) return true;
     const int64_t tr = esize == 2 ? 128 : 256, tc = 256 / esize;  // auto tiles: rows x 256-B rows
-    return rv * cv * esize > (int64_t(256) << 20) && (rv / tr) * (cv / tc) >= 2 * (int64_t)num_sms(dev);
+    // 256 MB itself (fp32 8192^2, bf16 8192x16384) goes to the cp.async path for 2- / 4-byte
+    // cells (+5 % / +1.4 %), not for 8-byte cells (fp64 4096x8192: -2.4 %; r02k_cpa_mid.jsonl)
+    const int64_t bytes = rv * cv * esize, lim = int64_t(256) << 20;
+    return (esize == 8 ? bytes > lim : bytes >= lim) && (rv / tr) * (cv / tc) >= 2 * (int64_t)num_sms(dev);
 }
 
 int launch_transpose_cpa(const void *in, void *out, int64_t rv, int64_t cv, int64_t ld_in, int64_t ld_out,

@@ -48,6 +48,8 @@ def parse():
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--scaling", choices=["weak", "strong"], default="strong")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-ref-c2", action="store_true",
+                   help="reference arm: skip the ~100 s full-size C2 run of the reference interpreter")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-graph", action="store_true", help="eager launches instead of a CUDA graph")
     p.add_argument("--combine", default="fused", choices=["fused", "nccl"],
@@ -304,6 +306,8 @@ def run_reference(args):
     if not args.no_cpu:
         line["interp_semantics"] = interp_leg(min(rows, 2048), cols, min(n, 1 << 26))
         line["reference_interp"] = reference_interp_leg()
+        if not args.no_ref_c2:
+            line["reference_interp_c2"] = reference_c2_leg()
     print(json.dumps(line), flush=True)
     return 0
 
@@ -330,6 +334,49 @@ s, _ = run_program(rp, "reduce", {"arr": x, "N": n})
 t3 = time.perf_counter()
 print(json.dumps({"transpose_s": t1 - t0, "reduce_s": t3 - t2, "ok": bool(ok_t and s == sum(x))}))
 """
+
+
+REF_C2_SCRIPT = r"""
+import json, sys, time
+sys.path.insert(0, sys.argv[1])
+from minigpu.parser import parse_program
+from minigpu.interp import run_program
+import numpy as np
+p = parse_program(sys.argv[2])
+pin = json.loads(sys.argv[3])
+x = np.random.default_rng(pin["seed"]).uniform(pin["lo"], 1, pin["n"]).astype(np.float32).tolist()
+t0 = time.perf_counter()
+s, _ = run_program(p, "reduce", {"arr": x, "N": len(x)})
+t1 = time.perf_counter()
+bits = int(np.float32(s).view(np.uint32))
+print(json.dumps({"seconds": t1 - t0, "result_f32_bits": bits, "ok": bits == pin["result_f32_bits"]}))
+"""
+
+
+def reference_c2_leg(timeout_s=400):
+    """The reference ITSELF on the paper's case study 2 / BASELINE C2 at full size:
+    program A.2 (naive fp32 sum) over 2^24 cells, the input of the first pinned C2 case
+    (tests/golden/fullsize_ref.json, generated by the reference here); its binary32
+    result must equal the pinned bits. ~100 s of one core in the build container."""
+    import subprocess
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "minigpu")):
+        return {"unavailable": "baseline/_ref/minigpu not installed (run __graft_entry__.build())"}
+    sys.path.insert(0, ROOT)
+    from paper_2605_13864_b200 import programs
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "fullsize_ref.json")) as f:
+            pin = json.load(f)["C2"][0]
+        r = subprocess.run([sys.executable, "-c", REF_C2_SCRIPT, ref, programs.source(programs.REDUCE_NAIVE, "float"),
+                            json.dumps(pin)], capture_output=True, text=True, timeout=timeout_s)
+        d = json.loads(r.stdout.strip().splitlines()[-1])
+    except Exception as e:  # noqa: BLE001 - reported, not fatal
+        return {"unavailable": f"reference C2 run failed: {str(e)[:200]}"}
+    nb = pin["n"] * 4 + 4
+    return {"kind": "reference", "cores": 1, "value": nb / d["seconds"] / 1e9, "unit": "GB/s",
+            "seconds": d["seconds"], "bit_exact_vs_pin": d["ok"],
+            "sample": ("minigpu.interp.run_program (baseline/_ref, unmodified) on program A.2 over fp32 "
+                       f"2^24 cells (BASELINE C2 / paper case study 2, seed {pin['seed']}), single core")}
 
 
 def reference_interp_leg(timeout_s=240):

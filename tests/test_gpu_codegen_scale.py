@@ -30,15 +30,22 @@ def test_transpose_family_vs_vinterp(T, R):
     assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
 
 
+@pytest.mark.parametrize("blocks", [2048, 2047])
 @pytest.mark.parametrize("B,cell", [(256, "float"), (1024, "float"), (512, "int")])
-def test_reduce_family_vs_vinterp(B, cell):
-    rng = np.random.default_rng(B)
-    n = B * 2048
+def test_reduce_family_vs_vinterp(B, cell, blocks):
+    """Also the block packing of generated kernels: B = 256 / 512 (128 / 256 program
+    threads) pack two program blocks per CUDA block on an even block count, and run
+    unpacked on an odd one — the same bits either way."""
+    from paper_2605_13864_b200 import codegen
+    rng = np.random.default_rng(B + blocks)
+    n = B * blocks
     x = rng.uniform(-1, 1, n).astype(np.float32) if cell == "float" else \
         rng.integers(-2**31, 2**31, n, dtype=np.int64).astype(np.int32)
     prog = b2.parse_program(reduce_family(B, cell))
     arr = b2.Array([n], x, cell)
     got, _ = b2.run_program(prog, "reduce", {"arr": arr, "N": n}, backend="codegen")
+    c = codegen.compile_fn(prog.fn("reduce"))
+    assert c.kernel_pack()[0] == (2 if (B <= 512 and blocks % 2 == 0) else 1), (B, blocks, c.kernel_pack())
     want, _ = vinterp.run_program(prog, "reduce", {"arr": b2.Array([n], x.copy(), cell), "N": n}, as_numpy=True)
     if cell == "float":
         assert np.float32(got).view(np.uint32) == np.float32(want).view(np.uint32)

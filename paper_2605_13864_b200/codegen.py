@@ -66,6 +66,44 @@ def _is_const(e) -> bool:
     return False
 
 
+def _ast_eq(a, b) -> bool:
+    """Structural equality of index expressions (works for either parser's nodes)."""
+    ca, cb = _cls(a), _cls(b)
+    if ca != cb:
+        return False
+    if ca in ("IntLit", "FloatLit"):
+        return a.value == b.value
+    if ca == "Var":
+        return a.name == b.name
+    if ca == "BinOp":
+        return a.op == b.op and _ast_eq(a.lhs, b.lhs) and _ast_eq(a.rhs, b.rhs)
+    if ca == "Call":
+        return a.fn == b.fn and len(a.args) == len(b.args) and all(_ast_eq(x, y) for x, y in zip(a.args, b.args))
+    if ca in ("Access", "Ptr"):
+        return a.base == b.base and len(a.idxs) == len(b.idxs) and all(_ast_eq(x, y) for x, y in zip(a.idxs, b.idxs))
+    return False
+
+
+def _even(e) -> bool:
+    """The integer expression is even for every value of its variables: an even
+    literal, a product with an even factor, a sum / difference of even terms."""
+    c = _cls(e)
+    if c == "IntLit":
+        return int(e.value) % 2 == 0
+    if c == "BinOp":
+        if e.op == "*":
+            return _even(e.lhs) or _even(e.rhs)
+        if e.op in ("+", "-"):
+            return _even(e.lhs) and _even(e.rhs)
+    return False
+
+
+def _plus_one(hi, lo) -> bool:
+    """hi is literally `lo + 1`."""
+    return (_cls(hi) == "BinOp" and hi.op == "+" and _cls(hi.rhs) == "IntLit" and int(hi.rhs.value) == 1
+            and _ast_eq(hi.lhs, lo))
+
+
 def _is_ghost(s) -> bool:
     return _cls(s) == "CallStmt" and getattr(s, "ghost", False)
 
@@ -703,8 +741,11 @@ class _Gen:
         if c == "Access":
             return self.access_read(e.base, e.idxs, dev)
         if c == "BinOp":
+            pair = self.cell_pair(e, dev)
             a, ta = self.expr(e.lhs, dev)
             b, tb = self.expr(e.rhs, dev)
+            if pair is not None:
+                a, b = pair(a, b)
             op = e.op
             if op in ("==", "!=", "<", "<=", ">", ">="):
                 ity = "B2IX" if dev is not None else "int64_t"
@@ -807,6 +848,35 @@ class _Gen:
         self.pre.extend(lines)
         zero = "0.0f" if s.ctype == "float" else "0"
         return f"({ok} ? {s.cname}[{off}] : {zero})", t
+
+    def cell_pair(self, e, dev):
+        """Vector access (round 2): `d[i] op d[i + 1]` on a 1-D float device array with
+        i even for every value of its variables (a sum of even terms) reads both cells
+        with one 64-bit load in the check-free instantiation — the pair is 8-B aligned
+        (device allocations are 256-B aligned) and both cells are proved in bounds there.
+        A.5's adjacent-pair load `d_a[b * 512 + 2 * t] + d_a[b * 512 + 2 * t + 1]` is
+        the case. Returns a function rewriting the two scalar operand codes (evaluated
+        only by the checked instantiation) or None."""
+        if dev is None or e.op not in ("+", "-", "*") or _cls(e.lhs) != "Access" or _cls(e.rhs) != "Access":
+            return None
+        if e.lhs.base != e.rhs.base or len(e.lhs.idxs) != 1 or len(e.rhs.idxs) != 1:
+            return None
+        s = self.syms.get(e.lhs.base)
+        if s is None or s.kind != "dev_arr" or s.ctype != "float" or s.rank != 1:
+            return None
+        i1, i2 = e.lhs.idxs[0], e.rhs.idxs[0]
+        if _plus_one(i2, i1) and _even(i1):
+            lo, first = i1, True
+        elif _plus_one(i1, i2) and _even(i2):
+            lo, first = i2, False
+        else:
+            return None
+        (code,) = self._indices(s, [lo], dev)
+        v = self.fresh("v2")
+        self.pre.append(f"const float2 {v} = B2CK ? make_float2(0.0f, 0.0f) : "
+                        f"*reinterpret_cast<const float2 *>({s.cname} + ({code}));")
+        lo_c, hi_c = f"{v}.x", f"{v}.y"
+        return lambda a, b: (f"(B2CK ? {a} : {lo_c if first else hi_c})", f"(B2CK ? {b} : {hi_c if first else lo_c})")
 
     def f32_op(self, code, a, op, b, device):
         """Record that the binary64 `code` is one +, -, * of the binary32 values a, b.

@@ -211,3 +211,15 @@ def test_single_float_ops_stored_in_binary32():
     assert kernel.count("__fmul_rn(") == 1  # a*b + a keeps the interpreter's binary64 evaluation
     nested = [ln for ln in kernel.splitlines() if "((double)(((double)(" in ln]
     assert len(nested) == 1 and "__f" not in nested[0]
+
+
+def test_adjacent_cell_pair_is_one_64_bit_load():
+    """A.5's `d_a[b * 512 + 2 * t] + d_a[b * 512 + 2 * t + 1]` (an even index and its
+    successor on a 1-D float device array) reads both cells with one float2 load in the
+    check-free instantiation; an odd-based pair, or one on different arrays, stays scalar."""
+    src = codegen.generate(_fn("reduce_tree_f32.optc"))
+    assert src.count("*reinterpret_cast<const float2 *>(v_d_a + ") == 1
+    odd = F32_OPS.replace("d_r[5 * i] = d_a[i] + d_b[i];", "d_r[5 * i] = d_a[2 * i + 1] + d_a[2 * i + 2];")
+    odd = odd.replace("kernel_launch(N / 64, 64, 0);", "kernel_launch(N / 128, 64, 0);").replace(
+        "thread for (int i = 0; i < N; i++)", "thread for (int i = 0; i < N / 2; i++)")
+    assert "float2" not in codegen.generate(parse_program(odd).entry())

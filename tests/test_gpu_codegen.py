@@ -349,3 +349,46 @@ def test_single_float_ops_match_binary64_rounding(b2):
     with np.errstate(over="ignore"):
         want = np.stack([a64 + b64, a64 - b64, a64 * b64, a64 * b64 + a64, a64 + b64], 1).astype(np.float32)
     assert np.array_equal(r.reshape(n, 5).view(np.uint32), want.view(np.uint32))
+
+
+PAIR_PROG = """void f(float* a, float* r, int N, int M) {
+    float* const d = gmem_malloc1<float>(N);
+    memcpy_host_to_device1(d, a, N);
+    float* const o = gmem_malloc1<float>(M);
+    {
+        kernel_launch(M / 64, 64, 0);
+        kernel_setup_end();
+        thread for (int t = 0; t < M; t++) {
+            o[t] = d[2 * t] * d[2 * t + 1];
+        }
+        kernel_teardown_begin();
+        kernel_kill();
+    }
+    memcpy_device_to_host1(r, o, M);
+    gmem_free(o);
+    gmem_free(d);
+}
+"""
+
+
+@pytest.mark.parametrize("short", [False, True])
+def test_paired_loads_bit_exact_and_bounds(b2, short):
+    """`d[2t] * d[2t + 1]` runs as one 64-bit load per program thread in the check-free
+    instantiation (bit-exact products); with the input one cell short the last pair is
+    out of bounds, the proof fails, and the checked kernel raises the reference's error."""
+    from paper_2605_13864_b200 import codegen
+    p = b2.parse_program(PAIR_PROG)
+    m = 64 * 300
+    n = 2 * m - (1 if short else 0)
+    a = np.random.default_rng(5).standard_normal(n).astype(np.float32)
+    r = np.zeros(m, np.float32)
+    args = {"a": b2.Array.from_numpy(a), "r": b2.Array.from_numpy(r), "N": n, "M": m}
+    if short:
+        with pytest.raises(b2.InterpError, match="out of bounds"):
+            b2.run_program(p, "f", args, backend="codegen")
+        assert not codegen.compile_fn(p.fn("f")).kernel_unchecked()[0]
+        return
+    b2.run_program(p, "f", args, backend="codegen")
+    assert codegen.compile_fn(p.fn("f")).kernel_unchecked()[0]
+    want = (a[0::2].astype(np.float64) * a[1::2].astype(np.float64)).astype(np.float32)
+    assert np.array_equal(r.view(np.uint32), want.view(np.uint32))

@@ -850,10 +850,11 @@ class _Gen:
         return f"({ok} ? {s.cname}[{off}] : {zero})", t
 
     def cell_pair(self, e, dev):
-        """Vector access (round 2): `d[i] op d[i + 1]` on a 1-D float device array with
-        i even for every value of its variables (a sum of even terms) reads both cells
-        with one 64-bit load in the check-free instantiation — the pair is 8-B aligned
-        (device allocations are 256-B aligned) and both cells are proved in bounds there.
+        """Vector access (round 2): `d[i] op d[i + 1]` on a 1-D device array with i even
+        for every value of its variables (a sum of even terms) reads both cells with one
+        64-bit (float cells) / 128-bit (int64 cells) load in the check-free instantiation
+        — the pair is aligned to its size (device allocations are 256-B aligned) and both
+        cells are proved in bounds there.
         A.5's adjacent-pair load `d_a[b * 512 + 2 * t] + d_a[b * 512 + 2 * t + 1]` is
         the case. Returns a function rewriting the two scalar operand codes (evaluated
         only by the checked instantiation) or None."""
@@ -862,7 +863,7 @@ class _Gen:
         if e.lhs.base != e.rhs.base or len(e.lhs.idxs) != 1 or len(e.rhs.idxs) != 1:
             return None
         s = self.syms.get(e.lhs.base)
-        if s is None or s.kind != "dev_arr" or s.ctype != "float" or s.rank != 1:
+        if s is None or s.kind != "dev_arr" or s.rank != 1:
             return None
         i1, i2 = e.lhs.idxs[0], e.rhs.idxs[0]
         if _plus_one(i2, i1) and _even(i1):
@@ -873,8 +874,11 @@ class _Gen:
             return None
         (code,) = self._indices(s, [lo], dev)
         v = self.fresh("v2")
-        self.pre.append(f"const float2 {v} = B2CK ? make_float2(0.0f, 0.0f) : "
-                        f"*reinterpret_cast<const float2 *>({s.cname} + ({code}));")
+        # float cells: an 8-B float2; int cells (int64): a 16-B longlong2 (16-B aligned)
+        vt, zero = ("float2", "make_float2(0.0f, 0.0f)") if s.ctype == "float" else \
+            ("longlong2", "make_longlong2(0, 0)")
+        self.pre.append(f"const {vt} {v} = B2CK ? {zero} : "
+                        f"*reinterpret_cast<const {vt} *>({s.cname} + ({code}));")
         lo_c, hi_c = f"{v}.x", f"{v}.y"
         return lambda a, b: (f"(B2CK ? {a} : {lo_c if first else hi_c})", f"(B2CK ? {b} : {hi_c if first else lo_c})")
 

@@ -215,10 +215,13 @@ def test_single_float_ops_stored_in_binary32():
 
 def test_adjacent_cell_pair_is_one_64_bit_load():
     """A.5's `d_a[b * 512 + 2 * t] + d_a[b * 512 + 2 * t + 1]` (an even index and its
-    successor on a 1-D float device array) reads both cells with one float2 load in the
+    successor on a 1-D device array) reads both cells with one float2 load in the
     check-free instantiation; an odd-based pair, or one on different arrays, stays scalar."""
     src = codegen.generate(_fn("reduce_tree_f32.optc"))
     assert src.count("*reinterpret_cast<const float2 *>(v_d_a + ") == 1
+    # int cells are int64 in device memory: a 128-bit longlong2 pair
+    src = codegen.generate(_fn("reduce_tree_int256.optc"))
+    assert src.count("*reinterpret_cast<const longlong2 *>(v_d_a + ") == 1
     odd = F32_OPS.replace("d_r[5 * i] = d_a[i] + d_b[i];", "d_r[5 * i] = d_a[2 * i + 1] + d_a[2 * i + 2];")
     odd = odd.replace("kernel_launch(N / 64, 64, 0);", "kernel_launch(N / 128, 64, 0);").replace(
         "thread for (int i = 0; i < N; i++)", "thread for (int i = 0; i < N / 2; i++)")

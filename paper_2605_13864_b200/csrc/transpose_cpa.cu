@@ -2,13 +2,16 @@
 //
 // The same permutation as transpose_vec_kernel (transpose.cu; SURVEY A.1 / A.4,
 // PAPER.md:1041-1068), with the load side moved off the register file: every
-// input tile row (512 B = 32 x 16-B chunks) is fetched by one warp-wide
-// `cp.async.cg` straight from L2 into shared memory, into an S-stage ring, so
-// S - 1 tiles per CTA are in flight without holding a single register.
+// 16-B chunk of a tile row (CH chunks: 256 B in the default geometry, a warp fetches
+// 512 contiguous bytes per instruction) goes global -> shared with `cp.async.cg`
+// (LDGSTS, optionally with an L2 evict-first cache policy) into an S-stage ring, so
+// S - 1 tiles per CTA are in flight without holding a single register. Default (the
+// C4 bench kernel): 256-row x 256-B tiles, 2 stages of 64 KB, 256 threads, 1 CTA/SM,
+// evict-first loads for 4- / 8-byte cells (profiles/r02k_cpa.md).
 //
-//   * shared layout: input orientation, row i of the tile at i * 32 chunks, chunk
+//   * shared layout: input orientation, row i of the tile at i * CH chunks, chunk
 //     k stored at slot k ^ ((i / R) & 7) (R = 8 rows, 4 for 8-byte cells). The
-//     cp.async writes of a row are a permutation of its 32 slots (conflict-free);
+//     cp.async writes of a row are a permutation of its slots (conflict-free);
 //   * stage-out: a warp unit is one chunk column x 64 tile rows; each lane gathers
 //     the cells of one output row segment with scalar LDS at a constant stride (all
 //     rows of a lane share one swizzle; the rows the warp reads at one instruction

@@ -79,8 +79,8 @@ B2_API size_t b2_dtype_size(int dtype);
  *   2 = always, 0 = LDG tiles only), "transpose.cpa_variant" / "transpose.cpa_hint"
  *   / "transpose.cpa_ctas" (forced geometry, L2 load hint, CTAs per SM),
  *   "transpose.variant" LDG tile shape, "transpose.group" tile-rows per band of the
- *   tile walk, "transpose.ctas_per_sm", "transpose.staged" / "transpose.tma" /
- *   "transpose.any" alternative paths, "reduce.variant" <threads, loads in
+ *   tile walk, "transpose.ctas_per_sm", "transpose.staged" / "transpose.staged_geom" /
+ *   "transpose.tma" / "transpose.any" alternative paths and geometries, "reduce.variant" <threads, loads in
  *   flight>, "reduce.ctas_per_sm" (0 = occupancy limit), "reduce.spin_ms"
  *   (bounded wait of the fused combine, default 20000), "host.chunk_mb" host
  *   pipeline stage, "codegen.pipe_kb" / "codegen.coarsen" / "codegen.pack"

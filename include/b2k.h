@@ -145,6 +145,16 @@ B2_API int b2_reduce_sum_fused(const void *in, int64_t n, int dtype, void *out, 
  * 16-byte int (B2_I64), as b2_reduce_sum. */
 B2_API int b2_reduce_sum_host(const void *in_host, int64_t n, int dtype, void *out_host, int dev);
 
+/* The naive fp32 program A.2 in the reference's OWN order (interp.py:262-270, `sum +=
+ * arr[i]`: one binary32 rounding per cell, i ascending) — bit-identical with the
+ * reference interpreter, where b2_reduce_sum returns the correctly rounded sum. The
+ * order is inherently sequential: one warp, ~4 cycles per cell. *acc (device float)
+ * += in[0], ..., in[n - 1]; set it to 0 for a fresh sum, successive calls chain.
+ * `in`: device pointer, 4-byte aligned. */
+B2_API int b2_reduce_sum_seq_f32(const float *in, int64_t n, float *acc, int dev, void *stream);
+/* Host-buffer form: chunked H2D, the chunks summed in order; *result_host receives it. */
+B2_API int b2_reduce_sum_seq_f32_host(const float *in_host, int64_t n, float *result_host, int dev);
+
 /* Appendix A.5 order: per 512-element block b,
  * s[t] = a[2t] + a[2t+1], then s[t] = s[t] + s[t + 2^(7-k)] for k = 0..7;
  * partials[b] = s[0]. Bit-identical to the reference interpreter's tree form.

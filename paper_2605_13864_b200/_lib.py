@@ -35,6 +35,8 @@ SIGNATURES = {
     "b2_reduce_ws_bytes": (_sz, [_i64, _int]),
     "b2_reduce_sum": (_int, [_vp, _i64, _int, _vp, _vp, _sz, _int, _vp]),
     "b2_reduce_sum_host": (_int, [_vp, _i64, _int, _vp, _int]),
+    "b2_reduce_sum_seq_f32": (_int, [_vp, _i64, _vp, _int, _vp]),
+    "b2_reduce_sum_seq_f32_host": (_int, [_vp, _i64, _vp, _int]),
     "b2_mailbox_create": (_int, [_int, ctypes.POINTER(_vp), _vp]),
     "b2_mailbox_open": (_int, [_vp, _int, ctypes.POINTER(_vp)]),
     "b2_mailbox_close": (_int, [_vp, _int, _int]),

@@ -159,6 +159,8 @@ int launch_reduce(const void *in, int64_t n, int dtype, void *out, void *ws, siz
                   int dev, cudaStream_t st, const FusedCombine &fz = FusedCombine(),
                   bool acc_out = false);
 int launch_tree512(const float *in, int64_t n, float *partials, int dev, cudaStream_t st);
+// the naive fp32 program's own order: *acc += in[0], in[1], ... in binary32 (one warp)
+int launch_seq_sum_f32(const float *in, int64_t n, float *acc, int dev, cudaStream_t st);
 // B-element tree blocks (power of two, 64..2048): the A.5 family
 bool tree_block_supported(int block);
 int launch_tree(const float *in, int64_t n, int block, float *partials, int dev, cudaStream_t st);

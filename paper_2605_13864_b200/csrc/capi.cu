@@ -519,6 +519,47 @@ int b2_reduce_tree_host(const float *in_host, int64_t n, int block, float *resul
     return B2_OK;
 }
 
+int b2_reduce_sum_seq_f32(const float *in, int64_t n, float *acc, int dev, void *stream) {
+    B2_NVTX("b2_reduce_sum_seq_f32");
+    if ((!in && n) || !acc) return fail(B2_ERR_INVALID, "sequential sum: NULL buffer");
+    if (int rc = check_dev(dev)) return rc;
+    return launch_seq_sum_f32(in, n, acc, dev, (cudaStream_t)stream);
+}
+
+int b2_reduce_sum_seq_f32_host(const float *in_host, int64_t n, float *result_host, int dev) {
+    B2_NVTX("b2_reduce_sum_seq_f32_host");
+    if ((!in_host && n) || !result_host) return fail(B2_ERR_INVALID, "sequential sum: NULL buffer");
+    if (n < 0) return fail(B2_ERR_INVALID, "sequential sum: negative length");
+    if (int rc = check_dev(dev)) return rc;
+    Lane lane = acquire_lane(dev);  // any free pipeline lane of the device
+    DevCtx &c = *lane.c;
+    if (int rc = ctx_init(c, dev)) return rc;
+    const int64_t ce = std::max<int64_t>(1, std::min<int64_t>(std::max<int64_t>(n, 1),
+                                                              (int64_t)(chunk_bytes() / sizeof(float))));
+    if (int rc = ensure_stages(c, (size_t)ce * sizeof(float))) return rc;
+    if (int rc = ensure_small(c, sizeof(float))) return rc;
+    B2_CUDA(cudaMemsetAsync(c.d_small, 0, sizeof(float), c.s_comp));
+    const int64_t nchunks = (n + ce - 1) / ce;
+    const bool stage_in = n > 0 && !is_pinned(in_host);
+    if (stage_in && ensure_host_stages(c, (size_t)ce * sizeof(float))) return B2_ERR_NOMEM;
+    for (int64_t i = 0; i < nchunks; ++i) {  // chunks in order on one compute stream
+        const int k = (int)(i % kStages);
+        const int64_t e0 = i * ce, ne = std::min(ce, n - e0);
+        if (i >= kStages) B2_CUDA(cudaStreamWaitEvent(c.s_h2d, c.ev_comp[k], 0));
+        if (int rc = h2d_rows(c, k, stage_in, c.d_in[k], (const char *)(in_host + e0), ne * sizeof(float),
+                              ne * sizeof(float), 1))
+            return rc;
+        B2_CUDA(cudaEventRecord(c.ev_in[k], c.s_h2d));
+        B2_CUDA(cudaStreamWaitEvent(c.s_comp, c.ev_in[k], 0));
+        if (int rc = launch_seq_sum_f32((const float *)c.d_in[k], ne, (float *)c.d_small, dev, c.s_comp)) return rc;
+        B2_CUDA(cudaEventRecord(c.ev_comp[k], c.s_comp));
+    }
+    B2_CUDA(cudaMemcpyAsync(c.h_small, c.d_small, sizeof(float), cudaMemcpyDeviceToHost, c.s_comp));
+    B2_CUDA(cudaStreamSynchronize(c.s_comp));
+    *result_host = *(const float *)c.h_small;
+    return B2_OK;
+}
+
 int b2_reduce_tree512_host(const float *in_host, int64_t n, float *result_host, int dev) {
     return b2_reduce_tree_host(in_host, n, 512, result_host, dev);
 }

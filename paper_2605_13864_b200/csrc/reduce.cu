@@ -410,6 +410,64 @@ int run_reduce(const void *in_, int64_t n, void *out, void *ws, size_t ws_bytes,
 
 }  // namespace
 
+// The reference's own evaluation order for the naive fp32 program A.2 (interp.py:
+// 262-270: `sum += arr[i]`, one binary32 rounding per step, i ascending): inherently
+// sequential, so one warp runs it — all 32 lanes stream 8-KB chunks global -> shared
+// with 4-byte cp.async (any alignment) into a double buffer, lane 0 adds each chunk's
+// cells in order onto the carried binary32 sum (`*acc`, so chunks of a host pipeline
+// chain). ~4 cycles per cell (the FADD dependency): C2's 2^24 cells in ~35 ms,
+// bit-identical with the reference (tests/test_gpu_seq_sum.py).
+constexpr int kSeqChunk = 2048;
+__global__ void __launch_bounds__(32) seq_sum_f32_kernel(const float *__restrict__ in, int64_t n, float *acc) {
+    __shared__ __align__(16) float buf[2][kSeqChunk];
+    const int lane = threadIdx.x;
+    const int64_t nch = (n + kSeqChunk - 1) / kSeqChunk;
+    pdl_enter();
+    auto issue = [&](int64_t c) {
+        const int64_t base = c * kSeqChunk;
+        const int cnt = (int)min((int64_t)kSeqChunk, n - base);
+        float *b = buf[c & 1];
+        for (int j = lane; j < cnt; j += 32) {
+            const uint32_t sa = (uint32_t)__cvta_generic_to_shared(b + j);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(in + base + j) : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    float s = lane == 0 ? *acc : 0.0f;
+    if (nch > 0) issue(0);
+    for (int64_t c = 0; c < nch; ++c) {
+        if (c + 1 < nch) issue(c + 1);
+        else asm volatile("cp.async.commit_group;" ::: "memory");
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+        __syncwarp();  // every lane's copies of chunk c are visible to lane 0
+        if (lane == 0) {
+            const float *b = buf[c & 1];
+            const int cnt = (int)min((int64_t)kSeqChunk, n - c * kSeqChunk);
+            int j = 0;
+            for (; j + 4 <= cnt; j += 4) {
+                const float4 v = *reinterpret_cast<const float4 *>(b + j);
+                s = __fadd_rn(s, v.x);
+                s = __fadd_rn(s, v.y);
+                s = __fadd_rn(s, v.z);
+                s = __fadd_rn(s, v.w);
+            }
+            for (; j < cnt; ++j) s = __fadd_rn(s, b[j]);
+        }
+        __syncwarp();  // lane 0 is done with buf[c & 1] before chunk c + 2 refills it
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    if (lane == 0) *acc = s;
+}
+
+int launch_seq_sum_f32(const float *in, int64_t n, float *acc, int dev, cudaStream_t st) {
+    (void)dev;
+    if (n < 0) return fail(B2_ERR_INVALID, "sequential sum: negative length");
+    if ((uintptr_t)in % 4) return fail(B2_ERR_INVALID, "sequential sum: input must be 4-byte aligned");
+    B2_CUDA(launch_kernel(seq_sum_f32_kernel, dim3(1), dim3(32), 0, st, in, n, acc));
+    count_launch();
+    return B2_OK;
+}
+
 size_t reduce_ws_bytes(int64_t, int dtype, int dev) {
     size_t a = dtype == B2_I64 ? 16 : 8;  // fp32 partials are binary64
     return (size_t)max_grid(dev) * a + 64;

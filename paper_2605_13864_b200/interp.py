@@ -19,8 +19,9 @@ exact_div), and the work runs through libb200k.so's host-buffer pipelines
 Results: transposes are bit-identical to the reference; integer sums are exact
 (the reference's unbounded ints; int cells are 4 bytes, intrinsics.py:35); the
 A.5 tree-form fp32 sum is bit-identical; the naive fp32 sum (sequential order in
-the reference) is returned in the GPU's tree order, within the north-star
-tolerance (DESIGN.md "Parity").
+the reference) is returned correctly rounded from a parallel sum by default, within
+the north-star tolerance, and bit-identical with the reference
+with run_program(..., fp_order="reference") (its own sequential order, one warp).
 
 Extensions (documented deviations):
   * `Array.data` may be a numpy array (zero-copy host buffer); results are then
@@ -32,6 +33,7 @@ Extensions (documented deviations):
 """
 from __future__ import annotations
 
+import contextvars
 import struct
 from dataclasses import dataclass
 
@@ -40,6 +42,10 @@ import numpy as np
 from . import ops
 from .errors import InterpError, UnsupportedProgram
 from .recognize import Plan, recognize
+
+
+# fp_order of the Interp currently dispatching (run_program(..., fp_order=...))
+_FP_ORDER: contextvars.ContextVar = contextvars.ContextVar("b2_fp_order", default="tree")
 
 
 def f32(x: float) -> float:
@@ -195,8 +201,9 @@ class Interp:
     """run(fn_name, inputs) mirrors minigpu.interp.Interp.run (interp.py:106-128)."""
 
     BACKENDS = ("auto", "kernels", "codegen")
+    FP_ORDERS = ("tree", "reference")
 
-    def __init__(self, program, backend: str = "auto", check=None):
+    def __init__(self, program, backend: str = "auto", check=None, fp_order: str = "tree"):
         """backend: "kernels" = only the hand-written kernels (recognised
         programs); "codegen" = compile any GPU-form program (codegen.py);
         "auto" = kernels when the program is recognised, else codegen.
@@ -205,6 +212,9 @@ class Interp:
         such as minigpu.checker.check_program."""
         if backend not in self.BACKENDS:
             raise ValueError(f"backend must be one of {self.BACKENDS}")
+        if fp_order not in self.FP_ORDERS:
+            raise ValueError(f"fp_order must be one of {self.FP_ORDERS}")
+        self.fp_order = fp_order
         self.program = program
         self.backend = backend
         self.check = check
@@ -215,7 +225,11 @@ class Interp:
         if self.backend != "codegen":
             try:
                 plan = recognize(self.program, fn_name)
-                return _EXEC[(plan.kind, plan.form)](plan, env)
+                token = _FP_ORDER.set(self.fp_order)
+                try:
+                    return _EXEC[(plan.kind, plan.form)](plan, env)
+                finally:
+                    _FP_ORDER.reset(token)
             except UnsupportedProgram:
                 if self.backend == "kernels":
                     raise
@@ -259,13 +273,18 @@ class Interp:
         return self._dispatch(fn, fn_name, env, arrays), arrays
 
 
-def run_program(program, entry: str, inputs: dict, backend: str = "auto", check=None):
+def run_program(program, entry: str, inputs: dict, backend: str = "auto", check=None,
+                fp_order: str = "tree"):
     """Returns (return value, {param name: flat final array data}) (interp.py:380-387).
 
     List-backed arrays come back as fresh lists; numpy-backed arrays come back
     as the (mutated) numpy buffer itself. `backend` selects hand-written kernels
-    and/or generated code, `check` an optional pre-dispatch gate (see Interp)."""
-    it = Interp(program, backend, check)
+    and/or generated code, `check` an optional pre-dispatch gate (see Interp).
+    `fp_order` for the naive fp32 sum (A.2): "tree" (default) returns the correctly
+    rounded sum computed in parallel (binary64 accumulation; within the north-star
+    tolerance of the reference's value), "reference" the reference's own sequential
+    binary32 order, bit-identical with its result (one warp on the device)."""
+    it = Interp(program, backend, check, fp_order)
     ret, arrays = it.run(entry, dict(inputs))
     out = {k: (a.data if isinstance(a.data, np.ndarray) else list(a.data))
            for k, a in arrays.items()}
@@ -439,6 +458,8 @@ def _exec_reduce_naive(plan: Plan, env):
         raise InterpError(f"index {arr.dims[0]} out of bounds 0..{arr.dims[0]}")
     x = _cells(arr, N, cell)
     if cell == "float":
+        if _FP_ORDER.get() == "reference":  # the interpreter's own order, bit for bit
+            return ("ret", ops.reduce_sum_sequential(np.ascontiguousarray(x)))
         return ("ret", float(np.float32(ops.reduce_sum(np.ascontiguousarray(x)))))
     if x.dtype not in (np.int32, np.int64):
         raise InterpError("int cell value outside the 64-bit range (cells beyond int64 are "

@@ -155,6 +155,33 @@ def reduce_sum(arr, *, out=None, ws=None, stream=None):
     return _int128(res) if words == 2 else res[0].item()
 
 
+def reduce_sum_sequential(arr, *, out=None, stream=None):
+    """The naive fp32 program A.2 in the reference's own order (interp.py:262-270:
+    `sum += arr[i]`, one binary32 rounding per cell, i ascending) — bit-identical with
+    the reference interpreter, where `reduce_sum` returns the correctly rounded sum.
+    Inherently sequential (one warp, ~4 cycles per cell). float32 1-D input.
+
+    Device: returns a 1-element float32 CUDA tensor (async; `out`, if given, is
+    overwritten with the sum). Host: returns a Python float."""
+    arr, out = _as_device(arr), _as_device(out)
+    if b2_dtype(arr) != _lib.F32:
+        raise TypeError("sequential sum: dtype must be float32")
+    if _is_torch_cuda(arr):
+        if arr.dim() != 1 or (arr.numel() and arr.stride(0) != 1):
+            raise ValueError("sequential sum: input must be a contiguous 1-D tensor")
+        if out is None:
+            out = torch.zeros(1, dtype=torch.float32, device=arr.device)
+        else:
+            out.zero_()
+        check(lib().b2_reduce_sum_seq_f32(arr.data_ptr(), arr.numel(), out.data_ptr(), arr.device.index,
+                                          _stream_ptr(arr, stream)))
+        return out
+    a = np.ascontiguousarray(arr, dtype=np.float32).reshape(-1)
+    res = np.zeros(1, dtype=np.float32)
+    check(lib().b2_reduce_sum_seq_f32_host(a.ctypes.data, a.size, res.ctypes.data, _host_device()))
+    return float(res[0])
+
+
 def int128(t) -> int:
     """Python int of a device int64-sum result tensor (lo, hi words)."""
     return _int128(t.cpu().numpy() if hasattr(t, "cpu") else t)

@@ -192,6 +192,20 @@ def run_reduce(rng):
         dfree(p)
         dfree(ws)
         dfree(outp)
+    # the naive fp32 program in the reference's order (one warp, 4-byte cp.async ring),
+    # device entry on a misaligned view and the chunked host entry; bit-exact
+    for n in [0, 1, 5, 2048, 2049, 10007]:
+        xf = rng.uniform(-1, 1, n + 1).astype(np.float32)
+        want = np.cumsum(xf[1:], dtype=np.float32)[-1] if n else np.float32(0)
+        p = h2d(xf)
+        acc = h2d(np.zeros(1, np.float32))
+        check(L.b2_reduce_sum_seq_f32(p + 4, n, acc, DEV, None))
+        assert d2h(acc, np.zeros(1, np.float32))[0].view(np.uint32) == want.view(np.uint32), n
+        res = np.zeros(1, np.float32)
+        check(L.b2_reduce_sum_seq_f32_host(xf[1:].ctypes.data, n, res.ctypes.data, DEV))
+        assert res[0].view(np.uint32) == want.view(np.uint32), n
+        dfree(p)
+        dfree(acc)
     # every reduce variant
     x = rng.integers(-2**31, 2**31, 300_001, dtype=np.int64).astype(np.int32)
     p = h2d(x)

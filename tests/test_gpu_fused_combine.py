@@ -1,5 +1,5 @@
-"""Fused cross-GPU combine (b2_reduce_sum_fused) with two processes. This pool
-grants one GPU, so both ranks share cuda:0: the mailbox still crosses a process
+"""Fused cross-GPU combine (b2_reduce_sum_fused) with two, four and eight processes. This
+pool grants one GPU, so all ranks share cuda:0: the mailbox still crosses a process
 boundary through a CUDA IPC mapping and the release/acquire protocol, the epoch
 window and the bounded waits run exactly as across NVLink (the two contexts are
 time-sliced, so this checks correctness, not speed). No barriers between the
@@ -61,19 +61,22 @@ def _worker(rank, world, port, q):
     dist.destroy_process_group()
 
 
-def test_fused_combine_two_processes():
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_fused_combine_processes(world):
+    """2, 4 and 8 ranks (the 8-GPU step's mailbox has one slot per rank and a window of
+    epochs; more writers exercise the slot rows and the root's rank-order sum)."""
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    ps = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    ps = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in ps:
         p.start()
     for p in ps:
         p.join(300)
         assert p.exitcode == 0
-    res = dict(q.get() for _ in range(2))
-    assert res[0] and res[1]
+    res = dict(q.get() for _ in range(world))
+    assert all(res[r] for r in range(world))
 
 
 def test_timeout_does_not_poison_later_epochs():
